@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the FTK critical-point tracking hot path on B200 (bench contract: ONE JSON line).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one full `track` call (all SURVEY.md 8(a) rows: closed-form mesh, fused quantize/gradient
+prefilter, exact SoS test, location/type, compaction, link, union-find, labels) over one batch of
+synthetic input already resident in HBM.  Metric (BASELINE.json): spacetime faces tested per second
+(every face gets a definitive classification), plus the K1 extraction kernel's fraction of the
+measured HBM roofline.
+
+N = 1: workload C2 (2D woven 1024 x 1024 x 256, BASELINE.json configs[1]).
+N > 1: weak scaling -- every rank owns a C2-sized time slab (256 timesteps + one ghost plane) of a
+global woven field with 256*N timesteps; trajectories are stitched across slabs (NCCL).
+
+--impl reference: the CPU oracle (oracle/, plain C + OpenMP, never tuned) on this box's host cores,
+same metric and config, each step a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spacetime faces tested/sec"
+UNIT = "faces/s"
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _ncu_traffic(config_name: str):
+    """dram bytes per K1 launch from the committed ncu --set full summary, if present"""
+    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config_name)
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, seconds_budget: float = 20.0):
+    """The oracle, as it stands, on the host cores: track on a bounded sample of the workload
+    (full spatial plane, first nt_s timesteps as its own domain).  Returns a dict."""
+    import oracle
+    import ftk_inputs as fi
+    import paper_2011_08697_b200 as ftk
+
+    nx, ny = cfg.shape[0], cfg.shape[1]
+    nt_s = 3
+    w = cfg.make()
+    f = w.generate(nt=nt_s).numpy()
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+    dt = time.perf_counter() - t
+    return {"value": nf / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle track (plain C, OpenMP {cores} threads) on {nx}x{ny}x{nt_s} timesteps of {cfg.name} "
+                      f"as its own domain: {nf} faces in {dt:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, same metric/config, bounded samples."""
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import ftk_inputs as fi
+
+    cfg = fi.CONFIGS[args.config]
+    nx, ny, nt = cfg.shape
+    cores = os.cpu_count() or 1
+    w = cfg.make()
+    # per-step sample: full rows x a band of rows x 2 timesteps, sized so the whole run ends in
+    # about two minutes
+    total_budget = 120.0
+    per_step = total_budget / max(1, args.steps + args.warmup)
+    rows = 16
+    f_full = w.generate(nt=2).numpy()
+    while True:
+        f = f_full[:, :rows, :].copy()
+        t = time.perf_counter()
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+        dt = time.perf_counter() - t
+        if dt > per_step * 0.5 or rows >= ny:
+            break
+        rows = min(ny, rows * 2)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = nf / (ms / 1000.0)
+    sample = f"oracle track on {nx}x{rows}x2 of {cfg.name} per step ({nf} faces), {cores} threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import ftk_inputs as fi
+    import paper_2011_08697_b200 as ftk
+
+    rank, world, local = _dist_env()
+    if args.gpus > 1 or world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    ftk.lib()
+
+    cfg = fi.CONFIGS[args.config]
+    nx, ny, nt = cfg.shape
+    w = cfg.make()
+    if world > 1:
+        nt_global = nt * world
+        w.nt = nt_global
+        t0 = rank * nt
+        ghost = rank < world - 1
+        nbuf = nt + (1 if ghost else 0)
+    else:
+        nt_global, t0, ghost, nbuf = nt, 0, False, nt
+    field = w.generate(t0=t0, nt=nbuf, device=dev)
+    desc = ftk.make_desc(tuple(field.shape), field.dtype, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost)
+    faces = ftk.num_faces(desc)
+    comm = None  # multi-GPU stitch: see paper_2011_08697_b200/dist.py (labels local without it)
+
+    stream = torch.cuda.current_stream(dev)
+    ftk.set_profiling(True)
+    rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, return_buffers=True)
+    n_punct = rec.shape[0]
+    # warmup
+    for _ in range(args.warmup):
+        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    k1_ms, p2_ms = [], []
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+            ms4, st3 = ftk.last_timings()
+            k1_ms.append(ms4[0])
+            p2_ms.append(ms4[1])
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    ms_total = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        ft = torch.tensor([faces], device=dev, dtype=torch.float64)
+        dist.all_reduce(ft)
+        total_faces = float(ft.item())
+    else:
+        total_faces = float(faces)
+    ms_step = ms_total / args.steps
+    value = total_faces / (ms_step / 1000.0)
+
+    # roofline of the dominant kernel (K1): algorithmic bytes = field read once + records written
+    esz = field.element_size()
+    k1_avg = sum(k1_ms) / len(k1_ms)
+    alg_bytes = field.numel() * esz + n_punct * ftk.RECORD_BYTES
+    achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
+    peak, peak_src = _peaks()
+    traffic = _ncu_traffic(cfg.name)
+
+    # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host = field.cpu().pin_memory()
+        out_host = torch.empty(buf.capacity * ftk.RECORD_BYTES, dtype=torch.uint8).pin_memory()
+        stage = torch.empty_like(field)
+        n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host)  # warm
+        e_steps = max(3, min(args.steps, 20))
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        for _ in range(e_steps):
+            n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host)
+        e_ms = (time.perf_counter() - t) * 1000.0 / e_steps
+        e2e = {"value": faces / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": field.numel() * esz, "d2h_bytes_per_step": n * ftk.RECORD_BYTES + 64}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}" + (f", {world} time slabs of {nt} + ghost" if world > 1 else ""),
+                   "grid": [nx, ny, nt_global], "faces_per_step": int(total_faces),
+                   "punctured_per_step": int(n_punct), "input": f"{field.dtype}".replace("torch.", ""),
+                   "arith": "exact int64/int128 predicates, fixed-order f64 location/type, f32 prefilter",
+                   "l2": "input (%.2f GB) larger than L2 (126 MB); no flush" % (field.numel() * esz / 1e9),
+                   "k1_ms": k1_avg, "pass2_ms": sum(p2_ms) / len(p2_ms)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "k_extract2d (K1)", "alg_bytes_per_launch": alg_bytes},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": 4 * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,153 @@
+/*
+ * ftk_cp.h -- C-ABI of the B200-native FTK critical-point tracking hot path.
+ *
+ * Method: Guo et al., "FTK: A Simplicial Spacetime Meshing Framework for Robust and Scalable
+ * Feature Tracking", arXiv 2011.08697 (PAPER.md = /root/reference/PAPER.md, cited "P:<line>").
+ *
+ * Problem: a time-varying scalar field f on a regular nx x ny [x nz] grid, nt
+ * timesteps.  Its gradient g (central differences) is piecewise linear on the Kuhn
+ * (Freudenthal) subdivision of the (n+1)-D spacetime grid.  A spacetime critical point
+ * is a zero of g; the zeros form trajectories.  Two-pass algorithm (Alg. 1 left,
+ * P:350-369): pass 1 tests every n-simplex ("face") for a zero with an exact Simulation-of-
+ * Simplicity point-in-simplex predicate on int64 fixed-point values, and gives each
+ * punctured face its barycentric location (Eq. 2) and Hessian type; pass 2
+ * joins the punctured faces of every (n+1)-simplex ("cell") by union-find.
+ *
+ * Every entry point returns an ftk_status (0 = FTK_OK).  No entry point allocates device memory
+ * on the hot path; the caller owns every buffer it passes and nothing is retained after return.
+ * All device work is enqueued on `stream`; the calls return after the result count is known
+ * (one device->host read at the end), i.e. they are synchronous with respect to `stream`.
+ * Results are deterministic: the SET of records and every field of each record depend only on the
+ * input bytes and the descriptor (not on scheduling, tiling, or the number of GPUs); the ORDER of
+ * records is unspecified unless FTK_SORTED is set.
+ */
+#ifndef FTK_CP_H
+#define FTK_CP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FTK_API __attribute__((visibility("default")))
+#else
+#define FTK_API
+#endif
+
+typedef enum {
+  FTK_OK = 0,
+  FTK_ERR_INVALID_ARG = 1, /* bad descriptor / null pointer / workspace too small */
+  FTK_ERR_RANGE = 2,       /* some |q| = |rint(f * 2^s)| >= 2^59 (2D) or 2^38 (3D), or a non-
+                              finite input: the exact integer predicates could overflow */
+  FTK_ERR_CAPACITY = 3,    /* more records than `capacity`: *n_out = required count, contents
+                              unspecified; the call is idempotent, retry with a larger buffer */
+  FTK_ERR_CUDA = 4,        /* a CUDA runtime error (message via ftk_last_error()) */
+  FTK_ERR_NCCL = 5,        /* an NCCL error in the multi-GPU stitch */
+  FTK_ERR_INVARIANT = 6,   /* a cell with a punctured-face count not in {0, 2}; impossible under
+                              SoS, so this signals a bug */
+  FTK_ERR_NOMEM = 7
+} ftk_status;
+
+typedef enum { FTK_F32 = 0, FTK_F64 = 1 } ftk_dtype;
+
+/* Critical point types (for a gradient field, maxima, minima and saddles). */
+typedef enum {
+  FTK_CP_DEGENERATE = 0, /* singular interpolated Hessian (exact zero determinant) */
+  FTK_CP_MIN = 1,
+  FTK_CP_SADDLE = 2,  /* 2D saddle */
+  FTK_CP_SADDLE1 = 3, /* 3D, Morse index 1 (one negative eigenvalue) */
+  FTK_CP_SADDLE2 = 4, /* 3D, Morse index 2 */
+  FTK_CP_MAX = 5
+} ftk_cp_type;
+
+/* ftk_desc.flags */
+#define FTK_GHOST_PLANE 1u      /* the buffer's last plane is a read-only ghost (time slab):
+                                   faces anchored on it are tested for linking but not returned */
+#define FTK_SORTED 2u           /* return records sorted by face_id */
+
+/* ftk_cp.flags */
+#define FTK_CP_ORDINAL 1u       /* all vertices in one timestep */
+#define FTK_CP_BOUNDARY 2u      /* face shared by fewer than two cells (domain boundary) */
+#define FTK_CP_DEGENERATE_LOC 4u /* sum of barycentric numerators == 0: location = centroid */
+
+typedef struct {
+  int32_t ndim;        /* spatial dimension n: 2 or 3 */
+  int32_t dtype;       /* ftk_dtype of the field; layout dense row-major [t][z][y][x], x fastest */
+  int64_t n[3];        /* nx, ny, nz; nz = 1 when ndim == 2; every spatial extent >= 3 */
+  int64_t nt;          /* planes in the buffer (incl. the ghost plane when FTK_GHOST_PLANE) >= 1 */
+  int64_t t0;          /* global timestep of the buffer's first plane (0 on a single GPU) */
+  int64_t nt_global;   /* global number of timesteps; t0 + nt <= nt_global */
+  int32_t scale_log2;  /* fixed point: q = rint(f * 2^scale_log2), round-half-even; [-64, 64] */
+  uint32_t flags;      /* FTK_GHOST_PLANE | FTK_SORTED */
+} ftk_desc;
+
+/* One punctured face (56 bytes). */
+typedef struct {
+  int64_t face_id;     /* I(anchor) * T + type; I = x + nx*(y + ny*(z + nz*t)) with global t;
+                          T = 12 (2D+t) or 60 (3D+t) face types of the Kuhn cube */
+  int64_t label;       /* trajectory id = the minimum face_id of its component; -1 from extract */
+  double x, y, z, t;   /* spacetime location in grid units, t in global timesteps (z = 0 in 2D) */
+  int32_t type;        /* ftk_cp_type */
+  uint32_t flags;      /* FTK_CP_ORDINAL | FTK_CP_BOUNDARY | FTK_CP_DEGENERATE_LOC */
+} ftk_cp;
+
+typedef struct CUstream_st* ftk_stream; /* == cudaStream_t; NULL = legacy default stream */
+typedef struct ftk_comm ftk_comm;       /* opaque multi-GPU communicator (NCCL) */
+
+FTK_API int ftk_abi_version(void);
+FTK_API const char* ftk_strerror(int status);
+/* last CUDA/NCCL error text of the calling thread (empty if none) */
+FTK_API const char* ftk_last_error(void);
+
+/* Number of faces this buffer OWNS (anchors t in [t0, t0 + nt - ghost)): the faces every call
+ * classifies; used for the faces/s metric.  Host-only arithmetic. */
+FTK_API int ftk_num_faces(const ftk_desc* desc, int64_t* n_faces);
+
+/* Device workspace needed by extract/track for up to `capacity` records. */
+FTK_API int ftk_workspace_size(const ftk_desc* desc, int64_t capacity, size_t* bytes);
+
+/* Pass 1: test every owned face, write the punctured ones to d_out[0 .. *n_out)
+ * (label = -1).  d_field: device pointer to the buffer; d_out: device array of `capacity`
+ * records; d_ws: device workspace of ws_bytes >= ftk_workspace_size(). */
+FTK_API int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                   int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream);
+
+/* Pass 1 + pass 2: as extract, then join the punctured faces of every cell with a
+ * lock-free union-find and label each record with its trajectory's minimum face_id.  With a
+ * communicator (time slabs, one process per GPU): every rank passes its slab with one ghost plane
+ * (FTK_GHOST_PLANE on all but the last rank), returns only the records it owns, and the labels
+ * are global (identical to a single-GPU run).  comm = NULL: single GPU. */
+FTK_API int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                 int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream, ftk_comm* comm);
+
+/* End-to-end variant from HOST memory: h_field is a host buffer (pinned for overlap) of the whole
+ * input; the library streams it to d_stage (device buffer of the field's size) in time chunks,
+ * overlapping the copies with pass 1, runs track, and copies the records to h_out (host array of
+ * `capacity` records). */
+FTK_API int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, ftk_cp* d_out,
+                      ftk_cp* h_out, int64_t capacity, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                      ftk_stream stream);
+
+/* Per-phase device times (ms) of the last extract/track call on this thread, measured with CUDA
+ * events on `stream` when profiling is enabled: [0] pass 1 (K1 extraction kernel), [1] pass 2
+ * (hash + link + union-find + labels), [2] slab stitch, [3] whole call.  Also the survivor
+ * statistics of the last call: stats[0] = faces tested (owned), stats[1] = cubes surviving the
+ * sign prefilter, stats[2] = punctured faces. */
+FTK_API int ftk_set_profiling(int enable);
+FTK_API int ftk_last_timings(float* ms4, int64_t* stats3);
+
+/* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
+ * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
+FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);
+FTK_API int ftk_comm_init(ftk_comm** comm, int rank, int world, const uint8_t id[128]);
+FTK_API int ftk_comm_destroy(ftk_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTK_CP_H */

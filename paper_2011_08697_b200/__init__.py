@@ -1,0 +1,229 @@
+"""B200-native FTK critical-point tracking: thin Python binding of the C-ABI (include/ftk_cp.h).
+
+Argument marshalling only -- every step of the path runs in the CUDA kernels of libftk_cp.so.
+PyTorch provides device memory and the current stream.  There is no CPU fallback: if the library
+is missing or no GPU is present, calls raise.
+
+    import paper_2011_08697_b200 as ftk
+    rec = ftk.track(field_cuda, scale_log2=26)      # torch.int64 [n, 7] on the device
+    arr = ftk.to_numpy(rec)                         # structured numpy view (face_id, label, x..t, type, flags)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libftk_cp.so")
+
+OK, ERR_INVALID_ARG, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_INVARIANT, ERR_NOMEM = range(8)
+F32, F64 = 0, 1
+DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX = range(6)
+GHOST_PLANE, SORTED = 1, 2
+CP_ORDINAL, CP_BOUNDARY, CP_DEGENERATE_LOC = 1, 2, 4
+
+RECORD_DTYPE = np.dtype(
+    [("face_id", "<i8"), ("label", "<i8"), ("x", "<f8"), ("y", "<f8"), ("z", "<f8"), ("t", "<f8"),
+     ("type", "<i4"), ("flags", "<u4")]
+)
+RECORD_BYTES = 56
+assert RECORD_DTYPE.itemsize == RECORD_BYTES
+
+EXPORTS = [
+    "ftk_abi_version", "ftk_strerror", "ftk_last_error", "ftk_num_faces", "ftk_workspace_size",
+    "ftk_cp_extract", "ftk_cp_track", "ftk_cp_track_host", "ftk_set_profiling", "ftk_last_timings",
+    "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy",
+]
+
+
+class FtkError(RuntimeError):
+    def __init__(self, status: int, what: str, detail: str = ""):
+        msg = f"{what}: status {status}"
+        if _lib is not None:
+            msg += f" ({_lib.ftk_strerror(status).decode()})"
+        if detail:
+            msg += f": {detail}"
+        super().__init__(msg)
+        self.status = status
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [
+        ("ndim", ctypes.c_int32), ("dtype", ctypes.c_int32), ("n", ctypes.c_int64 * 3),
+        ("nt", ctypes.c_int64), ("t0", ctypes.c_int64), ("nt_global", ctypes.c_int64),
+        ("scale_log2", ctypes.c_int32), ("flags", ctypes.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libftk_cp.so (built by __graft_entry__.build() / paper_2011_08697_b200/build.py)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FtkError(-1, f"{LIB_PATH} is missing; run python paper_2011_08697_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, PD = ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(Desc)
+        L.ftk_strerror.restype = ctypes.c_char_p
+        L.ftk_strerror.argtypes = [ctypes.c_int]
+        L.ftk_last_error.restype = ctypes.c_char_p
+        L.ftk_num_faces.argtypes = [PD, P]
+        L.ftk_workspace_size.argtypes = [PD, I64, P]
+        L.ftk_cp_extract.argtypes = [PD, P, P, I64, P, P, ctypes.c_size_t, P]
+        L.ftk_cp_track.argtypes = [PD, P, P, I64, P, P, ctypes.c_size_t, P, P]
+        L.ftk_cp_track_host.argtypes = [PD, P, P, P, P, I64, P, P, ctypes.c_size_t, P]
+        L.ftk_set_profiling.argtypes = [ctypes.c_int]
+        L.ftk_last_timings.argtypes = [P, P]
+        L.ftk_comm_get_unique_id.argtypes = [P]
+        L.ftk_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+        L.ftk_comm_destroy.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+def make_desc(shape, dtype, scale_log2: int, t0: int = 0, nt_global: int | None = None,
+              ghost: bool = False, sorted_output: bool = False) -> Desc:
+    """shape: [t][y][x] (2D) or [t][z][y][x] (3D)."""
+    d = Desc()
+    if len(shape) == 3:
+        nt, ny, nx = shape
+        nz, d.ndim = 1, 2
+    elif len(shape) == 4:
+        nt, nz, ny, nx = shape
+        d.ndim = 3
+    else:
+        raise ValueError("field must be [t][y][x] or [t][z][y][x]")
+    if dtype in (torch.float32, np.float32):
+        d.dtype = F32
+    elif dtype in (torch.float64, np.float64):
+        d.dtype = F64
+    else:
+        raise TypeError(f"unsupported field dtype {dtype}")
+    d.n[0], d.n[1], d.n[2] = nx, ny, nz
+    d.nt, d.t0 = nt, t0
+    d.nt_global = t0 + nt if nt_global is None else nt_global
+    d.scale_log2 = scale_log2
+    d.flags = (GHOST_PLANE if ghost else 0) | (SORTED if sorted_output else 0)
+    return d
+
+
+def num_faces(desc: Desc) -> int:
+    n = ctypes.c_int64(0)
+    _check(lib().ftk_num_faces(ctypes.byref(desc), ctypes.byref(n)), "ftk_num_faces")
+    return n.value
+
+
+def workspace_size(desc: Desc, capacity: int) -> int:
+    b = ctypes.c_size_t(0)
+    _check(lib().ftk_workspace_size(ctypes.byref(desc), capacity, ctypes.byref(b)), "ftk_workspace_size")
+    return b.value
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise FtkError(status, what, lib().ftk_last_error().decode())
+
+
+def default_capacity(field: torch.Tensor) -> int:
+    return max(1 << 16, field.numel() // 64)
+
+
+@dataclass
+class Buffers:
+    """Caller-owned device buffers (records + workspace), reusable across calls."""
+    records: torch.Tensor     # uint8 [capacity * 56]
+    workspace: torch.Tensor   # uint8
+    capacity: int
+
+    @staticmethod
+    def allocate(desc: Desc, capacity: int, device) -> "Buffers":
+        ws = workspace_size(desc, capacity)
+        return Buffers(torch.empty(max(capacity, 1) * RECORD_BYTES, dtype=torch.uint8, device=device),
+                       torch.empty(ws, dtype=torch.uint8, device=device), capacity)
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global, capacity, ghost,
+         buffers: Buffers | None, comm=None, sorted_output=False):
+    if not field.is_cuda:
+        raise FtkError(ERR_INVALID_ARG, f"{fn_name}: field must be a CUDA tensor (no CPU fallback)")
+    if not field.is_contiguous():
+        field = field.contiguous()
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost, sorted_output)
+    cap = capacity if capacity is not None else (buffers.capacity if buffers else default_capacity(field))
+    while True:
+        if buffers is None or buffers.capacity < cap:
+            buffers = Buffers.allocate(desc, cap, field.device)
+        n_out = ctypes.c_int64(0)
+        args = [ctypes.byref(desc), ctypes.c_void_p(field.data_ptr()), ctypes.c_void_p(buffers.records.data_ptr()),
+                buffers.capacity, ctypes.byref(n_out), ctypes.c_void_p(buffers.workspace.data_ptr()),
+                buffers.workspace.numel(), ctypes.c_void_p(_stream_ptr(field.device))]
+        if fn_name == "ftk_cp_track":
+            args.append(comm)
+        st = getattr(lib(), fn_name)(*args)
+        if st == ERR_CAPACITY:
+            cap = int(n_out.value * 1.25) + 1024
+            buffers = None
+            continue
+        _check(st, fn_name)
+        rec = buffers.records[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
+        return rec, buffers
+
+
+def extract(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
+            capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
+            return_buffers: bool = False):
+    """Pass 1: punctured faces of the buffer's owned timesteps (label = -1).
+    Returns an int64 [n, 7] device tensor of 56-byte records (see RECORD_DTYPE)."""
+    rec, buf = _run("ftk_cp_extract", field, scale_log2, t0, nt_global, capacity, ghost, buffers)
+    return (rec, buf) if return_buffers else rec
+
+
+def track(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
+          capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
+          comm=None, return_buffers: bool = False):
+    """Pass 1 + pass 2: punctured faces labelled with their trajectory (min face_id)."""
+    rec, buf = _run("ftk_cp_track", field, scale_log2, t0, nt_global, capacity, ghost, buffers, comm)
+    return (rec, buf) if return_buffers else rec
+
+
+def track_host(field_host: torch.Tensor, scale_log2: int, stage: torch.Tensor, buffers: Buffers,
+               out_host: torch.Tensor):
+    """End-to-end from host memory (pinned for speed): H2D inside the call, records copied back to
+    out_host (uint8 [capacity * 56], pinned).  Returns the record count."""
+    desc = make_desc(tuple(field_host.shape), field_host.dtype, scale_log2)
+    n_out = ctypes.c_int64(0)
+    st = lib().ftk_cp_track_host(
+        ctypes.byref(desc), ctypes.c_void_p(field_host.data_ptr()), ctypes.c_void_p(stage.data_ptr()),
+        ctypes.c_void_p(buffers.records.data_ptr()), ctypes.c_void_p(out_host.data_ptr()), buffers.capacity,
+        ctypes.byref(n_out), ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
+        ctypes.c_void_p(_stream_ptr(stage.device)))
+    _check(st, "ftk_cp_track_host")
+    return n_out.value
+
+
+def to_numpy(rec: torch.Tensor) -> np.ndarray:
+    """Copy device records to a structured numpy array (RECORD_DTYPE)."""
+    a = rec.detach().cpu().contiguous().numpy()
+    return a.view(np.uint8).view(RECORD_DTYPE).reshape(-1)
+
+
+def set_profiling(enable: bool):
+    lib().ftk_set_profiling(1 if enable else 0)
+
+
+def last_timings():
+    """(ms[4]: pass1, pass2, stitch, call; stats[3]: faces, prefilter survivors, punctured)"""
+    ms = (ctypes.c_float * 4)()
+    st = (ctypes.c_int64 * 3)()
+    lib().ftk_last_timings(ms, st)
+    return list(ms), list(st)

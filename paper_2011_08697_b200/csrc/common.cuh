@@ -1,0 +1,66 @@
+// common.cuh -- device/host helpers shared by the FTK B200 kernels (product path only).
+//
+// Nothing here is shared with oracle/ (the CPU oracle is independent test infrastructure).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ftk_cp.h"
+
+namespace ftk {
+
+using i64 = long long;
+using u64 = unsigned long long;
+using i128 = __int128;
+using u128 = unsigned __int128;
+
+// Workspace counters (u64 each), zeroed at the start of every call.
+enum Counter : int {
+  CNT_NOUT = 0,       // punctured faces found (may exceed capacity)
+  CNT_SURVIVORS = 1,  // cubes surviving the sign prefilter
+  CNT_MAXBITS = 2,    // max over |f| as IEEE bits (float bits for f32, double bits for f64)
+  CNT_INVARIANT = 3,  // link: faces whose parent cell does not hold exactly one other punctured face
+  CNT_EXPORT = 4,     // slab stitch: exported boundary faces
+  CNT_N = 8
+};
+
+// Correctly rounded (round-half-even) int128 -> double; the oracle's reading of step 5
+// (R11) -- implemented independently with 64-bit conversions plus a sticky bit.
+__device__ __forceinline__ double i128_to_double_rn(i128 v) {
+  if (v == (i128)(i64)v) return __ll2double_rn((i64)v);
+  const bool neg = v < 0;
+  u128 m = neg ? (u128)0 - (u128)v : (u128)v;
+  const u64 hi = (u64)(m >> 64);
+  double d;
+  if (hi == 0) {
+    d = __ull2double_rn((u64)m);
+  } else {
+    const int k = 64 - __clzll((i64)hi);         // shift so the leading bit lands at bit 63
+    const u64 w = (u64)(m >> k);
+    const u64 sticky = ((m & (((u128)1 << k) - 1)) != 0) ? 1ull : 0ull;
+    d = __ull2double_rn(w | sticky);              // bit 0 is below the round bit (bit 10)
+    d = ldexp(d, k);                              // exact power-of-two scaling
+  }
+  return neg ? -d : d;
+}
+
+__device__ __forceinline__ int sgn128(i128 v) { return (v > 0) - (v < 0); }
+__device__ __forceinline__ int sgn64(i64 v) { return (v > 0) - (v < 0); }
+
+// Exact 2x2 determinant | ua va ; ub vb | in int128.
+__device__ __forceinline__ i128 det2(i64 ua, i64 va, i64 ub, i64 vb) {
+  return (i128)ua * vb - (i128)va * ub;
+}
+
+}  // namespace ftk
+
+#define FTK_CUDA_TRY(expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::ftk::set_cuda_error(_e, #expr); \
+  } while (0)
+
+namespace ftk {
+int set_cuda_error(cudaError_t e, const char* what);  // runtime.cu
+}

@@ -1,0 +1,28 @@
+// extract2d.cuh -- launch interface of the pass-1 extraction kernels (K1).
+#pragma once
+
+#include "common.cuh"
+
+namespace ftk {
+
+struct ExtractParams {
+  const void* field;   // device buffer [nt_buf][nz][ny][nx]
+  int dtype;           // FTK_F32 / FTK_F64
+  i64 nx, ny, nz;
+  i64 nt_buf;          // planes in the buffer
+  i64 t0;              // global timestep of plane 0
+  i64 nt_global;
+  i64 ta, tb;          // anchor timesteps (global) to test and emit: [ta, tb)
+  i64 tchunk;          // anchor timesteps per CTA
+  double scale;        // 2^s
+  double thr;          // 2^(1-s): prefilter threshold on raw field differences
+  ftk_cp* out;
+  i64 capacity;
+  unsigned long long* counters;  // Counter enum
+  bool force_generic;  // testing: disable TMA
+};
+
+int launch_extract2d(const ExtractParams& P, cudaStream_t stream);
+int launch_extract3d(const ExtractParams& P, cudaStream_t stream);
+
+}  // namespace ftk
