@@ -1,25 +1,32 @@
 // extract2d.cu -- K1: pass 1 of Alg. 1 for 2D+t on sm_100a.
 //
-// One CTA owns a 124 x 32 tile of anchors (x, y) and a chunk of anchor timesteps.  It marches t:
+// One CTA owns a 124 x 32 tile of anchors (x, y) and a chunk of anchor timesteps; it marches t.
+// Warp-specialised:
 //
-//   TMA (cp.async.bulk.tensor, mbarrier ring of NSTAGE planes) stages the plane tile with a halo
-//   (x0-4 .. x0+131, y0-2 .. y0+34) in shared memory, so every vertex is read from HBM once and
-//   reused by all 12 faces of the 8 cubes it belongs to (north_star (2)).
+//   producer warp -- TMA (cp.async.bulk.tensor) stages each plane tile with its halo
+//     (x0-4 .. x0+131, y0-2 .. y0+34) into an NSTAGE-deep shared-memory ring guarded by full/empty
+//     mbarriers: every vertex is read from HBM once and reused by all 12 faces of the 8 cubes it
+//     belongs to (north_star (2)).
 //
-//   Scan (all warps, lane = 4 consecutive x, warp = 8 rows): a CONSERVATIVE sign prefilter on the
-//   raw field values.  For gradient component g_a = q[+a] - q[-a] (q = rint(f 2^s)), the float
-//   test (f[+a] - f[-a]) >= 2^(1-s) implies g_a > 0 exactly.  Four bits
-//   per vertex (x+, x-, y+, y-) are ANDed over the 8 corners of each spacetime cube; a cube whose
-//   AND is nonzero has a gradient component of one strict sign on all corners, so no face inside
-//   it can contain the origin -- even under SoS (the perturbation is infinitesimal).  Survivors
-//   (about 0.5% of cubes on the woven field) go to a CTA queue.
+//   8 scan warps (4 anchor rows x 124 columns each; lane = 4 consecutive x, lane 31 is a halo lane)
+//     -- a CONSERVATIVE sign prefilter on raw field values.  For the gradient component
+//     g_a = q[+a] - q[-a] (q = rint(f 2^s)) the float test d = f[+a] - f[-a] >= 2^(1-s) implies
+//     g_a > 0 exactly, and d < -2^(1-s) implies g_a < 0.  The sign bits of
+//     d -+ 2^(1-s) (paired FADD2) are funnel-shifted into a 4-bit code per vertex (bit = 1: that
+//     strict sign condition does NOT hold) and ORed over the 8 corners of each spacetime cube: a
+//     nibble with a zero bit means one gradient component has one strict sign on every corner, so no
+//     face of the cube can contain the origin -- even under SoS (the perturbation is infinitesimal).
+//     For each surviving cube (~0.45% on the woven field) the warp copies its 4x4x2 window of raw
+//     values into a CTA window ring (1 LDS + 1 STS per lane) and moves on.
 //
-//   Exact stage (survivor queue, 32 cubes per warp at a time, data from shared memory): quantize,
-//   exact int64 gradients, per-face exact sign reject, SoS point-in-simplex with exact 2x2
-//   determinants (int64, or int128 when |g| >= 2^31), Eq. 2 location and the Hessian type in
-//   fixed-order FP64 (no FMA), ballot/prefix-sum compaction with one global atomic per warp batch.
+//   3 exact warps -- take the ring in batches of 32 cubes (one per lane, no divergence between
+//     cubes): exact quantization, gradients, the 19 distinct 2x2 determinants of the cube's 12 faces,
+//     SoS point-in-simplex; then the punctured faces are redistributed over the
+//     lanes and each gets its Eq. 2 location and Hessian type in fixed-order FP64 (no FMA), written
+//     with one global atomic per batch.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstring>
 #include <utility>
 
@@ -31,7 +38,7 @@ namespace ftk {
 namespace k2d {
 
 // ---------------------------------------------------------------------------------------------
-// PTX helpers: mbarrier + TMA
+// PTX helpers: mbarrier + TMA + packed fp32
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -43,18 +50,36 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  long long spins = 0;
-  while (true) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (++spins > (1ll << 26)) __trap();  // never hang the GPU on a lost transaction
-  }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count = 1) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// never hang the GPU: a wait that exceeds 2 s reports where it is stuck and traps
+__device__ unsigned long long* g_dbg_ring = nullptr;
+__device__ __noinline__ void wait_timeout(int what, int a, int b) {
+  if ((threadIdx.x & 31) == 0)
+    printf("ftk k_extract2d: wait timeout what=%d a=%d b=%d block=(%d,%d,%d) warp=%d\n", what, a, b, blockIdx.x,
+           blockIdx.y, blockIdx.z, threadIdx.x >> 5);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what = 0, int a = 0) {
+  if (mbar_try(bar, parity)) return;
+  const unsigned long long t0 = gtimer_ns();
+  while (!mbar_try(bar, parity))
+    if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
@@ -64,149 +89,128 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct f2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ f2 pack2(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ uint32_t lo32(f2 a) { return (uint32_t)a.v; }
+__device__ __forceinline__ uint32_t hi32(f2 a) { return (uint32_t)(a.v >> 32); }
+// push the sign bit of `bits` into the low end of W
+__device__ __forceinline__ uint32_t push_sign(uint32_t W, uint32_t bits) { return __funnelshift_l(bits, W, 1); }
 
 // ---------------------------------------------------------------------------------------------
-// Tile geometry
+// Tile geometry and roles
 // ---------------------------------------------------------------------------------------------
 constexpr int LX = 128;             // x positions scanned per warp row (32 lanes x 4)
-constexpr int TX = 124;             // anchors owned per CTA in x: lane 31 is a halo lane whose
-                                    // codes only complete lane 30's cubes (a cube needs x+1)
-constexpr int RW = 8;               // anchor rows per warp
-constexpr int NWARP = 4;            // warps per CTA
-constexpr int TY = RW * NWARP;      // 32 anchor rows per CTA
+constexpr int TX = 124;             // anchors owned per CTA in x: lane 31 is a halo lane whose codes
+                                    // only complete lane 30's cubes (a cube needs its x+1 corners)
+constexpr int RW = 4;               // anchor rows per scan warp
+constexpr int NSW = 8;              // scan warps
+constexpr int PRODUCER = NSW;       // warp index of the TMA producer
+constexpr int NEW = 3;              // exact warps
+constexpr int NWARPS = NSW + 1 + NEW;
+constexpr int NTHREADS = NWARPS * 32;
+constexpr int TY = RW * NSW;        // 32 anchor rows per CTA
 constexpr int XOFF = 4;             // smem column of x0
 constexpr int YOFF = 2;             // smem row of y0
 constexpr int PITCH = LX + 8;       // x0-4 .. x0+131
 constexpr int ROWS = TY + 5;        // y0-2 .. y0+34
-constexpr int NSTAGE = 4;
-constexpr int QCAP = TX * TY;       // survivor queue capacity (one plane step)
+constexpr int NSTAGE = 3;
+constexpr int NB = 8;               // window-ring batch slots (32 cubes each)
+constexpr int RING = NB * 32;
+constexpr int WSTRIDE = 33;         // values per queued window (4x4x2 = 32, odd stride: no bank conflicts)
+constexpr uint32_t META_INVALID = 0xFFFFFFFFu;
+constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
 
-// one stage = the plane tile, padded to a multiple of 128 bytes (TMA destination alignment)
 template <typename T>
-constexpr int stage_elems() {
+constexpr int stage_elems() {       // plane tile padded to a multiple of 128 bytes (TMA alignment)
   return (ROWS * PITCH * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
 }
 
 template <typename T>
 struct alignas(128) Smem {
   T plane[NSTAGE][stage_elems<T>()];
+  T win[RING * WSTRIDE];           // queued survivor windows (raw values)
+  uint32_t meta[RING];             // xl | yl << 8 | hasB << 15, or META_INVALID (padding)
+  int qt[RING];                    // anchor timestep
+  uint16_t items[NEW][MAXITEMS];   // punctured faces of a batch: entry | type << 5
   uint64_t full[NSTAGE];
-  uint16_t queue[QCAP];
-  int qn[2];
+  uint64_t empty[NSTAGE];
+  int wfill[NB];                   // entries ever written into each batch slot (monotone counter)
+  volatile int wcons[NB];          // generations of each batch slot consumed by the exact warps
+                                   // (a counter, not an mbarrier: one scan warp may reserve many
+                                   // batches ahead, so waiters can be several phases ahead)
+  int tail;                        // window-ring entries reserved so far
+  volatile int dbg_eb[NEW];        // debug: batch each exact warp is on
+  int scan_done;
+  volatile int nbatch;             // batches in total, -1 until the scan warps are done
   unsigned long long surv;
-  unsigned long long maxbits;
-};
-
-template <typename T>
-struct Bits;
-template <>
-struct Bits<float> {
-  using U = uint32_t;
-  __device__ static U absbits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
-};
-template <>
-struct Bits<double> {
-  using U = unsigned long long;
-  __device__ static U absbits(double v) { return (U)__double_as_longlong(v) & 0x7fffffffffffffffull; }
+  unsigned int maxbits32;
+  unsigned long long maxbits64;
 };
 
 // ---------------------------------------------------------------------------------------------
-// Exact stage helpers
+// Exact stage
 // ---------------------------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ i64 quant(T f, double scale) {
-  // q = rint(f * 2^s): (double)f * 2^s is exact (power-of-two scale), __double2ll_rn rounds half-even
-  return __double2ll_rn(__dmul_rn((double)f, scale));
+__device__ __forceinline__ i64 quant(float f, float scale_f, double) {
+  // f * 2^s is exact in fp32 (power-of-two scale); F2I.S64 rounds half-even
+  return __float2ll_rn(__fmul_rn(f, scale_f));
 }
-
-// SoS sign of the 2x2 determinant | ua va ; ub vb | with rows a < b (global vertex order) and
-// perturbation eps_{r,j} = eps^(2^(2r+j)) (R4).  Leading terms of det(M + E) in
-// decreasing magnitude: det, +v_b, -u_b, -v_a, then -1 (a constant: the chain always ends).
-template <bool WIDE>
-__device__ __forceinline__ int sos2(i64 ua, i64 va, i64 ub, i64 vb) {
-  int s;
-  if (WIDE) {
-    s = sgn128(det2(ua, va, ub, vb));
-  } else {
-    s = sgn64(ua * vb - va * ub);  // |g| < 2^31: |det| < 2^63
-  }
-  if (s) return s;
-  if (vb) return vb > 0 ? 1 : -1;
-  if (ub) return ub > 0 ? -1 : 1;
-  if (va) return va > 0 ? -1 : 1;
-  return -1;
-}
-
-// Point-in-simplex for the face with vertex gradients g0 < g1 < g2:
-// s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
-template <bool WIDE>
-__device__ __forceinline__ bool punctured3(const i64* g0, const i64* g1, const i64* g2) {
-  const int s0 = sos2<WIDE>(g1[0], g1[1], g2[0], g2[1]);
-  const int s1 = -sos2<WIDE>(g0[0], g0[1], g2[0], g2[1]);
-  if (s0 != s1) return false;
-  const int s2 = sos2<WIDE>(g0[0], g0[1], g1[0], g1[1]);
-  return s0 == s2;
-}
+__device__ __forceinline__ i64 quant(double f, float, double scale) { return __double2ll_rn(__dmul_rn(f, scale)); }
 
 struct Geo {
   i64 nx, ny, ntg;   // grid extents (t = global)
   i64 x0, y0;        // tile origin
+  float scale_f;
   double scale;
 };
 
 template <typename T>
-__device__ __forceinline__ i64 qs(const T* P, const Geo& G, i64 x, i64 y) {
-  return quant(P[(int)(y - G.y0 + YOFF) * PITCH + (int)(x - G.x0 + XOFF)], G.scale);
-}
+struct Win {  // W[pl*16 + r*4 + c] = f(x - 1 + c, y - 1 + r, t + pl)
+  const T* W;
+  float sf;
+  double sd;
+  __device__ __forceinline__ i64 q(int pl, int c, int r) const { return quant(W[pl * 16 + r * 4 + c], sf, sd); }
+};
 
-// exact gradient (2x the derivative; one-sided doubled at the spatial boundary, R7)
+// exact gradient (2x the derivative, one-sided doubled at the spatial boundary; R7) at
+// cube corner c (bit0 x, bit1 y, bit2 t)
 template <typename T>
-__device__ __forceinline__ void grad_exact(const T* P, const Geo& G, i64 x, i64 y, i64* g) {
-  if (x == 0) g[0] = 2 * (qs(P, G, 1, y) - qs(P, G, 0, y));
-  else if (x == G.nx - 1) g[0] = 2 * (qs(P, G, x, y) - qs(P, G, x - 1, y));
-  else g[0] = qs(P, G, x + 1, y) - qs(P, G, x - 1, y);
-  if (y == 0) g[1] = 2 * (qs(P, G, x, 1) - qs(P, G, x, 0));
-  else if (y == G.ny - 1) g[1] = 2 * (qs(P, G, x, y) - qs(P, G, x, y - 1));
-  else g[1] = qs(P, G, x, y + 1) - qs(P, G, x, y - 1);
+__device__ __forceinline__ void corner_grad(const Win<T>& w, const Geo& G, i64 x, i64 y, int c, i64& gx, i64& gy) {
+  const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
+  const i64 xc = x + cx, yc = y + cy;
+  if (xc == 0) gx = 2 * (w.q(pl, cx + 2, cy + 1) - w.q(pl, cx + 1, cy + 1));
+  else if (xc == G.nx - 1) gx = 2 * (w.q(pl, cx + 1, cy + 1) - w.q(pl, cx, cy + 1));
+  else gx = w.q(pl, cx + 2, cy + 1) - w.q(pl, cx, cy + 1);
+  if (yc == 0) gy = 2 * (w.q(pl, cx + 1, cy + 2) - w.q(pl, cx + 1, cy + 1));
+  else if (yc == G.ny - 1) gy = 2 * (w.q(pl, cx + 1, cy + 1) - w.q(pl, cx + 1, cy));
+  else gy = w.q(pl, cx + 1, cy + 2) - w.q(pl, cx + 1, cy);
 }
 
-// integer Hessian, 4x scale, stencil centre clamped into [1, N-2] (R8); xx, xy, yy
-template <typename T>
-__device__ __forceinline__ void hessian_exact(const T* P, const Geo& G, i64 x, i64 y, i64* H) {
-  const i64 cx = x < 1 ? 1 : (x > G.nx - 2 ? G.nx - 2 : x);
-  const i64 cy = y < 1 ? 1 : (y > G.ny - 2 ? G.ny - 2 : y);
-  H[0] = 4 * (qs(P, G, cx + 1, y) - 2 * qs(P, G, cx, y) + qs(P, G, cx - 1, y));
-  H[1] = qs(P, G, cx + 1, cy + 1) - qs(P, G, cx + 1, cy - 1) - qs(P, G, cx - 1, cy + 1) + qs(P, G, cx - 1, cy - 1);
-  H[2] = 4 * (qs(P, G, x, cy + 1) - 2 * qs(P, G, x, cy) + qs(P, G, x, cy - 1));
-}
-
-__device__ __forceinline__ double fma_free_dot3(const double* mu, double a, double b, double c) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(mu[0], a), __dmul_rn(mu[1], b)), __dmul_rn(mu[2], c));
-}
-
-// one face type, compile-time masks (the 12 canonical 2D+t types, kuhn.cuh)
-template <int TY, bool WIDE>
-__device__ __forceinline__ void face_test(const i64 (&g)[8][2], uint32_t exists, uint32_t& pmask) {
-  constexpr int m1 = kKuhn3.masks[TY][0];
-  constexpr int m2 = kKuhn3.masks[TY][1];
-  if (((exists >> m2) & 1) == 0) return;  // the span's far corner must exist
-  const i64* g0 = g[0];
-  const i64* g1 = g[m1];
-  const i64* g2 = g[m2];
-  // exact per-face reject: a component of one strict sign on all three vertices
-  bool rej = false;
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-    rej |= (g0[j] > 0 && g1[j] > 0 && g2[j] > 0) || (g0[j] < 0 && g1[j] < 0 && g2[j] < 0);
-  if (rej) return;
-  if (punctured3<WIDE>(g0, g1, g2)) pmask |= 1u << TY;
-}
-
-template <bool WIDE, int... TY>
-__device__ __forceinline__ void all_faces(const i64 (&g)[8][2], uint32_t exists, uint32_t& pmask,
-                                          std::integer_sequence<int, TY...>) {
-  (face_test<TY, WIDE>(g, exists, pmask), ...);
+// SoS sign of | ua va ; ub vb | (rows a < b in global vertex order) given its exact value d;
+// perturbation eps_{r,j} = eps^(2^(2r+j)) (R4): the leading terms of det(M + E) in
+// decreasing magnitude are det, +v_b, -u_b, -v_a, then the constant -1.
+__device__ __forceinline__ int sos_sign(int ds, i64 ua, i64 va, i64 ub, i64 vb) {
+  if (ds) return ds;
+  if (vb) return vb > 0 ? 1 : -1;
+  if (ub) return ub > 0 ? -1 : 1;
+  if (va) return va > 0 ? -1 : 1;
+  return -1;
 }
 
 template <int K>
@@ -219,47 +223,177 @@ __device__ __forceinline__ void masks_of(int ty, int& m1, int& m2, std::integer_
   ((ty == K ? (m1 = Face3<K>::m1, m2 = Face3<K>::m2, 0) : 0), ...);
 }
 
-// g[c] for a runtime corner index without dynamic register indexing
-__device__ __forceinline__ void sel_corner(const i64 (&g)[8][2], int c, i64* out) {
-  out[0] = g[0][0];
-  out[1] = g[0][1];
-#pragma unroll
-  for (int k = 1; k < 8; ++k)
-    if (c == k) {
-      out[0] = g[k][0];
-      out[1] = g[k][1];
-    }
+// Face test from precomputed determinant signs: point-in-simplex for the face
+// (0, m1, m2): s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
+template <int K>
+__device__ __forceinline__ void face_test(const i64 (&g)[8][2], const int (&s0k)[8], const int (&sp)[12],
+                                          uint32_t exists, uint32_t& pmask) {
+  constexpr int m1 = Face3<K>::m1, m2 = Face3<K>::m2;
+  if (((exists >> m2) & 1) == 0) return;  // the span's far corner must exist
+  const int s0 = sos_sign(sp[K], g[m1][0], g[m1][1], g[m2][0], g[m2][1]);
+  const int s1 = -sos_sign(s0k[m2], g[0][0], g[0][1], g[m2][0], g[m2][1]);
+  const int s2 = sos_sign(s0k[m1], g[0][0], g[0][1], g[m1][0], g[m1][1]);
+  if (s0 == s1 && s1 == s2) pmask |= 1u << K;
+}
+template <int... K>
+__device__ __forceinline__ void all_faces(const i64 (&g)[8][2], const int (&s0k)[8], const int (&sp)[12],
+                                          uint32_t exists, uint32_t& pmask, std::integer_sequence<int, K...>) {
+  (face_test<K>(g, s0k, sp, exists, pmask), ...);
+}
+template <bool WIDE>
+__device__ __forceinline__ int det_sign(const i64* a, const i64* b) {
+  if (WIDE) return sgn128(det2(a[0], a[1], b[0], b[1]));
+  return sgn64(a[0] * b[1] - a[1] * b[0]);  // |g| < 2^31: |det| < 2^63
+}
+template <bool WIDE, int... K>
+__device__ __forceinline__ void pair_signs(const i64 (&g)[8][2], int (&sp)[12], std::integer_sequence<int, K...>) {
+  ((sp[K] = det_sign<WIDE>(g[Face3<K>::m1], g[Face3<K>::m2])), ...);
 }
 
-// Process one surviving cube anchored at (x, y, t): test its 12 faces exactly and write records.
-// A = plane t, B = plane t+1 (nullptr when t is the last global timestep).  All lanes of the warp
-// call this together (valid = false lanes contribute nothing) for the warp-aggregated atomic.
+// Punctured face types of one cube (window w, anchor (x, y)).
 template <typename T>
-__device__ void process_cube(const T* A, const T* B, const Geo& G, i64 x, i64 y, i64 t, bool valid,
-                             const ExtractParams& P) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ uint32_t cube_faces(const Win<T>& w, const Geo& G, i64 x, i64 y, bool hasB) {
   i64 g[8][2];
-  uint32_t exists = 0;   // corner existence
-  uint32_t pmask = 0;    // punctured face types
+  uint32_t exists = 0;
   bool wide = false;
-  if (valid) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const i64 cx = x + (c & 1), cy = y + ((c >> 1) & 1);
-      const bool has_t = !(c & 4) || B != nullptr;
-      if (cx < G.nx && cy < G.ny && has_t) {
-        grad_exact((c & 4) ? B : A, G, cx, cy, g[c]);
-        exists |= 1u << c;
-        const i64 m = (g[c][0] < 0 ? -g[c][0] : g[c][0]) | (g[c][1] < 0 ? -g[c][1] : g[c][1]);
-        wide |= m >= (1ll << 31);
-      } else {
-        g[c][0] = g[c][1] = 0;
-      }
-    }
-    if (wide) all_faces<true>(g, exists, pmask, std::make_integer_sequence<int, 12>{});
-    else all_faces<false>(g, exists, pmask, std::make_integer_sequence<int, 12>{});
+  for (int c = 0; c < 8; ++c) {
+    const bool ex = (x + (c & 1) < G.nx) && (y + ((c >> 1) & 1) < G.ny) && ((c >> 2) == 0 || hasB);
+    i64 gx, gy;
+    corner_grad(w, G, x, y, c, gx, gy);
+    g[c][0] = ex ? gx : 0;
+    g[c][1] = ex ? gy : 0;
+    exists |= (ex ? 1u : 0u) << c;
+    wide |= ((gx < 0 ? -gx : gx) | (gy < 0 ? -gy : gy)) >= (1ll << 31);
   }
-  // warp-aggregated reservation of output slots (one global atomic per warp batch)
+  // the 19 distinct determinants of the 12 faces: (0, k) for k = 1..7 and (m1, m2) per type
+  int s0k[8], sp[12];
+  s0k[0] = 0;
+  uint32_t pmask = 0;
+  if (!wide) {
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s0k[k] = det_sign<false>(g[0], g[k]);
+    pair_signs<false>(g, sp, std::make_integer_sequence<int, 12>{});
+  } else {
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s0k[k] = det_sign<true>(g[0], g[k]);
+    pair_signs<true>(g, sp, std::make_integer_sequence<int, 12>{});
+  }
+  all_faces(g, s0k, sp, exists, pmask, std::make_integer_sequence<int, 12>{});
+  return pmask;
+}
+
+__device__ __forceinline__ double dot3_nofma(const double* mu, double a, double b, double c) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(mu[0], a), __dmul_rn(mu[1], b)), __dmul_rn(mu[2], c));
+}
+
+// Hessian (4x scale, centre clamped into [1, N-2], R8) straight from global memory;
+// used only for partial cubes on the last row/column, whose stencil leaves the 4x4 window.
+template <typename T>
+__device__ void hessian_global(const ExtractParams& P, const Geo& G, i64 x, i64 y, i64 t, i64* H) {
+  const T* base = reinterpret_cast<const T*>(P.field) + (t - P.t0) * G.nx * G.ny;
+  auto q = [&](i64 xx, i64 yy) { return quant(base[yy * G.nx + xx], G.scale_f, G.scale); };
+  const i64 cx = x < 1 ? 1 : (x > G.nx - 2 ? G.nx - 2 : x);
+  const i64 cy = y < 1 ? 1 : (y > G.ny - 2 ? G.ny - 2 : y);
+  H[0] = 4 * (q(cx + 1, y) - 2 * q(cx, y) + q(cx - 1, y));
+  H[1] = q(cx + 1, cy + 1) - q(cx + 1, cy - 1) - q(cx - 1, cy + 1) + q(cx - 1, cy - 1);
+  H[2] = 4 * (q(x, cy + 1) - 2 * q(x, cy) + q(x, cy - 1));
+}
+
+// Location (Eq. 2), type and flags of punctured face `ty` of the cube at (x, y, t); writes the record.
+template <typename T>
+__device__ void emit_record(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y, i64 t, int ty,
+                            unsigned long long slot) {
+  int m[3] = {0, 0, 0};
+  masks_of(ty, m[1], m[2], std::make_integer_sequence<int, 12>{});
+  i64 gv[3][2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) corner_grad(w, G, x, y, m[k], gv[k][0], gv[k][1]);
+  // mu_k = D_k / sum D, D_k = (-1)^(k+2) det(rows != k)
+  const i128 D0 = det2(gv[1][0], gv[1][1], gv[2][0], gv[2][1]);
+  const i128 D1 = -det2(gv[0][0], gv[0][1], gv[2][0], gv[2][1]);
+  const i128 D2 = det2(gv[0][0], gv[0][1], gv[1][0], gv[1][1]);
+  const i128 S = D0 + D1 + D2;
+  double mu[3];
+  uint32_t flags = 0;
+  if (S == 0) {
+    mu[0] = mu[1] = mu[2] = 1.0 / 3.0;
+    flags |= FTK_CP_DEGENERATE_LOC;
+  } else {
+    const double s = i128_to_double_rn(S);
+    mu[0] = __ddiv_rn(i128_to_double_rn(D0), s);
+    mu[1] = __ddiv_rn(i128_to_double_rn(D1), s);
+    mu[2] = __ddiv_rn(i128_to_double_rn(D2), s);
+  }
+  const bool partial = (x == G.nx - 1) || (y == G.ny - 1);  // Hessian stencil leaves the window
+  double px[3], py[3], pt[3];
+  i64 Hk[3][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int mx = m[k] & 1, my = (m[k] >> 1) & 1, pl = (m[k] >> 2) & 1;
+    const i64 vx = x + mx, vy = y + my, vt = t + pl;
+    px[k] = (double)vx;
+    py[k] = (double)vy;
+    pt[k] = (double)vt;
+    if (partial) {
+      hessian_global<T>(P, G, vx, vy, vt, Hk[k]);
+    } else {
+      // integer Hessian, 4x scale, centre clamped into [1, N-2] (R8), from the window
+      const i64 cxg = vx < 1 ? 1 : (vx > G.nx - 2 ? G.nx - 2 : vx);
+      const i64 cyg = vy < 1 ? 1 : (vy > G.ny - 2 ? G.ny - 2 : vy);
+      const int cx = (int)(cxg - x) + 1, cy = (int)(cyg - y) + 1, wx = mx + 1, wy = my + 1;
+      Hk[k][0] = 4 * (w.q(pl, cx + 1, wy) - 2 * w.q(pl, cx, wy) + w.q(pl, cx - 1, wy));
+      Hk[k][1] = w.q(pl, cx + 1, cy + 1) - w.q(pl, cx + 1, cy - 1) - w.q(pl, cx - 1, cy + 1) + w.q(pl, cx - 1, cy - 1);
+      Hk[k][2] = 4 * (w.q(pl, wx, cy + 1) - 2 * w.q(pl, wx, cy) + w.q(pl, wx, cy - 1));
+    }
+  }
+  const double lx = dot3_nofma(mu, px[0], px[1], px[2]);
+  const double ly = dot3_nofma(mu, py[0], py[1], py[2]);
+  const double lt = dot3_nofma(mu, pt[0], pt[1], pt[2]);
+  double Hb[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e)
+    Hb[e] = dot3_nofma(mu, __ll2double_rn(Hk[0][e]), __ll2double_rn(Hk[1][e]), __ll2double_rn(Hk[2][e]));
+  // type (R9): sign of the interpolated Hessian's determinant, no tolerance
+  const double det = __dsub_rn(__dmul_rn(Hb[0], Hb[2]), __dmul_rn(Hb[1], Hb[1]));
+  int type;
+  if (det < 0) type = FTK_CP_SADDLE;
+  else if (det > 0) type = Hb[0] > 0 ? FTK_CP_MIN : FTK_CP_MAX;
+  else type = FTK_CP_DEGENERATE;
+  const int span = m[2];
+  if (!(span & 4)) flags |= FTK_CP_ORDINAL;
+  if (span != 7) {  // closed-form side_of: both parents exist iff v0[c] in [1, N_c - 2]
+    const int c = 7 & ~span;
+    const i64 vc = c == 1 ? x : (c == 2 ? y : t);
+    const i64 Nc = c == 1 ? G.nx : (c == 2 ? G.ny : G.ntg);
+    if (vc == 0 || vc == Nc - 1) flags |= FTK_CP_BOUNDARY;
+  }
+  if (slot < (unsigned long long)P.capacity) {
+    ftk_cp* r = P.out + slot;
+    r->face_id = ((t * G.ny + y) * G.nx + x) * 12 + ty;
+    r->label = -1;
+    r->x = lx;
+    r->y = ly;
+    r->z = 0.0;
+    r->t = lt;
+    r->type = type;
+    r->flags = flags;
+  }
+}
+
+// One batch of 32 ring entries (one cube per lane): face tests, then the punctured faces spread
+// over the lanes for the record stage.
+template <typename T>
+__device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G, const ExtractParams& P) {
+  const int lane = threadIdx.x & 31;
+  const int e = base_entry + lane;
+  const uint32_t mt = sm.meta[e];
+  const bool valid = mt != META_INVALID;
+  const i64 x = G.x0 + (mt & 255u), y = G.y0 + ((mt >> 8) & 127u), t = sm.qt[e];
+  const bool hasB = (mt >> 15) & 1u;
+  const Win<T> w{sm.win + e * WSTRIDE, G.scale_f, G.scale};
+  const uint32_t pmask = valid ? cube_faces<T>(w, G, x, y, hasB) : 0u;
+  // redistribute the punctured faces over the lanes
   const int cnt = __popc(pmask);
   int incl = cnt;
 #pragma unroll
@@ -269,84 +403,32 @@ __device__ void process_cube(const T* A, const T* B, const Geo& G, i64 x, i64 y,
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0) return;
-  unsigned long long base = 0;
-  if (lane == 31) base = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  unsigned long long slot = base + (unsigned long long)(incl - cnt);
-
-  while (pmask) {
-    const int ty = __ffs(pmask) - 1;
-    pmask &= pmask - 1;
-    int m[3] = {0, 0, 0};
-    masks_of(ty, m[1], m[2], std::make_integer_sequence<int, 12>{});
-    i64 gv[3][2];
-    sel_corner(g, 0, gv[0]);
-    sel_corner(g, m[1], gv[1]);
-    sel_corner(g, m[2], gv[2]);
-    // Eq. 2: mu_k = D_k / sum D, D_k = (-1)^(k+2) det(rows != k)
-    const i128 D0 = det2(gv[1][0], gv[1][1], gv[2][0], gv[2][1]);
-    const i128 D1 = -det2(gv[0][0], gv[0][1], gv[2][0], gv[2][1]);
-    const i128 D2 = det2(gv[0][0], gv[0][1], gv[1][0], gv[1][1]);
-    const i128 S = D0 + D1 + D2;
-    double mu[3];
-    uint32_t flags = 0;
-    if (S == 0) {
-      mu[0] = mu[1] = mu[2] = 1.0 / 3.0;
-      flags |= FTK_CP_DEGENERATE_LOC;
-    } else {
-      const double s = i128_to_double_rn(S);
-      mu[0] = __ddiv_rn(i128_to_double_rn(D0), s);
-      mu[1] = __ddiv_rn(i128_to_double_rn(D1), s);
-      mu[2] = __ddiv_rn(i128_to_double_rn(D2), s);
+  uint16_t* items = sm.items[ew];
+  {
+    int pos = incl - cnt;
+    uint32_t pm = pmask;
+    while (pm) {
+      const int ty = __ffs(pm) - 1;
+      pm &= pm - 1;
+      items[pos++] = (uint16_t)(lane | (ty << 5));
     }
-    double px[3], py[3], pt[3];
-    double Hb[3] = {0, 0, 0};
-    i64 Hk[3][3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const i64 vx = x + (m[k] & 1), vy = y + ((m[k] >> 1) & 1), vt = t + ((m[k] >> 2) & 1);
-      px[k] = (double)vx;
-      py[k] = (double)vy;
-      pt[k] = (double)vt;
-      hessian_exact((m[k] & 4) ? B : A, G, vx, vy, Hk[k]);
-    }
-    const double lx = fma_free_dot3(mu, px[0], px[1], px[2]);
-    const double ly = fma_free_dot3(mu, py[0], py[1], py[2]);
-    const double lt = fma_free_dot3(mu, pt[0], pt[1], pt[2]);
-#pragma unroll
-    for (int e = 0; e < 3; ++e)
-      Hb[e] = fma_free_dot3(mu, __ll2double_rn(Hk[0][e]), __ll2double_rn(Hk[1][e]), __ll2double_rn(Hk[2][e]));
-    // type (R9): det of the interpolated Hessian, no tolerance
-    const double det = __dsub_rn(__dmul_rn(Hb[0], Hb[2]), __dmul_rn(Hb[1], Hb[1]));
-    int type;
-    if (det < 0) type = FTK_CP_SADDLE;
-    else if (det > 0) type = Hb[0] > 0 ? FTK_CP_MIN : FTK_CP_MAX;
-    else type = FTK_CP_DEGENERATE;
-    const int span = m[2];
-    if (!(span & 4)) flags |= FTK_CP_ORDINAL;
-    if (span != 7) {  // closed-form side_of: parents exist iff v0[c] in [1, N_c - 2]
-      const int c = 7 & ~span;
-      const i64 vc = c == 1 ? x : (c == 2 ? y : t);
-      const i64 Nc = c == 1 ? G.nx : (c == 2 ? G.ny : G.ntg);
-      if (vc == 0 || vc == Nc - 1) flags |= FTK_CP_BOUNDARY;
-    }
-    if (slot < (unsigned long long)P.capacity) {
-      ftk_cp* r = P.out + slot;
-      r->face_id = ((t * G.ny + y) * G.nx + x) * 12 + ty;
-      r->label = -1;
-      r->x = lx;
-      r->y = ly;
-      r->z = 0.0;
-      r->t = lt;
-      r->type = type;
-      r->flags = flags;
-    }
-    ++slot;
   }
+  unsigned long long obase = 0;
+  if (lane == 0) obase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
+  obase = __shfl_sync(0xffffffffu, obase, 0);
+  __syncwarp();
+  for (int i = lane; i < total; i += 32) {
+    const int it = items[i];
+    const int le = base_entry + (it & 31), ty = it >> 5;
+    const uint32_t m2 = sm.meta[le];
+    const Win<T> w2{sm.win + le * WSTRIDE, G.scale_f, G.scale};
+    emit_record<T>(w2, G, P, G.x0 + (m2 & 255u), G.y0 + ((m2 >> 8) & 127u), sm.qt[le], ty, obase + i);
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------------------------
-// Scan helpers
+// Scan
 // ---------------------------------------------------------------------------------------------
 template <typename T>
 struct Row {
@@ -367,8 +449,7 @@ __device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane) {
   }
   T up = __shfl_up_sync(0xffffffffu, w.d, 1);
   T dn = __shfl_down_sync(0xffffffffu, w.a, 1);
-  // lanes 0 and 31 take the tile halo from shared memory (one predicated load)
-  if (lane == 0 || lane == 31) {
+  if (lane == 0 || lane == 31) {  // tile halo from shared memory (one predicated load)
     const T h = S[srow * PITCH + (lane == 0 ? XOFF - 1 : XOFF + LX)];
     if (lane == 0) up = h; else dn = h;
   }
@@ -377,22 +458,41 @@ __device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane) {
   return w;
 }
 
-// 4-bit sign code of one vertex: bit0 dx >= thr, bit1 dx <= -thr, bit2 dy >= thr, bit3 dy <= -thr.
-template <typename T>
-__device__ __forceinline__ uint32_t code4(T dx, T dy, T thr) {
-  return (uint32_t)(dx >= thr) | ((uint32_t)(dx <= -thr) << 1) | ((uint32_t)(dy >= thr) << 2) |
-         ((uint32_t)(dy <= -thr) << 3);
+// 16-bit row code, position i in nibble (3 - i); nibble bits 3..0 = NOT(dx >= thr), NOT(dx < -thr),
+// NOT(dy >= thr), NOT(dy < -thr) -- the sign bits of dx - thr, ~(dx + thr), dy - thr, ~(dy + thr).
+__device__ __forceinline__ uint32_t row_code_fast(const Row<float>& up, const Row<float>& cur, const Row<float>& dn,
+                                                  f2 thr2) {
+  const f2 dx01 = sub2(pack2(cur.b, cur.c), pack2(cur.l, cur.a));
+  const f2 dx23 = sub2(pack2(cur.d, cur.r), pack2(cur.b, cur.c));
+  const f2 dy01 = sub2(pack2(dn.a, dn.b), pack2(up.a, up.b));
+  const f2 dy23 = sub2(pack2(dn.c, dn.d), pack2(up.c, up.d));
+  const f2 ax01 = sub2(dx01, thr2), ex01 = add2(dx01, thr2);
+  const f2 ax23 = sub2(dx23, thr2), ex23 = add2(dx23, thr2);
+  const f2 ay01 = sub2(dy01, thr2), ey01 = add2(dy01, thr2);
+  const f2 ay23 = sub2(dy23, thr2), ey23 = add2(dy23, thr2);
+  uint32_t W = 0;
+  W = push_sign(W, lo32(ax01)); W = push_sign(W, lo32(ex01)); W = push_sign(W, lo32(ay01)); W = push_sign(W, lo32(ey01));
+  W = push_sign(W, hi32(ax01)); W = push_sign(W, hi32(ex01)); W = push_sign(W, hi32(ay01)); W = push_sign(W, hi32(ey01));
+  W = push_sign(W, lo32(ax23)); W = push_sign(W, lo32(ex23)); W = push_sign(W, lo32(ay23)); W = push_sign(W, lo32(ey23));
+  W = push_sign(W, hi32(ax23)); W = push_sign(W, hi32(ex23)); W = push_sign(W, hi32(ay23)); W = push_sign(W, hi32(ey23));
+  return W ^ 0x5555u;
 }
 
-// codes of the lane's 4 positions on one row (16 bits).  EDGE: apply the one-sided boundary rule
-// and neutral codes (0xF) outside the grid.
+template <typename T>
+__device__ __forceinline__ uint32_t sign_bit(T v) {
+  if constexpr (sizeof(T) == 4) return __float_as_uint(v) >> 31;
+  else return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63);
+}
+
+// generic row code: any dtype, one-sided differences at the spatial boundary, neutral (0) nibbles
+// for positions outside the grid
 template <typename T, bool EDGE>
-__device__ __forceinline__ uint32_t row_codes(const Row<T>& up, const Row<T>& cur, const Row<T>& dn, T thr,
-                                              i64 gx, i64 gy, i64 nx, i64 ny) {
+__device__ __forceinline__ uint32_t row_code_generic(const Row<T>& up, const Row<T>& cur, const Row<T>& dn, T thr,
+                                                     i64 gx, i64 gy, i64 nx, i64 ny) {
   const T f[6] = {cur.l, cur.a, cur.b, cur.c, cur.d, cur.r};
   const T fu[4] = {up.a, up.b, up.c, up.d};
   const T fd[4] = {dn.a, dn.b, dn.c, dn.d};
-  uint32_t C = 0;
+  uint32_t W = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     T lo = f[i], hi = f[i + 2], ylo = fu[i], yhi = fd[i];
@@ -403,22 +503,32 @@ __device__ __forceinline__ uint32_t row_codes(const Row<T>& up, const Row<T>& cu
       if (gy == 0) ylo = f[i + 1];
       if (gy == ny - 1) yhi = f[i + 1];
     }
-    uint32_t c = code4(hi - lo, yhi - ylo, thr);
-    if (EDGE && (gx + i >= nx || gy >= ny)) c = 0xF;
-    C |= c << (4 * i);
+    const T dx = hi - lo, dy = yhi - ylo;
+    uint32_t nib = (sign_bit<T>(dx - thr) << 3) | ((sign_bit<T>(dx + thr) ^ 1u) << 2) |
+                   (sign_bit<T>(dy - thr) << 1) | (sign_bit<T>(dy + thr) ^ 1u);
+    if (EDGE && (gx + i >= nx || gy >= ny)) nib = 0u;  // no such corner: OR-neutral
+    W = (W << 4) | nib;
   }
-  return C;
+  return W;
+}
+
+__device__ __forceinline__ uint32_t max_abs_bits(uint32_t m, float a, float b, float c, float d) {
+  float r = __uint_as_float(m), t1, t2;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t1) : "f"(fabsf(a)), "f"(fabsf(b)));
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t2) : "f"(fabsf(c)), "f"(fabsf(d)));
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t1) : "f"(t1), "f"(t2));
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(r), "f"(t1));
+  return __float_as_uint(r);
 }
 
 // ---------------------------------------------------------------------------------------------
 // The kernel
 // ---------------------------------------------------------------------------------------------
 template <typename T, bool TMA>
-__global__ void __launch_bounds__(NWARP * 32, 2)
+__global__ void __launch_bounds__(NTHREADS, 2)
     k_extract2d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // the dynamic shared window is only guaranteed 16-byte alignment: round up to 128
-  const uint32_t mis = smem_u32(smem_raw) & 127u;
+  const uint32_t mis = smem_u32(smem_raw) & 127u;  // dynamic smem is only 16-byte aligned
   Smem<T>& sm = *reinterpret_cast<Smem<T>*>(smem_raw + (mis ? 128 - mis : 0));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -429,185 +539,277 @@ __global__ void __launch_bounds__(NWARP * 32, 2)
   G.x0 = (i64)blockIdx.x * TX;
   G.y0 = (i64)blockIdx.y * TY;
   G.scale = P.scale;
+  G.scale_f = (float)P.scale;
   const i64 ta = P.ta + (i64)blockIdx.z * P.tchunk;
   const i64 tb = min(ta + P.tchunk, P.tb);           // anchor planes [ta, tb)
   const i64 plast = min(tb, P.nt_global - 1);         // planes ta .. plast are loaded
   const int nplanes = (int)(plast - ta + 1);
-  const T* field = reinterpret_cast<const T*>(P.field);
-  const T thr = (T)P.thr;
+  constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
 
   if (tid == 0) {
-    sm.qn[0] = sm.qn[1] = 0;
     sm.surv = 0;
-    sm.maxbits = 0;
-    if (TMA) {
-      for (int s = 0; s < NSTAGE; ++s) mbar_init(&sm.full[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sm.maxbits32 = 0;
+    sm.maxbits64 = 0;
+    sm.tail = 0;
+    sm.scan_done = 0;
+    sm.nbatch = -1;
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], NSW);
     }
+    for (int b = 0; b < NB; ++b) {
+      sm.wfill[b] = 0;
+      sm.wcons[b] = 0;
+    }
+    for (int e = 0; e < NEW; ++e) sm.dbg_eb[e] = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
-  if (TMA && tid == 0) {
-    for (int k = 0; k < NSTAGE && k < nplanes; ++k) {
-      mbar_expect_tx(&sm.full[k], STAGE_BYTES);
-      tma_load_3d(sm.plane[k], &tmap, &sm.full[k], (int)(G.x0 - XOFF), (int)(G.y0 - YOFF), (int)(ta + k - P.t0));
-    }
-  }
 
-  const bool edge = G.x0 < 1 || G.x0 + LX + 1 > G.nx || G.y0 < 1 || G.y0 + TY + 2 > G.ny;
-  const i64 gx = G.x0 + 4 * lane;            // first x of this lane
-  const i64 gy0 = G.y0 + warp * RW;          // first anchor row of this warp
-  const int srow0 = YOFF + warp * RW;        // its smem row
-  typename Bits<T>::U maxb = 0;
-  uint32_t prevSq[RW];
-#pragma unroll
-  for (int r = 0; r < RW; ++r) prevSq[r] = 0xFFFFu;
-
-  auto scan_plane = [&](const T* S, uint32_t* Sq) {
-    Row<T> up = load_row<T>(S, srow0 - 1, lane);
-    Row<T> cur = load_row<T>(S, srow0, lane);
-    uint32_t Cprev = 0;
-#pragma unroll
-    for (int r = 0; r <= RW; ++r) {
-      const Row<T> dn = load_row<T>(S, srow0 + r + 1, lane);
-      if (r < RW) {
-        maxb = max(maxb, max(max(Bits<T>::absbits(cur.a), Bits<T>::absbits(cur.b)),
-                             max(Bits<T>::absbits(cur.c), Bits<T>::absbits(cur.d))));
+  if (warp == PRODUCER) {
+    // ------------------------------------------------------------------ producer warp
+    const T* field = reinterpret_cast<const T*>(P.field);
+    for (int k = 0; k < nplanes; ++k) {
+      const int s = k % NSTAGE;
+      if (k >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)((k / NSTAGE - 1) & 1), 1, k);
+      if (TMA) {
+        if (lane == 0) {
+          mbar_expect_tx(&sm.full[s], STAGE_BYTES);
+          tma_load_3d(sm.plane[s], &tmap, &sm.full[s], (int)(G.x0 - XOFF), (int)(G.y0 - YOFF), (int)(ta + k - P.t0));
+        }
+      } else {
+        // generic loader for unaligned shapes: guarded element loads (zero outside the grid)
+        const T* src = field + (ta + k - P.t0) * G.nx * G.ny;
+        T* dst = sm.plane[s];
+        for (int idx = lane; idx < ROWS * PITCH; idx += 32) {
+          const int rr = idx / PITCH, cc = idx - rr * PITCH;
+          const i64 yy = G.y0 - YOFF + rr, xx = G.x0 - XOFF + cc;
+          dst[idx] = (yy >= 0 && yy < G.ny && xx >= 0 && xx < G.nx) ? src[yy * G.nx + xx] : (T)0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.full[s]);
       }
-      const uint32_t C = edge ? row_codes<T, true>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny)
-                              : row_codes<T, false>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny);
-      if (r > 0) {
-        uint32_t Y = Cprev & C;                                   // y-pair AND (per position)
-        // x-pair AND; position 4 = the next lane's position 0 (lane 31's cubes are not owned:
-        // its x+1 corners are unknown here, and unknown corners must NOT enter the AND)
-        const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1) & 0xFu;
-        Sq[r - 1] = Y & ((Y >> 4) | (nb << 12));
+    }
+  } else if (warp > PRODUCER) {
+    // ------------------------------------------------------------------ exact warps
+    const int ew = warp - PRODUCER - 1;
+    for (int b = ew;; b += NEW) {
+      if (lane == 0) sm.dbg_eb[ew] = b;
+      const int j = b % NB;
+      bool go = true;
+      const int target = 32 * (b / NB + 1);
+      if (*(volatile int*)&sm.wfill[j] < target) {
+        const unsigned long long t0 = gtimer_ns();
+        while (*(volatile int*)&sm.wfill[j] < target) {
+          const int nbf = sm.nbatch;
+          if (nbf >= 0 && b >= nbf) {
+            go = false;
+            break;
+          }
+          __nanosleep(64);
+          if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(4, b, nbf);
+        }
       }
-      Cprev = C;
-      up = cur;
-      cur = dn;
-    }
-  };
-
-  // push the survivors of anchor plane (given by their 32-bit mask: bit 4r+i) to the CTA queue
-  auto push = [&](uint32_t mask, int qsel) {
-    const int cnt = __popc(mask);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) return;
-    int base = 0;
-    if (lane == 31) base = atomicAdd(&sm.qn[qsel], total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - cnt;
-    while (mask) {
-      const int b = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const int r = b >> 2, i = b & 3;
-      sm.queue[pos++] = (uint16_t)((4 * lane + i) | ((warp * RW + r) << 7));
-    }
-  };
-
-  auto survivors_of = [&](const uint32_t* K) {
-    uint32_t mask = 0;
-    if (lane == 31) return mask;  // halo lane owns no anchors
-#pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      uint32_t z = K[r] | (K[r] >> 1);
-      z |= z >> 2;
-      const uint32_t m = ~z & 0x1111u;                 // nibble == 0  ->  survivor
-      mask |= (((m * 0x249u) >> 9) & 0xFu) << (4 * r); // gather bits 0,4,8,12 -> 0..3
-    }
-    return mask;
-  };
-
-  auto process_queue = [&](const T* A, const T* B, i64 t, int n) {
-    for (int e0 = warp * 32; e0 < n; e0 += NWARP * 32) {
-      const int e = e0 + lane;
-      const bool valid = e < n;
-      const uint32_t code = valid ? sm.queue[e] : 0u;
-      const i64 x = G.x0 + (code & 127u), y = G.y0 + (code >> 7);
-      process_cube<T>(A, B, G, x, y, t, valid, P);
-    }
-  };
-
-  for (int k = 0; k < nplanes; ++k) {
-    const i64 p = ta + k;
-    const int s = k % NSTAGE;
-    T* S = sm.plane[s];
-    if (TMA) {
-      mbar_wait(&sm.full[s], (uint32_t)((k / NSTAGE) & 1));
-    } else {
-      // generic loader: guarded element loads of the plane tile (zero outside the grid)
-      const T* src = field + (p - P.t0) * G.nx * G.ny;
-      for (int idx = tid; idx < ROWS * PITCH; idx += NWARP * 32) {
-        const int rr = idx / PITCH, cc = idx % PITCH;
-        const i64 yy = G.y0 - YOFF + rr, xx = G.x0 - XOFF + cc;
-        S[idx] = (yy >= 0 && yy < G.ny && xx >= 0 && xx < G.nx) ? src[yy * G.nx + xx] : (T)0;
+      __threadfence_block();
+      if (!go) break;
+      process_batch<T>(sm, ew, j * 32, G, P);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();  // our reads of the slot happen before it is handed back
+        sm.wcons[j] = b / NB + 1;
       }
-      __syncthreads();
     }
-    uint32_t Sq[RW];
-    scan_plane(S, Sq);
-    const int qsel = k & 1;
-    if (k > 0) {
-      uint32_t K[RW];
-#pragma unroll
-      for (int r = 0; r < RW; ++r) K[r] = prevSq[r] & Sq[r];
-      push(survivors_of(K), qsel);
-    }
-#pragma unroll
-    for (int r = 0; r < RW; ++r) prevSq[r] = Sq[r];
-    const bool last_global = (p == P.nt_global - 1) && (p < tb);  // anchors on the last timestep
-    __syncthreads();  // (A) queue complete
-    const int n1 = sm.qn[qsel];
-    if (k > 0) process_queue(sm.plane[(k - 1) % NSTAGE], S, p - 1, n1);
-    int n2 = 0;
-    if (last_global) {
-      __syncthreads();  // queue entries consumed
-      uint32_t K[RW];
-#pragma unroll
-      for (int r = 0; r < RW; ++r) K[r] = Sq[r];  // no t+1 corners: AND over the plane only
-      push(survivors_of(K), qsel ^ 1);
-      __syncthreads();
-      n2 = sm.qn[qsel ^ 1];
-      process_queue(S, nullptr, p, n2);
-    }
-    __syncthreads();  // (B) plane p-1 is free, every reader of the counters is done
-    if (tid == 0) {
-      sm.surv += (unsigned long long)(n1 + n2);
-      sm.qn[qsel] = 0;
-      if (last_global) sm.qn[qsel ^ 1] = 0;
-    }
-    if (TMA && tid == 0 && k >= 1 && k - 1 + NSTAGE < nplanes) {
-      const int kn = k - 1 + NSTAGE;
-      const int sn = kn % NSTAGE;
-      fence_proxy_async();
-      mbar_expect_tx(&sm.full[sn], STAGE_BYTES);
-      tma_load_3d(sm.plane[sn], &tmap, &sm.full[sn], (int)(G.x0 - XOFF), (int)(G.y0 - YOFF), (int)(ta + kn - P.t0));
-    }
-  }
-
-  // block-level reductions of the statistics
-  if constexpr (sizeof(T) == 4) {
-    uint32_t m = maxb;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) atomicMax(&sm.maxbits, (unsigned long long)m);
   } else {
-    unsigned long long m = maxb;
+    // ------------------------------------------------------------------ scan warps
+    const i64 gx = G.x0 + 4 * lane;          // first x of this lane
+    const i64 gy0 = G.y0 + warp * RW;        // first anchor row of this warp
+    const int srow0 = YOFF + warp * RW;      // its smem row
+    const bool xedge = G.x0 < 1 || G.x0 + LX + 1 > G.nx;
+    const bool edge = xedge || gy0 < 1 || gy0 + RW + 2 > G.ny;  // code rows gy0 .. gy0+RW in [1, ny-2]
+    const T thr = (T)P.thr;
+    const f2 thr2 = pack2((float)P.thr, (float)P.thr);
+    uint32_t maxb32 = 0;
+    double maxd = 0.0;
+    unsigned long long mysurv = 0;
+    uint32_t prevSq[RW];
+    // window copy: lane k copies element k = (pl, r, c) of the 4x4x2 window
+    const int c_pl = lane >> 4, c_r = (lane >> 2) & 3, c_c = lane & 3;
+    const int c_off = (c_r - 1 + YOFF) * PITCH + (c_c - 1 + XOFF);
+
+    auto scan_plane = [&](const T* S, uint32_t* Sq) {
+      Row<T> up = load_row<T>(S, srow0 - 1, lane);
+      Row<T> cur = load_row<T>(S, srow0, lane);
+      uint32_t Cprev = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) atomicMax(&sm.maxbits, m);
+      for (int r = 0; r <= RW; ++r) {
+        const Row<T> dn = load_row<T>(S, srow0 + r + 1, lane);
+        if (r < RW) {
+          if constexpr (sizeof(T) == 4) {
+            maxb32 = max_abs_bits(maxb32, cur.a, cur.b, cur.c, cur.d);
+          } else {
+            maxd = fmax(maxd, fmax(fmax(fabs(cur.a), fabs(cur.b)), fmax(fabs(cur.c), fabs(cur.d))));
+            if (cur.a != cur.a || cur.b != cur.b || cur.c != cur.c || cur.d != cur.d)
+              maxd = __longlong_as_double(0x7ff8000000000000ll);
+          }
+        }
+        uint32_t C;
+        if constexpr (sizeof(T) == 4) {
+          C = edge ? row_code_generic<T, true>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny)
+                   : row_code_fast(up, cur, dn, thr2);
+        } else {
+          C = edge ? row_code_generic<T, true>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny)
+                   : row_code_generic<T, false>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny);
+        }
+        if (r > 0) {
+          const uint32_t Y = Cprev | C;                                   // y-pair
+          const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1) >> 12;  // next lane's position 0
+          Sq[r - 1] = (Y | (Y << 4) | nb) & 0xFFFFu;                      // x-pair
+        }
+        Cprev = C;
+        up = cur;
+        cur = dn;
+      }
+    };
+
+    // survivors of one anchor plane: bit (4r + j) <-> row r, position 3 - j
+    auto survivors_of = [&](const uint32_t* K) {
+      uint32_t mask = 0;
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        uint32_t z = K[r] & (K[r] >> 1);
+        z &= z >> 2;
+        const uint32_t m = z & 0x1111u;                  // nibble all ones -> survivor
+        mask |= (((m * 0x249u) >> 9) & 0xFu) << (4 * r); // gather bits 0,4,8,12 -> 0..3
+      }
+      return lane == 31 ? 0u : mask;                     // the halo lane owns no anchors
+    };
+
+    // hand the survivors to the exact warps: reserve ring entries, copy each cube's 4x4x2 window
+    // (planes A = t, B = t+1), publish on the batch's wfull barrier
+    auto enqueue = [&](uint32_t mask, const T* A, const T* B, i64 t) {
+      const int cnt = __popc(mask);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) return;
+      mysurv += total;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&sm.tail, total);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      int myfirst = incl - cnt;
+      int i = 0;
+      while (true) {
+        const uint32_t have = __ballot_sync(0xffffffffu, mask != 0);
+        if (!have) break;
+        const int myb = mask ? __ffs(mask) - 1 : 0;
+        mask &= mask - 1;
+        uint32_t h = have;
+        while (h) {
+          const int L = __ffs(h) - 1;
+          h &= h - 1;
+          const int b = __shfl_sync(0xffffffffu, myb, L);
+          const int xl = 4 * L + 3 - (b & 3), yl = warp * RW + (b >> 2);
+          const int e = base + i++;
+          const int bat = e >> 5, slot = bat % NB, pos = e & (RING - 1);
+          if ((e & 31) == 0 || i == 1) {
+            // first write into this batch slot for this warp: the slot's previous generation
+            // must have been consumed
+            if (bat >= NB && sm.wcons[slot] < bat / NB) {
+              const unsigned long long t0 = gtimer_ns();
+              while (sm.wcons[slot] < bat / NB) {
+                __nanosleep(32);
+                if (gtimer_ns() - t0 > 2000000000ull) {
+                  if (lane == 0)
+                    printf("ring stall: warp %d e=%d bat=%d tail=%d nbatch=%d exact=[%d %d %d]\n", warp, e, bat,
+                           *(volatile int*)&sm.tail, sm.nbatch, sm.dbg_eb[0], sm.dbg_eb[1], sm.dbg_eb[2]);
+                  wait_timeout(2, bat, e);
+                }
+              }
+              __threadfence_block();
+            }
+          }
+          const T* src = (c_pl ? (B ? B : A) : A) + yl * PITCH + xl + c_off;
+          sm.win[pos * WSTRIDE + lane] = *src;
+          if (lane == 0) {
+            sm.meta[pos] = (uint32_t)xl | ((uint32_t)yl << 8) | ((B ? 1u : 0u) << 15);
+            sm.qt[pos] = (int)t;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(&sm.wfill[slot], 1);
+          }
+        }
+      }
+      (void)myfirst;
+    };
+
+    for (int k = 0; k < nplanes; ++k) {
+      const i64 p = ta + k;
+      const int s = k % NSTAGE;
+      const T* S = sm.plane[s];
+      mbar_wait(&sm.full[s], (uint32_t)((k / NSTAGE) & 1), 3, k);
+      uint32_t Sq[RW];
+      scan_plane(S, Sq);
+      if (k > 0) {
+        uint32_t K[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) K[r] = prevSq[r] | Sq[r];
+        enqueue(survivors_of(K), sm.plane[(k - 1) % NSTAGE], S, p - 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[(k - 1) % NSTAGE]);  // plane p-1 no longer needed
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) prevSq[r] = Sq[r];
+      if (p == P.nt_global - 1 && p < tb) {
+        // anchors on the last timestep: no t+1 corners, the OR runs over the plane only
+        enqueue(survivors_of(Sq), S, nullptr, p);
+      }
+    }
+
+    // the last scan warp to finish pads the final partial batch and publishes the batch count
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&sm.scan_done, 1) == NSW - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      const int n = *((volatile int*)&sm.tail);
+      const int nb = (n + 31) >> 5;
+      const int pad = nb * 32 - n;
+      if (pad) {
+        const int bat = nb - 1, slot = bat % NB;
+        if (lane < pad) sm.meta[(n + lane) & (RING - 1)] = META_INVALID;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicAdd(&sm.wfill[slot], pad);
+        }
+      }
+      if (lane == 0) sm.nbatch = nb;
+    }
+
+    // statistics
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      maxb32 = max(maxb32, __shfl_xor_sync(0xffffffffu, maxb32, o));
+      const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
+      maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
+    }
+    if (lane == 0) {
+      atomicAdd(&sm.surv, mysurv);
+      atomicMax(&sm.maxbits32, maxb32);
+      atomicMax(&sm.maxbits64, (unsigned long long)__double_as_longlong(maxd));
+    }
   }
   __syncthreads();
   if (tid == 0) {
     atomicAdd(&P.counters[CNT_SURVIVORS], sm.surv);
-    atomicMax(&P.counters[CNT_MAXBITS], sm.maxbits);
+    atomicMax(&P.counters[CNT_MAXBITS], sizeof(T) == 4 ? (unsigned long long)sm.maxbits32 : sm.maxbits64);
   }
 }
 
@@ -657,7 +859,7 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   const dim3 grid((unsigned)((P.nx + TX - 1) / TX), (unsigned)((P.ny + TY - 1) / TY),
                   (unsigned)((P.tb - P.ta + P.tchunk - 1) / P.tchunk));
   if (grid.z == 0) return FTK_OK;
-  kern<<<grid, NWARP * 32, smem, stream>>>(map, P);
+  kern<<<grid, NTHREADS, smem, stream>>>(map, P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }
