@@ -22,6 +22,7 @@ enum Counter : int {
   CNT_MAXBITS = 2,    // max over |f| as IEEE bits (float bits for f32, double bits for f64)
   CNT_INVARIANT = 3,  // link: faces whose parent cell does not hold exactly one other punctured face
   CNT_EXPORT = 4,     // slab stitch: exported boundary faces
+  CNT_WORK = 5,       // K1 persistent scheduler: next work item
   CNT_N = 8
 };
 

@@ -1,12 +1,13 @@
 // extract2d.cu -- K1: pass 1 of Alg. 1 for 2D+t on sm_100a.
 //
-// One CTA owns a 124 x 32 tile of anchors (x, y) and a chunk of anchor timesteps; it marches t.
-// Warp-specialised:
+// Persistent kernel, 2 CTAs per SM.  A work item is a 124 x 32 tile of anchors (x, y) times a chunk
+// of anchor timesteps; CTAs pull items from a global counter and march t through them.  Each CTA is
+// warp-specialised:
 //
-//   producer warp -- TMA (cp.async.bulk.tensor) stages each plane tile with its halo
-//     (x0-4 .. x0+131, y0-2 .. y0+34) into an NSTAGE-deep shared-memory ring guarded by full/empty
-//     mbarriers: every vertex is read from HBM once and reused by all 12 faces of the 8 cubes it
-//     belongs to (north_star (2)).
+//   producer warp -- fetches items and, plane after plane, stages the tile with its halo
+//     (x0-4 .. x0+131, y0-2 .. y0+34) into an NSTAGE-deep shared-memory ring with TMA
+//     (cp.async.bulk.tensor) under full/empty mbarriers, so every vertex is read from HBM once and
+//     reused by all 12 faces of the 8 cubes it belongs to (north_star (2)).
 //
 //   8 scan warps (4 anchor rows x 124 columns each; lane = 4 consecutive x, lane 31 is a halo lane)
 //     -- a CONSERVATIVE sign prefilter on raw field values.  For the gradient component
@@ -16,16 +17,20 @@
 //     strict sign condition does NOT hold) and ORed over the 8 corners of each spacetime cube: a
 //     nibble with a zero bit means one gradient component has one strict sign on every corner, so no
 //     face of the cube can contain the origin -- even under SoS (the perturbation is infinitesimal).
-//     For each surviving cube (~0.45% on the woven field) the warp copies its 4x4x2 window of raw
-//     values into a CTA window ring (1 LDS + 1 STS per lane) and moves on.
+//     Grid boundaries are handled by patching the neighbour values in registers (one-sided
+//     differences) and masking codes of positions outside the grid.  For each surviving cube
+//     (~0.45% on the woven field) the warp copies its 4x4x2 window of raw values into a CTA window
+//     ring (1 LDS + 1 STS per lane) and moves on.
 //
-//   3 exact warps -- take the ring in batches of 32 cubes (one per lane, no divergence between
-//     cubes): exact quantization, gradients, the 19 distinct 2x2 determinants of the cube's 12 faces,
-//     SoS point-in-simplex; then the punctured faces are redistributed over the
-//     lanes and each gets its Eq. 2 location and Hessian type in fixed-order FP64 (no FMA), written
-//     with one global atomic per batch.
+//   3 exact warps -- take the ring in batches of 32 cubes (one per lane): exact int32 quantization
+//     and gradients, the 19 distinct 2x2 determinants of the cube's 12 faces, SoS point-in-simplex
+//     (an exact int64/int128 path covers boundary cubes, zero determinants and
+//     large values); the punctured faces are then spread over the lanes and each gets its Eq. 2
+//     location and Hessian type in fixed-order FP64 (no FMA), written with one global atomic per
+//     batch.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <utility>
@@ -68,14 +73,13 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   return t;
 }
 // never hang the GPU: a wait that exceeds 2 s reports where it is stuck and traps
-__device__ unsigned long long* g_dbg_ring = nullptr;
 __device__ __noinline__ void wait_timeout(int what, int a, int b) {
   if ((threadIdx.x & 31) == 0)
-    printf("ftk k_extract2d: wait timeout what=%d a=%d b=%d block=(%d,%d,%d) warp=%d\n", what, a, b, blockIdx.x,
-           blockIdx.y, blockIdx.z, threadIdx.x >> 5);
+    printf("ftk k_extract2d: wait timeout what=%d a=%d b=%d block=%d warp=%d\n", what, a, b, blockIdx.x,
+           threadIdx.x >> 5);
   __trap();
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what = 0, int a = 0) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what, int a) {
   if (mbar_try(bar, parity)) return;
   const unsigned long long t0 = gtimer_ns();
   while (!mbar_try(bar, parity))
@@ -114,10 +118,10 @@ __device__ __forceinline__ uint32_t hi32(f2 a) { return (uint32_t)(a.v >> 32); }
 __device__ __forceinline__ uint32_t push_sign(uint32_t W, uint32_t bits) { return __funnelshift_l(bits, W, 1); }
 
 // ---------------------------------------------------------------------------------------------
-// Tile geometry and roles
+// Geometry and roles
 // ---------------------------------------------------------------------------------------------
 constexpr int LX = 128;             // x positions scanned per warp row (32 lanes x 4)
-constexpr int TX = 124;             // anchors owned per CTA in x: lane 31 is a halo lane whose codes
+constexpr int TX = 124;             // anchors owned per tile in x: lane 31 is a halo lane whose codes
                                     // only complete lane 30's cubes (a cube needs its x+1 corners)
 constexpr int RW = 4;               // anchor rows per scan warp
 constexpr int NSW = 8;              // scan warps
@@ -125,7 +129,7 @@ constexpr int PRODUCER = NSW;       // warp index of the TMA producer
 constexpr int NEW = 3;              // exact warps
 constexpr int NWARPS = NSW + 1 + NEW;
 constexpr int NTHREADS = NWARPS * 32;
-constexpr int TY = RW * NSW;        // 32 anchor rows per CTA
+constexpr int TY = RW * NSW;        // 32 anchor rows per tile
 constexpr int XOFF = 4;             // smem column of x0
 constexpr int YOFF = 2;             // smem row of y0
 constexpr int PITCH = LX + 8;       // x0-4 .. x0+131
@@ -134,29 +138,35 @@ constexpr int NSTAGE = 3;
 constexpr int NB = 8;               // window-ring batch slots (32 cubes each)
 constexpr int RING = NB * 32;
 constexpr int WSTRIDE = 33;         // values per queued window (4x4x2 = 32, odd stride: no bank conflicts)
-constexpr uint32_t META_INVALID = 0xFFFFFFFFu;
 constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
+constexpr int TCHUNK = 32;          // anchor timesteps per work item
 
 template <typename T>
 constexpr int stage_elems() {       // plane tile padded to a multiple of 128 bytes (TMA alignment)
   return (ROWS * PITCH * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
 }
 
+struct StageMeta {                  // written by the producer before the plane lands
+  int x0, y0;                       // tile origin
+  int p;                            // global timestep of the plane
+  int k;                            // index of the plane within its work item
+  int nplanes;                      // planes in the work item
+  int tb;                           // end of the item's anchor range
+  int done;                         // no more work
+};
+
 template <typename T>
 struct alignas(128) Smem {
   T plane[NSTAGE][stage_elems<T>()];
-  T win[RING * WSTRIDE];           // queued survivor windows (raw values)
-  uint32_t meta[RING];             // xl | yl << 8 | hasB << 15, or META_INVALID (padding)
-  int qt[RING];                    // anchor timestep
+  T win[RING * WSTRIDE];           // queued survivor windows: W[pl*16 + r*4 + c] = f(x-1+c, y-1+r, t+pl)
+  int qx[RING], qy[RING], qt[RING];  // cube anchor; qt bit 31: the t+1 plane exists
   uint16_t items[NEW][MAXITEMS];   // punctured faces of a batch: entry | type << 5
+  StageMeta meta[NSTAGE];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
-  int wfill[NB];                   // entries ever written into each batch slot (monotone counter)
+  int wfill[NB];                   // entries ever written into each batch slot (monotone)
   volatile int wcons[NB];          // generations of each batch slot consumed by the exact warps
-                                   // (a counter, not an mbarrier: one scan warp may reserve many
-                                   // batches ahead, so waiters can be several phases ahead)
   int tail;                        // window-ring entries reserved so far
-  volatile int dbg_eb[NEW];        // debug: batch each exact warp is on
   int scan_done;
   volatile int nbatch;             // batches in total, -1 until the scan warps are done
   unsigned long long surv;
@@ -175,9 +185,9 @@ __device__ __forceinline__ i64 quant(double f, float, double scale) { return __d
 
 struct Geo {
   i64 nx, ny, ntg;   // grid extents (t = global)
-  i64 x0, y0;        // tile origin
   float scale_f;
   double scale;
+  double qmax;       // |f| below this quantizes to |q| < 2^29 (int32 fast path)
 };
 
 template <typename T>
@@ -202,9 +212,9 @@ __device__ __forceinline__ void corner_grad(const Win<T>& w, const Geo& G, i64 x
   else gy = w.q(pl, cx + 1, cy + 2) - w.q(pl, cx + 1, cy);
 }
 
-// SoS sign of | ua va ; ub vb | (rows a < b in global vertex order) given its exact value d;
-// perturbation eps_{r,j} = eps^(2^(2r+j)) (R4): the leading terms of det(M + E) in
-// decreasing magnitude are det, +v_b, -u_b, -v_a, then the constant -1.
+// SoS sign of | ua va ; ub vb | (rows a < b in global vertex order) given the sign of its exact
+// value; perturbation eps_{r,j} = eps^(2^(2r+j)) (R4): the leading terms of det(M + E)
+// in decreasing magnitude are det, +v_b, -u_b, -v_a, then the constant -1.
 __device__ __forceinline__ int sos_sign(int ds, i64 ua, i64 va, i64 ub, i64 vb) {
   if (ds) return ds;
   if (vb) return vb > 0 ? 1 : -1;
@@ -223,8 +233,8 @@ __device__ __forceinline__ void masks_of(int ty, int& m1, int& m2, std::integer_
   ((ty == K ? (m1 = Face3<K>::m1, m2 = Face3<K>::m2, 0) : 0), ...);
 }
 
-// Face test from precomputed determinant signs: point-in-simplex for the face
-// (0, m1, m2): s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
+// generic face test from the exact determinant signs: point-in-simplex for the
+// face (0, m1, m2): s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
 template <int K>
 __device__ __forceinline__ void face_test(const i64 (&g)[8][2], const int (&s0k)[8], const int (&sp)[12],
                                           uint32_t exists, uint32_t& pmask) {
@@ -250,9 +260,10 @@ __device__ __forceinline__ void pair_signs(const i64 (&g)[8][2], int (&sp)[12], 
   ((sp[K] = det_sign<WIDE>(g[Face3<K>::m1], g[Face3<K>::m2])), ...);
 }
 
-// Punctured face types of one cube (window w, anchor (x, y)).
+// Punctured face types of one cube -- the general path: any position (boundary rules, missing
+// corners), int64 gradients, int128 determinants when needed, full SoS chains.
 template <typename T>
-__device__ __forceinline__ uint32_t cube_faces(const Win<T>& w, const Geo& G, i64 x, i64 y, bool hasB) {
+__device__ __noinline__ uint32_t cube_faces_general(const Win<T>& w, const Geo& G, i64 x, i64 y, bool hasB) {
   i64 g[8][2];
   uint32_t exists = 0;
   bool wide = false;
@@ -266,7 +277,6 @@ __device__ __forceinline__ uint32_t cube_faces(const Win<T>& w, const Geo& G, i6
     exists |= (ex ? 1u : 0u) << c;
     wide |= ((gx < 0 ? -gx : gx) | (gy < 0 ? -gy : gy)) >= (1ll << 31);
   }
-  // the 19 distinct determinants of the 12 faces: (0, k) for k = 1..7 and (m1, m2) per type
   int s0k[8], sp[12];
   s0k[0] = 0;
   uint32_t pmask = 0;
@@ -281,6 +291,60 @@ __device__ __forceinline__ uint32_t cube_faces(const Win<T>& w, const Geo& G, i6
   }
   all_faces(g, s0k, sp, exists, pmask, std::make_integer_sequence<int, 12>{});
   return pmask;
+}
+
+// int32 fast path: interior cube with both planes, |q| < 2^29 on the window, no zero determinant.
+// Returns false when the general path is needed.
+template <typename T>
+__device__ __forceinline__ bool cube_faces_fast(const T* W, const Geo& G, uint32_t& pmask) {
+  // the 24 window values the 8 corner gradients use (the 4 window corners per plane are not needed)
+  float mx = 0.f;
+  int q[2][4][4];
+#pragma unroll
+  for (int pl = 0; pl < 2; ++pl)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if ((r == 0 || r == 3) && (c == 0 || c == 3)) continue;
+        const T f = W[pl * 16 + r * 4 + c];
+        mx = fmaxf(mx, fabsf((float)f));
+        q[pl][r][c] = (int)quant(f, G.scale_f, G.scale);
+      }
+  if (!(mx < (float)G.qmax)) return false;  // also catches NaN
+  int g[8][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
+    g[c][0] = q[pl][cy + 1][cx + 2] - q[pl][cy + 1][cx];
+    g[c][1] = q[pl][cy + 2][cx + 1] - q[pl][cy][cx + 1];
+  }
+  // determinants (0, k) and (m1, m2): |g| < 2^30 so |det| < 2^61
+  i64 d0[8], dp[12];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) d0[k] = (i64)g[0][0] * g[k][1] - (i64)g[0][1] * g[k][0];
+  bool zero = false;
+#pragma unroll
+  for (int k = 1; k < 8; ++k) zero |= d0[k] == 0;
+#define FTK_DP(K)                                                                                    \
+  dp[K] = (i64)g[Face3<K>::m1][0] * g[Face3<K>::m2][1] - (i64)g[Face3<K>::m1][1] * g[Face3<K>::m2][0]; \
+  zero |= dp[K] == 0;
+  FTK_DP(0) FTK_DP(1) FTK_DP(2) FTK_DP(3) FTK_DP(4) FTK_DP(5)
+  FTK_DP(6) FTK_DP(7) FTK_DP(8) FTK_DP(9) FTK_DP(10) FTK_DP(11)
+#undef FTK_DP
+  if (zero) return false;
+  // s0 = sgn D(m1,m2), s1 = -sgn D(0,m2), s2 = sgn D(0,m1): punctured iff all equal
+  uint32_t m = 0;
+#define FTK_FACE(K)                                                                  \
+  {                                                                                  \
+    const bool a = dp[K] < 0, b = d0[Face3<K>::m2] > 0, c = d0[Face3<K>::m1] < 0;    \
+    m |= (uint32_t)(a == b && b == c) << K;                                          \
+  }
+  FTK_FACE(0) FTK_FACE(1) FTK_FACE(2) FTK_FACE(3) FTK_FACE(4) FTK_FACE(5)
+  FTK_FACE(6) FTK_FACE(7) FTK_FACE(8) FTK_FACE(9) FTK_FACE(10) FTK_FACE(11)
+#undef FTK_FACE
+  pmask = m;
+  return true;
 }
 
 __device__ __forceinline__ double dot3_nofma(const double* mu, double a, double b, double c) {
@@ -387,13 +451,18 @@ template <typename T>
 __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G, const ExtractParams& P) {
   const int lane = threadIdx.x & 31;
   const int e = base_entry + lane;
-  const uint32_t mt = sm.meta[e];
-  const bool valid = mt != META_INVALID;
-  const i64 x = G.x0 + (mt & 255u), y = G.y0 + ((mt >> 8) & 127u), t = sm.qt[e];
-  const bool hasB = (mt >> 15) & 1u;
-  const Win<T> w{sm.win + e * WSTRIDE, G.scale_f, G.scale};
-  const uint32_t pmask = valid ? cube_faces<T>(w, G, x, y, hasB) : 0u;
-  // redistribute the punctured faces over the lanes
+  const int qtv = sm.qt[e];
+  const bool valid = qtv != -1;
+  const i64 x = sm.qx[e], y = sm.qy[e], t = qtv & 0x7fffffff;
+  const bool hasB = (qtv >> 31) & 1;
+  const T* W = sm.win + e * WSTRIDE;
+  uint32_t pmask = 0;
+  if (valid) {
+    const bool interior = x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny && hasB;
+    if (!(interior && cube_faces_fast<T>(W, G, pmask)))
+      pmask = cube_faces_general<T>(Win<T>{W, G.scale_f, G.scale}, G, x, y, hasB);
+  }
+  // spread the punctured faces over the lanes
   const int cnt = __popc(pmask);
   int incl = cnt;
 #pragma unroll
@@ -420,9 +489,8 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   for (int i = lane; i < total; i += 32) {
     const int it = items[i];
     const int le = base_entry + (it & 31), ty = it >> 5;
-    const uint32_t m2 = sm.meta[le];
     const Win<T> w2{sm.win + le * WSTRIDE, G.scale_f, G.scale};
-    emit_record<T>(w2, G, P, G.x0 + (m2 & 255u), G.y0 + ((m2 >> 8) & 127u), sm.qt[le], ty, obase + i);
+    emit_record<T>(w2, G, P, sm.qx[le], sm.qy[le], sm.qt[le] & 0x7fffffff, ty, obase + i);
   }
   __syncwarp();
 }
@@ -435,8 +503,12 @@ struct Row {
   T l, a, b, c, d, r;  // f[x-1], f[x..x+3], f[x+4]
 };
 
-template <typename T>
-__device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane) {
+// One row of the lane's 4 positions plus neighbours.  Boundary patch (EDGE): at x = 0 the left
+// neighbour becomes f[0] and at x = nx - 1 the right neighbour becomes f[nx-1], so the central
+// difference formula yields the one-sided difference of DESIGN.md R7 (values at x >= nx only feed
+// positions whose codes are masked).
+template <typename T, bool EDGE>
+__device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane, int rpos, bool lpat) {
   Row<T> w;
   const T* p = S + srow * PITCH + XOFF + 4 * lane;
   if constexpr (sizeof(T) == 4) {
@@ -455,13 +527,21 @@ __device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane) {
   }
   w.l = up;
   w.r = dn;
+  if (EDGE) {
+    // lpat: x = 0 is this lane's position 0; rpos: position (0..3) of x = nx - 1, else -1
+    if (lpat) w.l = w.a;
+    if (rpos == 0) w.b = w.a;
+    if (rpos == 1) w.c = w.b;
+    if (rpos == 2) w.d = w.c;
+    if (rpos == 3) w.r = w.d;
+  }
   return w;
 }
 
 // 16-bit row code, position i in nibble (3 - i); nibble bits 3..0 = NOT(dx >= thr), NOT(dx < -thr),
 // NOT(dy >= thr), NOT(dy < -thr) -- the sign bits of dx - thr, ~(dx + thr), dy - thr, ~(dy + thr).
-__device__ __forceinline__ uint32_t row_code_fast(const Row<float>& up, const Row<float>& cur, const Row<float>& dn,
-                                                  f2 thr2) {
+__device__ __forceinline__ uint32_t row_code(const Row<float>& up, const Row<float>& cur, const Row<float>& dn,
+                                             f2 thr2, float) {
   const f2 dx01 = sub2(pack2(cur.b, cur.c), pack2(cur.l, cur.a));
   const f2 dx23 = sub2(pack2(cur.d, cur.r), pack2(cur.b, cur.c));
   const f2 dy01 = sub2(pack2(dn.a, dn.b), pack2(up.a, up.b));
@@ -478,36 +558,20 @@ __device__ __forceinline__ uint32_t row_code_fast(const Row<float>& up, const Ro
   return W ^ 0x5555u;
 }
 
-template <typename T>
-__device__ __forceinline__ uint32_t sign_bit(T v) {
-  if constexpr (sizeof(T) == 4) return __float_as_uint(v) >> 31;
-  else return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63);
+__device__ __forceinline__ uint32_t sign_bit(double v) {
+  return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63);
 }
-
-// generic row code: any dtype, one-sided differences at the spatial boundary, neutral (0) nibbles
-// for positions outside the grid
-template <typename T, bool EDGE>
-__device__ __forceinline__ uint32_t row_code_generic(const Row<T>& up, const Row<T>& cur, const Row<T>& dn, T thr,
-                                                     i64 gx, i64 gy, i64 nx, i64 ny) {
-  const T f[6] = {cur.l, cur.a, cur.b, cur.c, cur.d, cur.r};
-  const T fu[4] = {up.a, up.b, up.c, up.d};
-  const T fd[4] = {dn.a, dn.b, dn.c, dn.d};
+__device__ __forceinline__ uint32_t row_code(const Row<double>& up, const Row<double>& cur, const Row<double>& dn,
+                                             f2, double thr) {
+  const double f[6] = {cur.l, cur.a, cur.b, cur.c, cur.d, cur.r};
+  const double fu[4] = {up.a, up.b, up.c, up.d};
+  const double fd[4] = {dn.a, dn.b, dn.c, dn.d};
   uint32_t W = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    T lo = f[i], hi = f[i + 2], ylo = fu[i], yhi = fd[i];
-    if (EDGE) {
-      const i64 x = gx + i;
-      if (x == 0) lo = f[i + 1];
-      if (x == nx - 1) hi = f[i + 1];
-      if (gy == 0) ylo = f[i + 1];
-      if (gy == ny - 1) yhi = f[i + 1];
-    }
-    const T dx = hi - lo, dy = yhi - ylo;
-    uint32_t nib = (sign_bit<T>(dx - thr) << 3) | ((sign_bit<T>(dx + thr) ^ 1u) << 2) |
-                   (sign_bit<T>(dy - thr) << 1) | (sign_bit<T>(dy + thr) ^ 1u);
-    if (EDGE && (gx + i >= nx || gy >= ny)) nib = 0u;  // no such corner: OR-neutral
-    W = (W << 4) | nib;
+    const double dx = f[i + 2] - f[i], dy = fd[i] - fu[i];
+    W = (W << 4) | (sign_bit(dx - thr) << 3) | ((sign_bit(dx + thr) ^ 1u) << 2) | (sign_bit(dy - thr) << 1) |
+        (sign_bit(dy + thr) ^ 1u);
   }
   return W;
 }
@@ -536,15 +600,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   G.nx = P.nx;
   G.ny = P.ny;
   G.ntg = P.nt_global;
-  G.x0 = (i64)blockIdx.x * TX;
-  G.y0 = (i64)blockIdx.y * TY;
   G.scale = P.scale;
   G.scale_f = (float)P.scale;
-  const i64 ta = P.ta + (i64)blockIdx.z * P.tchunk;
-  const i64 tb = min(ta + P.tchunk, P.tb);           // anchor planes [ta, tb)
-  const i64 plast = min(tb, P.nt_global - 1);         // planes ta .. plast are loaded
-  const int nplanes = (int)(plast - ta + 1);
+  G.qmax = ldexp(1.0, 29) / P.scale - 1.0 / P.scale;  // |f| < qmax -> |rint(f 2^s)| < 2^29
   constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
+  const int ntx = (int)((G.nx + TX - 1) / TX), nty = (int)((G.ny + TY - 1) / TY);
+  const int ntz = (int)((P.tb - P.ta + TCHUNK - 1) / TCHUNK);
+  const long long nitems = (long long)ntx * nty * ntz;
 
   if (tid == 0) {
     sm.surv = 0;
@@ -561,7 +623,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       sm.wfill[b] = 0;
       sm.wcons[b] = 0;
     }
-    for (int e = 0; e < NEW; ++e) sm.dbg_eb[e] = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -569,32 +630,64 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   if (warp == PRODUCER) {
     // ------------------------------------------------------------------ producer warp
     const T* field = reinterpret_cast<const T*>(P.field);
-    for (int k = 0; k < nplanes; ++k) {
-      const int s = k % NSTAGE;
-      if (k >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)((k / NSTAGE - 1) & 1), 1, k);
-      if (TMA) {
+    int gk = 0;  // planes issued so far (ring position)
+    auto acquire = [&](int s) {
+      if (gk >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
+    };
+    while (true) {
+      long long item = 0;
+      if (lane == 0) item = (long long)atomicAdd(&P.counters[CNT_WORK], 1ull);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= nitems) break;
+      const int tx = (int)(item % ntx), ty_ = (int)((item / ntx) % nty), tz = (int)(item / ((long long)ntx * nty));
+      const i64 x0 = (i64)tx * TX, y0 = (i64)ty_ * TY;
+      const i64 ta = P.ta + (i64)tz * TCHUNK;
+      const i64 tb = min(ta + TCHUNK, P.tb);
+      const i64 plast = min(tb, P.nt_global - 1);
+      const int np = (int)(plast - ta + 1);
+      for (int k = 0; k < np; ++k, ++gk) {
+        const int s = gk % NSTAGE;
+        acquire(s);
         if (lane == 0) {
-          mbar_expect_tx(&sm.full[s], STAGE_BYTES);
-          tma_load_3d(sm.plane[s], &tmap, &sm.full[s], (int)(G.x0 - XOFF), (int)(G.y0 - YOFF), (int)(ta + k - P.t0));
+          StageMeta& m = sm.meta[s];
+          m.x0 = (int)x0;
+          m.y0 = (int)y0;
+          m.p = (int)(ta + k);
+          m.k = k;
+          m.nplanes = np;
+          m.tb = (int)tb;
+          m.done = 0;
         }
-      } else {
-        // generic loader for unaligned shapes: guarded element loads (zero outside the grid)
-        const T* src = field + (ta + k - P.t0) * G.nx * G.ny;
-        T* dst = sm.plane[s];
-        for (int idx = lane; idx < ROWS * PITCH; idx += 32) {
-          const int rr = idx / PITCH, cc = idx - rr * PITCH;
-          const i64 yy = G.y0 - YOFF + rr, xx = G.x0 - XOFF + cc;
-          dst[idx] = (yy >= 0 && yy < G.ny && xx >= 0 && xx < G.nx) ? src[yy * G.nx + xx] : (T)0;
+        if (TMA) {
+          if (lane == 0) {
+            mbar_expect_tx(&sm.full[s], STAGE_BYTES);
+            tma_load_3d(sm.plane[s], &tmap, &sm.full[s], (int)(x0 - XOFF), (int)(y0 - YOFF), (int)(ta + k - P.t0));
+          }
+        } else {
+          // generic loader for unaligned shapes: guarded element loads (zero outside the grid)
+          const T* src = field + (ta + k - P.t0) * G.nx * G.ny;
+          T* dst = sm.plane[s];
+          for (int idx = lane; idx < ROWS * PITCH; idx += 32) {
+            const int rr = idx / PITCH, cc = idx - rr * PITCH;
+            const i64 yy = y0 - YOFF + rr, xx = x0 - XOFF + cc;
+            dst[idx] = (yy >= 0 && yy < G.ny && xx >= 0 && xx < G.nx) ? src[yy * G.nx + xx] : (T)0;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.full[s]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.full[s]);
       }
+    }
+    // end-of-work marker
+    const int s = gk % NSTAGE;
+    acquire(s);
+    if (lane == 0) {
+      sm.meta[s].done = 1;
+      mbar_arrive(&sm.full[s]);
     }
   } else if (warp > PRODUCER) {
     // ------------------------------------------------------------------ exact warps
     const int ew = warp - PRODUCER - 1;
     for (int b = ew;; b += NEW) {
-      if (lane == 0) sm.dbg_eb[ew] = b;
       const int j = b % NB;
       bool go = true;
       const int target = 32 * (b / NB + 1);
@@ -610,8 +703,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(4, b, nbf);
         }
       }
-      __threadfence_block();
       if (!go) break;
+      __threadfence_block();
       process_batch<T>(sm, ew, j * 32, G, P);
       __syncwarp();
       if (lane == 0) {
@@ -621,11 +714,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
   } else {
     // ------------------------------------------------------------------ scan warps
-    const i64 gx = G.x0 + 4 * lane;          // first x of this lane
-    const i64 gy0 = G.y0 + warp * RW;        // first anchor row of this warp
-    const int srow0 = YOFF + warp * RW;      // its smem row
-    const bool xedge = G.x0 < 1 || G.x0 + LX + 1 > G.nx;
-    const bool edge = xedge || gy0 < 1 || gy0 + RW + 2 > G.ny;  // code rows gy0 .. gy0+RW in [1, ny-2]
     const T thr = (T)P.thr;
     const f2 thr2 = pack2((float)P.thr, (float)P.thr);
     uint32_t maxb32 = 0;
@@ -635,58 +723,11 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     // window copy: lane k copies element k = (pl, r, c) of the 4x4x2 window
     const int c_pl = lane >> 4, c_r = (lane >> 2) & 3, c_c = lane & 3;
     const int c_off = (c_r - 1 + YOFF) * PITCH + (c_c - 1 + XOFF);
+    const int srow0 = YOFF + warp * RW;  // smem row of this warp's first anchor row
 
-    auto scan_plane = [&](const T* S, uint32_t* Sq) {
-      Row<T> up = load_row<T>(S, srow0 - 1, lane);
-      Row<T> cur = load_row<T>(S, srow0, lane);
-      uint32_t Cprev = 0;
-#pragma unroll
-      for (int r = 0; r <= RW; ++r) {
-        const Row<T> dn = load_row<T>(S, srow0 + r + 1, lane);
-        if (r < RW) {
-          if constexpr (sizeof(T) == 4) {
-            maxb32 = max_abs_bits(maxb32, cur.a, cur.b, cur.c, cur.d);
-          } else {
-            maxd = fmax(maxd, fmax(fmax(fabs(cur.a), fabs(cur.b)), fmax(fabs(cur.c), fabs(cur.d))));
-            if (cur.a != cur.a || cur.b != cur.b || cur.c != cur.c || cur.d != cur.d)
-              maxd = __longlong_as_double(0x7ff8000000000000ll);
-          }
-        }
-        uint32_t C;
-        if constexpr (sizeof(T) == 4) {
-          C = edge ? row_code_generic<T, true>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny)
-                   : row_code_fast(up, cur, dn, thr2);
-        } else {
-          C = edge ? row_code_generic<T, true>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny)
-                   : row_code_generic<T, false>(up, cur, dn, thr, gx, gy0 + r, G.nx, G.ny);
-        }
-        if (r > 0) {
-          const uint32_t Y = Cprev | C;                                   // y-pair
-          const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1) >> 12;  // next lane's position 0
-          Sq[r - 1] = (Y | (Y << 4) | nb) & 0xFFFFu;                      // x-pair
-        }
-        Cprev = C;
-        up = cur;
-        cur = dn;
-      }
-    };
-
-    // survivors of one anchor plane: bit (4r + j) <-> row r, position 3 - j
-    auto survivors_of = [&](const uint32_t* K) {
-      uint32_t mask = 0;
-#pragma unroll
-      for (int r = 0; r < RW; ++r) {
-        uint32_t z = K[r] & (K[r] >> 1);
-        z &= z >> 2;
-        const uint32_t m = z & 0x1111u;                  // nibble all ones -> survivor
-        mask |= (((m * 0x249u) >> 9) & 0xFu) << (4 * r); // gather bits 0,4,8,12 -> 0..3
-      }
-      return lane == 31 ? 0u : mask;                     // the halo lane owns no anchors
-    };
-
-    // hand the survivors to the exact warps: reserve ring entries, copy each cube's 4x4x2 window
-    // (planes A = t, B = t+1), publish on the batch's wfull barrier
-    auto enqueue = [&](uint32_t mask, const T* A, const T* B, i64 t) {
+    // hand the survivors (bit 4r + j <-> row r, position 3 - j) to the exact warps: reserve ring
+    // entries, copy each cube's 4x4x2 window (planes A = t, B = t+1), publish per batch slot
+    auto enqueue = [&](uint32_t mask, const T* A, const T* B, int t, int x0, int y0) {
       const int cnt = __popc(mask);
       int incl = cnt;
 #pragma unroll
@@ -700,8 +741,29 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       int base = 0;
       if (lane == 0) base = atomicAdd(&sm.tail, total);
       base = __shfl_sync(0xffffffffu, base, 0);
-      int myfirst = incl - cnt;
-      int i = 0;
+      const int tflag = (int)((uint32_t)t | (B ? 0x80000000u : 0u));
+      const T* B2 = B ? B : A;
+      int e = base, pending = 0;
+      // claim the first slot
+      auto claim = [&](int ee) {
+        const int bat = ee >> 5, slot = bat % NB;
+        if (bat >= NB && sm.wcons[slot] < bat / NB) {
+          const unsigned long long t0 = gtimer_ns();
+          while (sm.wcons[slot] < bat / NB) {
+            __nanosleep(32);
+            if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(2, bat, ee);
+          }
+          __threadfence_block();
+        }
+      };
+      auto publish = [&](int ee, int n) {  // n entries ending before ee in one batch slot
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicAdd(&sm.wfill[((ee - 1) >> 5) % NB], n);
+        }
+      };
+      claim(e);
       while (true) {
         const uint32_t have = __ballot_sync(0xffffffffu, mask != 0);
         if (!have) break;
@@ -713,62 +775,130 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           h &= h - 1;
           const int b = __shfl_sync(0xffffffffu, myb, L);
           const int xl = 4 * L + 3 - (b & 3), yl = warp * RW + (b >> 2);
-          const int e = base + i++;
-          const int bat = e >> 5, slot = bat % NB, pos = e & (RING - 1);
-          if ((e & 31) == 0 || i == 1) {
-            // first write into this batch slot for this warp: the slot's previous generation
-            // must have been consumed
-            if (bat >= NB && sm.wcons[slot] < bat / NB) {
-              const unsigned long long t0 = gtimer_ns();
-              while (sm.wcons[slot] < bat / NB) {
-                __nanosleep(32);
-                if (gtimer_ns() - t0 > 2000000000ull) {
-                  if (lane == 0)
-                    printf("ring stall: warp %d e=%d bat=%d tail=%d nbatch=%d exact=[%d %d %d]\n", warp, e, bat,
-                           *(volatile int*)&sm.tail, sm.nbatch, sm.dbg_eb[0], sm.dbg_eb[1], sm.dbg_eb[2]);
-                  wait_timeout(2, bat, e);
-                }
-              }
-              __threadfence_block();
-            }
-          }
-          const T* src = (c_pl ? (B ? B : A) : A) + yl * PITCH + xl + c_off;
-          sm.win[pos * WSTRIDE + lane] = *src;
+          const int pos = e & (RING - 1);
+          sm.win[pos * WSTRIDE + lane] = (c_pl ? B2 : A)[yl * PITCH + xl + c_off];
           if (lane == 0) {
-            sm.meta[pos] = (uint32_t)xl | ((uint32_t)yl << 8) | ((B ? 1u : 0u) << 15);
-            sm.qt[pos] = (int)t;
+            sm.qx[pos] = x0 + xl;
+            sm.qy[pos] = y0 + yl;
+            sm.qt[pos] = tflag;
           }
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence_block();
-            atomicAdd(&sm.wfill[slot], 1);
+          ++e;
+          ++pending;
+          if ((e & 31) == 0) {  // batch slot complete for this warp
+            publish(e, pending);
+            pending = 0;
+            if (e < base + total) claim(e);
           }
         }
       }
-      (void)myfirst;
+      if (pending) publish(e, pending);
     };
 
-    for (int k = 0; k < nplanes; ++k) {
-      const i64 p = ta + k;
-      const int s = k % NSTAGE;
+    int gk = 0;
+    int prev_s = 0;
+    int x0 = -1, y0 = -1;
+    bool edge = false;
+    int rpos = -1;            // boundary patches of this lane (see load_row)
+    bool lpat = false;
+    uint32_t xmask = 0xFFFFu; // codes of positions outside the grid are cleared
+    while (true) {
+      const int s = gk % NSTAGE;
+      mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk);
+      const StageMeta m = sm.meta[s];
+      if (m.done) break;
+      if (m.k == 0) {
+        x0 = m.x0;
+        y0 = m.y0;
+        const i64 gx = (i64)x0 + 4 * lane;
+        const i64 gy0 = (i64)y0 + warp * RW;
+        edge = x0 < 1 || x0 + LX + 1 > G.nx || gy0 < 1 || gy0 + RW + 2 > G.ny;
+        lpat = gx == 0;
+        rpos = (G.nx - 1 >= gx && G.nx - 1 <= gx + 3) ? (int)(G.nx - 1 - gx) : -1;
+        xmask = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (gx + i < G.nx) xmask |= 0xFu << (4 * (3 - i));
+      }
       const T* S = sm.plane[s];
-      mbar_wait(&sm.full[s], (uint32_t)((k / NSTAGE) & 1), 3, k);
       uint32_t Sq[RW];
-      scan_plane(S, Sq);
-      if (k > 0) {
+      {
+        // scan the plane: code rows y0w .. y0w + RW, squares for rows y0w .. y0w + RW - 1
+        const i64 gy0 = (i64)y0 + warp * RW;
+        Row<T> up, cur;
+        if (edge) {
+          up = load_row<T, true>(S, srow0 - 1, lane, rpos, lpat);
+          cur = load_row<T, true>(S, srow0, lane, rpos, lpat);
+        } else {
+          up = load_row<T, false>(S, srow0 - 1, lane, rpos, lpat);
+          cur = load_row<T, false>(S, srow0, lane, rpos, lpat);
+        }
+        uint32_t Cprev = 0;
+#pragma unroll
+        for (int r = 0; r <= RW; ++r) {
+          Row<T> dn = edge ? load_row<T, true>(S, srow0 + r + 1, lane, rpos, lpat)
+                           : load_row<T, false>(S, srow0 + r + 1, lane, rpos, lpat);
+          if (r < RW) {
+            if constexpr (sizeof(T) == 4) {
+              maxb32 = max_abs_bits(maxb32, cur.a, cur.b, cur.c, cur.d);
+            } else {
+              maxd = fmax(maxd, fmax(fmax(fabs(cur.a), fabs(cur.b)), fmax(fabs(cur.c), fabs(cur.d))));
+              if (cur.a != cur.a || cur.b != cur.b || cur.c != cur.c || cur.d != cur.d)
+                maxd = __longlong_as_double(0x7ff8000000000000ll);
+            }
+          }
+          uint32_t C;
+          if (edge) {
+            // one-sided differences in y at the boundary rows; rows outside the grid are neutral
+            const i64 gy = gy0 + r;
+            Row<T> u2 = up, d2 = dn;
+            if (gy == 0) u2 = cur;
+            if (gy == G.ny - 1) d2 = cur;
+            C = row_code(u2, cur, d2, thr2, thr) & xmask;
+            if (gy >= G.ny) C = 0;
+          } else {
+            C = row_code(up, cur, dn, thr2, thr);
+          }
+          if (r > 0) {
+            const uint32_t Y = Cprev | C;                                   // y-pair
+            const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1) >> 12;  // next lane's position 0
+            Sq[r - 1] = (Y | (Y << 4) | nb) & 0xFFFFu;                      // x-pair
+          }
+          Cprev = C;
+          up = cur;
+          cur = dn;
+        }
+      }
+      // survivors: nibble all ones after the OR over the cube's corners
+      auto survivors_of = [&](const uint32_t* K) {
+        uint32_t mask = 0;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+          uint32_t z = K[r] & (K[r] >> 1);
+          z &= z >> 2;
+          const uint32_t mm = z & 0x1111u;
+          mask |= (((mm * 0x249u) >> 9) & 0xFu) << (4 * r);  // gather bits 0,4,8,12 -> 0..3
+        }
+        return lane == 31 ? 0u : mask;  // the halo lane owns no anchors
+      };
+      if (m.k > 0) {
         uint32_t K[RW];
 #pragma unroll
         for (int r = 0; r < RW; ++r) K[r] = prevSq[r] | Sq[r];
-        enqueue(survivors_of(K), sm.plane[(k - 1) % NSTAGE], S, p - 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[(k - 1) % NSTAGE]);  // plane p-1 no longer needed
+        enqueue(survivors_of(K), sm.plane[prev_s], S, m.p - 1, x0, y0);
+      }
+      if (m.p == P.nt_global - 1 && m.p < m.tb) {
+        // anchors on the last timestep: no t+1 corners, the OR runs over the plane only
+        enqueue(survivors_of(Sq), S, nullptr, m.p, x0, y0);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (m.k > 0) mbar_arrive(&sm.empty[prev_s]);          // plane p-1 no longer needed
+        if (m.k == m.nplanes - 1) mbar_arrive(&sm.empty[s]);  // last plane of the item
       }
 #pragma unroll
       for (int r = 0; r < RW; ++r) prevSq[r] = Sq[r];
-      if (p == P.nt_global - 1 && p < tb) {
-        // anchors on the last timestep: no t+1 corners, the OR runs over the plane only
-        enqueue(survivors_of(Sq), S, nullptr, p);
-      }
+      prev_s = s;
+      ++gk;
     }
 
     // the last scan warp to finish pads the final partial batch and publishes the batch count
@@ -782,8 +912,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int nb = (n + 31) >> 5;
       const int pad = nb * 32 - n;
       if (pad) {
-        const int bat = nb - 1, slot = bat % NB;
-        if (lane < pad) sm.meta[(n + lane) & (RING - 1)] = META_INVALID;
+        const int slot = (nb - 1) % NB;
+        if (lane < pad) sm.qt[(n + lane) & (RING - 1)] = -1;
         __syncwarp();
         if (lane == 0) {
           __threadfence_block();
@@ -856,19 +986,23 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   const size_t smem = sizeof(Smem<T>) + 128;
   auto kern = k_extract2d<T, TMA>;
   FTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const dim3 grid((unsigned)((P.nx + TX - 1) / TX), (unsigned)((P.ny + TY - 1) / TY),
-                  (unsigned)((P.tb - P.ta + P.tchunk - 1) / P.tchunk));
-  if (grid.z == 0) return FTK_OK;
-  kern<<<grid, NTHREADS, smem, stream>>>(map, P);
+  int dev = 0, sms = 148, per_sm = 0;
+  FTK_CUDA_TRY(cudaGetDevice(&dev));
+  FTK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem));
+  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY) * ((P.tb - P.ta + TCHUNK - 1) / TCHUNK);
+  if (items <= 0) return FTK_OK;
+  const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }
 
 int launch_extract2d(const ExtractParams& P, cudaStream_t stream) {
   const size_t esz = P.dtype == FTK_F32 ? 4 : 8;
-  const bool aligned = (reinterpret_cast<uintptr_t>(P.field) % 16 == 0) && ((P.nx * esz) % 16 == 0) &&
-                       P.nx < (1ll << 31) && P.ny < (1ll << 31) && P.nt_buf < (1ll << 31);
+  const bool aligned = (reinterpret_cast<uintptr_t>(P.field) % 16 == 0) && ((P.nx * esz) % 16 == 0);
   const bool tma = aligned && get_encode() != nullptr && !P.force_generic;
+  if (P.nx >= (1ll << 31) - 256 || P.ny >= (1ll << 31) - 64 || P.nt_global >= (1ll << 31)) return FTK_ERR_INVALID_ARG;
   if (P.dtype == FTK_F32) return tma ? launch_t<float, true>(P, stream) : launch_t<float, false>(P, stream);
   return tma ? launch_t<double, true>(P, stream) : launch_t<double, false>(P, stream);
 }
