@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libftk_cp.so")
+LIB_PATH = os.environ.get("FTK_LIB") or os.path.join(_HERE, "libftk_cp.so")
 
 OK, ERR_INVALID_ARG, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_INVARIANT, ERR_NOMEM = range(8)
 F32, F64 = 0, 1

@@ -51,6 +51,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment builds: the same sources with -D overrides into libftk_cp_<name>.so (selected at run
+    time with FTK_LIB=<path>)."""
+    objdir = os.path.join(HERE, "build", name)
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        subprocess.check_call([NVCC, *ARCH, *FLAGS[:-2], *[f"-D{d}" for d in defines], "-c", src, "-o", obj])
+        objs.append(obj)
+    out = os.path.join(HERE, f"libftk_cp_{name}.so")
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -125,17 +125,39 @@ constexpr int TX = 124;             // anchors owned per tile in x: lane 31 is a
                                     // only complete lane 30's cubes (a cube needs its x+1 corners)
 constexpr int RW = 4;               // anchor rows per scan warp
 constexpr int NSW = 8;              // scan warps
-constexpr int PRODUCER = NSW;       // warp index of the TMA producer
 constexpr int NEW = 3;              // exact warps
 constexpr int NWARPS = NSW + 1 + NEW;
+// Roles by warp id.  A warp runs on SMSP (id % 4): the exact warps get SMSP 3 to themselves (ids
+// 3, 7, 11) so their large code does not evict the scan loop from the per-SMSP instruction cache;
+// the producer is id 10; ids 0-2, 4-6, 8-9 scan.
+#ifndef FTK_K1_REMAP
+#define FTK_K1_REMAP 0
+#endif
+#if FTK_K1_REMAP
+constexpr int PRODUCER = 10;
+__host__ __device__ constexpr bool is_exact(int w) { return (w & 3) == 3; }
+__host__ __device__ constexpr int exact_index(int w) { return w >> 2; }
+__host__ __device__ constexpr int scan_index(int w) { return w - (w >> 2); }
+#else
+constexpr int PRODUCER = NSW;
+__host__ __device__ constexpr bool is_exact(int w) { return w > NSW; }
+__host__ __device__ constexpr int exact_index(int w) { return w - NSW - 1; }
+__host__ __device__ constexpr int scan_index(int w) { return w; }
+#endif
 constexpr int NTHREADS = NWARPS * 32;
 constexpr int TY = RW * NSW;        // 32 anchor rows per tile
 constexpr int XOFF = 4;             // smem column of x0
-constexpr int YOFF = 2;             // smem row of y0
+constexpr int YOFF = 1;             // smem row of y0
 constexpr int PITCH = LX + 8;       // x0-4 .. x0+131
-constexpr int ROWS = TY + 5;        // y0-2 .. y0+34
-constexpr int NSTAGE = 3;
-constexpr int NB = 8;               // window-ring batch slots (32 cubes each)
+constexpr int ROWS = TY + 3;        // y0-1 .. y0+33
+#ifndef FTK_K1_NSTAGE
+#define FTK_K1_NSTAGE 3
+#endif
+#ifndef FTK_K1_NB
+#define FTK_K1_NB 8
+#endif
+constexpr int NSTAGE = FTK_K1_NSTAGE;
+constexpr int NB = FTK_K1_NB;       // window-ring batch slots (32 cubes each)
 constexpr int RING = NB * 32;
 constexpr int WSTRIDE = 33;         // values per queued window (4x4x2 = 32, odd stride: no bank conflicts)
 constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
@@ -354,7 +376,7 @@ __device__ __forceinline__ double dot3_nofma(const double* mu, double a, double 
 // Hessian (4x scale, centre clamped into [1, N-2], R8) straight from global memory;
 // used only for partial cubes on the last row/column, whose stencil leaves the 4x4 window.
 template <typename T>
-__device__ void hessian_global(const ExtractParams& P, const Geo& G, i64 x, i64 y, i64 t, i64* H) {
+__device__ __noinline__ void hessian_global(const ExtractParams& P, const Geo& G, i64 x, i64 y, i64 t, i64* H) {
   const T* base = reinterpret_cast<const T*>(P.field) + (t - P.t0) * G.nx * G.ny;
   auto q = [&](i64 xx, i64 yy) { return quant(base[yy * G.nx + xx], G.scale_f, G.scale); };
   const i64 cx = x < 1 ? 1 : (x > G.nx - 2 ? G.nx - 2 : x);
@@ -365,8 +387,16 @@ __device__ void hessian_global(const ExtractParams& P, const Geo& G, i64 x, i64 
 }
 
 // Location (Eq. 2), type and flags of punctured face `ty` of the cube at (x, y, t); writes the record.
+#ifndef FTK_K1_REC_NOINLINE
+#define FTK_K1_REC_NOINLINE 0
+#endif
+#if FTK_K1_REC_NOINLINE
+#define FTK_REC_INL __noinline__
+#else
+#define FTK_REC_INL __forceinline__
+#endif
 template <typename T>
-__device__ void emit_record(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y, i64 t, int ty,
+__device__ FTK_REC_INL void emit_record(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y, i64 t, int ty,
                             unsigned long long slot) {
   int m[3] = {0, 0, 0};
   masks_of(ty, m[1], m[2], std::make_integer_sequence<int, 12>{});
@@ -497,83 +527,53 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
 
 // ---------------------------------------------------------------------------------------------
 // Scan
+//
+// Code layout: position i (0..3) of a lane lives in byte i; the byte's top nibble holds, from bit 7
+// down, NOT(dx >= thr), NOT(dx <= -thr), NOT(dy >= thr), NOT(dy <= -thr) -- the sign bits of
+// dx - thr, -thr - dx, dy - thr, -thr - dy (1 = that strict sign condition does not hold).  ORing
+// codes over corners and testing for an all-ones nibble finds the cubes with no one-signed
+// component.  Low nibbles are always zero; out-of-grid positions get 0 (OR-neutral).
 // ---------------------------------------------------------------------------------------------
-template <typename T>
-struct Row {
-  T l, a, b, c, d, r;  // f[x-1], f[x..x+3], f[x+4]
+struct ScanCtx {
+  int srow0;       // smem row of the warp's first anchor row
+  int lane;
+  int rpos;        // position (0..3) of x = nx - 1 in this lane, else -1
+  bool lpat;       // x = 0 is this lane's position 0
+  uint32_t xmask;  // top-nibble mask of the lane's in-grid positions
+  long long gy0;   // global y of the warp's first anchor row
+  long long ny;
 };
 
-// One row of the lane's 4 positions plus neighbours.  Boundary patch (EDGE): at x = 0 the left
-// neighbour becomes f[0] and at x = nx - 1 the right neighbour becomes f[nx-1], so the central
-// difference formula yields the one-sided difference of DESIGN.md R7 (values at x >= nx only feed
-// positions whose codes are masked).
-template <typename T, bool EDGE>
-__device__ __forceinline__ Row<T> load_row(const T* S, int srow, int lane, int rpos, bool lpat) {
-  Row<T> w;
-  const T* p = S + srow * PITCH + XOFF + 4 * lane;
-  if constexpr (sizeof(T) == 4) {
-    const float4 v = *reinterpret_cast<const float4*>(p);
-    w.a = v.x; w.b = v.y; w.c = v.z; w.d = v.w;
-  } else {
-    const double2 v0 = *reinterpret_cast<const double2*>(p);
-    const double2 v1 = *reinterpret_cast<const double2*>(p + 2);
-    w.a = v0.x; w.b = v0.y; w.c = v1.x; w.d = v1.y;
-  }
-  T up = __shfl_up_sync(0xffffffffu, w.d, 1);
-  T dn = __shfl_down_sync(0xffffffffu, w.a, 1);
-  if (lane == 0 || lane == 31) {  // tile halo from shared memory (one predicated load)
-    const T h = S[srow * PITCH + (lane == 0 ? XOFF - 1 : XOFF + LX)];
-    if (lane == 0) up = h; else dn = h;
-  }
-  w.l = up;
-  w.r = dn;
-  if (EDGE) {
-    // lpat: x = 0 is this lane's position 0; rpos: position (0..3) of x = nx - 1, else -1
-    if (lpat) w.l = w.a;
-    if (rpos == 0) w.b = w.a;
-    if (rpos == 1) w.c = w.b;
-    if (rpos == 2) w.d = w.c;
-    if (rpos == 3) w.r = w.d;
-  }
-  return w;
-}
-
-// 16-bit row code, position i in nibble (3 - i); nibble bits 3..0 = NOT(dx >= thr), NOT(dx < -thr),
-// NOT(dy >= thr), NOT(dy < -thr) -- the sign bits of dx - thr, ~(dx + thr), dy - thr, ~(dy + thr).
-__device__ __forceinline__ uint32_t row_code(const Row<float>& up, const Row<float>& cur, const Row<float>& dn,
-                                             f2 thr2, float) {
-  const f2 dx01 = sub2(pack2(cur.b, cur.c), pack2(cur.l, cur.a));
-  const f2 dx23 = sub2(pack2(cur.d, cur.r), pack2(cur.b, cur.c));
-  const f2 dy01 = sub2(pack2(dn.a, dn.b), pack2(up.a, up.b));
-  const f2 dy23 = sub2(pack2(dn.c, dn.d), pack2(up.c, up.d));
-  const f2 ax01 = sub2(dx01, thr2), ex01 = add2(dx01, thr2);
-  const f2 ax23 = sub2(dx23, thr2), ex23 = add2(dx23, thr2);
-  const f2 ay01 = sub2(dy01, thr2), ey01 = add2(dy01, thr2);
-  const f2 ay23 = sub2(dy23, thr2), ey23 = add2(dy23, thr2);
-  uint32_t W = 0;
-  W = push_sign(W, lo32(ax01)); W = push_sign(W, lo32(ex01)); W = push_sign(W, lo32(ay01)); W = push_sign(W, lo32(ey01));
-  W = push_sign(W, hi32(ax01)); W = push_sign(W, hi32(ex01)); W = push_sign(W, hi32(ay01)); W = push_sign(W, hi32(ey01));
-  W = push_sign(W, lo32(ax23)); W = push_sign(W, lo32(ex23)); W = push_sign(W, lo32(ay23)); W = push_sign(W, lo32(ey23));
-  W = push_sign(W, hi32(ax23)); W = push_sign(W, hi32(ex23)); W = push_sign(W, hi32(ay23)); W = push_sign(W, hi32(ey23));
-  return W ^ 0x5555u;
-}
-
-__device__ __forceinline__ uint32_t sign_bit(double v) {
-  return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63);
-}
-__device__ __forceinline__ uint32_t row_code(const Row<double>& up, const Row<double>& cur, const Row<double>& dn,
-                                             f2, double thr) {
-  const double f[6] = {cur.l, cur.a, cur.b, cur.c, cur.d, cur.r};
-  const double fu[4] = {up.a, up.b, up.c, up.d};
-  const double fd[4] = {dn.a, dn.b, dn.c, dn.d};
-  uint32_t W = 0;
+// gather the sign bits of the 4 conditions x 4 positions into the byte-top-nibble layout
+__device__ __forceinline__ uint32_t gather_code(const f2 (&c)[8]) {
+  // c[2*j] = condition j for positions 0,1; c[2*j+1] = condition j for positions 2,3
+  uint32_t w[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double dx = f[i + 2] - f[i], dy = fd[i] - fu[i];
-    W = (W << 4) | (sign_bit(dx - thr) << 3) | ((sign_bit(dx + thr) ^ 1u) << 2) | (sign_bit(dy - thr) << 1) |
-        (sign_bit(dy + thr) ^ 1u);
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
+    const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
+    w[j] = __byte_perm(p01, p23, 0x5410);
   }
-  return W;
+  return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
+         ((w[3] >> 3) & 0x10101010u);
+}
+
+__device__ __forceinline__ uint32_t code_f32(const float4 u, const float4 v, const float4 d, float l, float r,
+                                             f2 thr2, f2 nthr2) {
+  const f2 dx01 = sub2(pack2(v.y, v.z), pack2(l, v.x));
+  const f2 dx23 = sub2(pack2(v.w, r), pack2(v.y, v.z));
+  const f2 dy01 = sub2(pack2(d.x, d.y), pack2(u.x, u.y));
+  const f2 dy23 = sub2(pack2(d.z, d.w), pack2(u.z, u.w));
+  f2 c[8];
+  c[0] = sub2(dx01, thr2);   // dx - thr
+  c[1] = sub2(dx23, thr2);
+  c[2] = sub2(nthr2, dx01);  // -thr - dx
+  c[3] = sub2(nthr2, dx23);
+  c[4] = sub2(dy01, thr2);
+  c[5] = sub2(dy23, thr2);
+  c[6] = sub2(nthr2, dy01);
+  c[7] = sub2(nthr2, dy23);
+  return gather_code(c);
 }
 
 __device__ __forceinline__ uint32_t max_abs_bits(uint32_t m, float a, float b, float c, float d) {
@@ -583,6 +583,111 @@ __device__ __forceinline__ uint32_t max_abs_bits(uint32_t m, float a, float b, f
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(t1) : "f"(t1), "f"(t2));
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(r), "f"(t1));
   return __float_as_uint(r);
+}
+
+// Scan one plane (fp32): all RW+3 rows are loaded first (independent shared loads and shuffles),
+// then the RW+1 code rows, then the squares Sq[r] (OR over the 4 corners of each square, per
+// position).  EDGE: one-sided differences at the grid boundary by patching neighbour values.
+template <bool EDGE>
+__device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c, f2 thr2, f2 nthr2,
+                                               uint32_t (&Sq)[RW], uint32_t& maxb) {
+  constexpr int NR = RW + 3;  // rows srow0-1 .. srow0+RW+1
+  float4 v[NR];
+  float l[NR], r[NR];
+  const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
+  const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const int row = c.srow0 - 1 + i;
+    v[i] = *reinterpret_cast<const float4*>(S + row * PITCH + XOFF + 4 * c.lane);
+    const float h = S[row * PITCH + hcol];  // tile halo (used by lanes 0 and 31)
+    const float up = __shfl_up_sync(0xffffffffu, v[i].w, 1);
+    const float dn = __shfl_down_sync(0xffffffffu, v[i].x, 1);
+    l[i] = lane0 ? h : up;
+    r[i] = lane31 ? h : dn;
+    if (EDGE) {
+      if (c.lpat) l[i] = v[i].x;
+      if (c.rpos == 0) v[i].y = v[i].x;
+      if (c.rpos == 1) v[i].z = v[i].y;
+      if (c.rpos == 2) v[i].w = v[i].z;
+      if (c.rpos == 3) r[i] = v[i].w;
+    }
+  }
+#pragma unroll
+  for (int i = 1; i <= RW; ++i) maxb = max_abs_bits(maxb, v[i].x, v[i].y, v[i].z, v[i].w);
+  uint32_t C[RW + 1];
+#pragma unroll
+  for (int k = 0; k <= RW; ++k) {  // code row k = rows i = k (up), k+1 (centre), k+2 (down)
+    if (EDGE) {
+      const long long gy = c.gy0 + k;
+      const float4 u = gy == 0 ? v[k + 1] : v[k];
+      const float4 d = gy == c.ny - 1 ? v[k + 1] : v[k + 2];
+      C[k] = gy >= c.ny ? 0u : code_f32(u, v[k + 1], d, l[k + 1], r[k + 1], thr2, nthr2) & c.xmask;
+    } else {
+      C[k] = code_f32(v[k], v[k + 1], v[k + 2], l[k + 1], r[k + 1], thr2, nthr2);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+    const uint32_t Y = C[k] | C[k + 1];                      // y-pair
+    const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0 = byte 0
+    Sq[k] = Y | (Y >> 8) | (nb << 24);                       // x-pair
+  }
+}
+
+// fp64 input: same layout, scalar arithmetic
+__device__ __forceinline__ uint32_t sbit(double v) { return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63); }
+template <bool EDGE>
+__device__ __forceinline__ void scan_plane_f64(const double* S, const ScanCtx& c, double thr, uint32_t (&Sq)[RW],
+                                               double& maxd) {
+  constexpr int NR = RW + 3;
+  double f[NR][6];  // f[x-1], f[x..x+3], f[x+4]
+  const int hcol = c.lane == 0 ? XOFF - 1 : XOFF + LX;
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const double* p = S + (c.srow0 - 1 + i) * PITCH;
+    const double2 a = *reinterpret_cast<const double2*>(p + XOFF + 4 * c.lane);
+    const double2 b = *reinterpret_cast<const double2*>(p + XOFF + 4 * c.lane + 2);
+    const double h = p[hcol];
+    f[i][1] = a.x; f[i][2] = a.y; f[i][3] = b.x; f[i][4] = b.y;
+    const double up = __shfl_up_sync(0xffffffffu, b.y, 1);
+    const double dn = __shfl_down_sync(0xffffffffu, a.x, 1);
+    f[i][0] = c.lane == 0 ? h : up;
+    f[i][5] = c.lane == 31 ? h : dn;
+    if (EDGE) {
+      if (c.lpat) f[i][0] = f[i][1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c.rpos == q) f[i][q + 2] = f[i][q + 1];
+    }
+  }
+#pragma unroll
+  for (int i = 1; i <= RW; ++i)
+#pragma unroll
+    for (int q = 1; q <= 4; ++q) {
+      const double a = fabs(f[i][q]);
+      maxd = (a != a || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, a);
+    }
+  uint32_t C[RW + 1];
+#pragma unroll
+  for (int k = 0; k <= RW; ++k) {
+    const long long gy = c.gy0 + k;
+    const int iu = (EDGE && gy == 0) ? k + 1 : k, id = (EDGE && gy == c.ny - 1) ? k + 1 : k + 2;
+    uint32_t W = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double dx = f[k + 1][q + 2] - f[k + 1][q], dy = f[id][q + 1] - f[iu][q + 1];
+      const uint32_t nib = (sbit(dx - thr) << 3) | (sbit(-thr - dx) << 2) | (sbit(dy - thr) << 1) | sbit(-thr - dy);
+      W |= nib << (8 * q + 4);
+    }
+    C[k] = (EDGE && gy >= c.ny) ? 0u : (EDGE ? W & c.xmask : W);
+  }
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+    const uint32_t Y = C[k] | C[k + 1];
+    const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+    Sq[k] = Y | (Y >> 8) | (nb << 24);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -684,9 +789,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       sm.meta[s].done = 1;
       mbar_arrive(&sm.full[s]);
     }
-  } else if (warp > PRODUCER) {
+  } else if (is_exact(warp)) {
     // ------------------------------------------------------------------ exact warps
-    const int ew = warp - PRODUCER - 1;
+    const int ew = exact_index(warp);
     for (int b = ew;; b += NEW) {
       const int j = b % NB;
       bool go = true;
@@ -716,6 +821,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     // ------------------------------------------------------------------ scan warps
     const T thr = (T)P.thr;
     const f2 thr2 = pack2((float)P.thr, (float)P.thr);
+    const f2 nthr2 = pack2(-(float)P.thr, -(float)P.thr);
     uint32_t maxb32 = 0;
     double maxd = 0.0;
     unsigned long long mysurv = 0;
@@ -723,7 +829,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     // window copy: lane k copies element k = (pl, r, c) of the 4x4x2 window
     const int c_pl = lane >> 4, c_r = (lane >> 2) & 3, c_c = lane & 3;
     const int c_off = (c_r - 1 + YOFF) * PITCH + (c_c - 1 + XOFF);
-    const int srow0 = YOFF + warp * RW;  // smem row of this warp's first anchor row
+    const int sw = scan_index(warp);     // scan-warp index: anchor rows sw*RW .. sw*RW + RW - 1
+    const int srow0 = YOFF + sw * RW;    // smem row of this warp's first anchor row
 
     // hand the survivors (bit 4r + j <-> row r, position 3 - j) to the exact warps: reserve ring
     // entries, copy each cube's 4x4x2 window (planes A = t, B = t+1), publish per batch slot
@@ -774,8 +881,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           const int L = __ffs(h) - 1;
           h &= h - 1;
           const int b = __shfl_sync(0xffffffffu, myb, L);
-          const int xl = 4 * L + 3 - (b & 3), yl = warp * RW + (b >> 2);
-          const int pos = e & (RING - 1);
+          const int xl = 4 * L + (b & 3), yl = sw * RW + (b >> 2);
+          const int pos = e % RING;
           sm.win[pos * WSTRIDE + lane] = (c_pl ? B2 : A)[yl * PITCH + xl + c_off];
           if (lane == 0) {
             sm.qx[pos] = x0 + xl;
@@ -798,9 +905,14 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     int prev_s = 0;
     int x0 = -1, y0 = -1;
     bool edge = false;
-    int rpos = -1;            // boundary patches of this lane (see load_row)
-    bool lpat = false;
-    uint32_t xmask = 0xFFFFu; // codes of positions outside the grid are cleared
+    ScanCtx sc;
+    sc.srow0 = srow0;
+    sc.lane = lane;
+    sc.ny = G.ny;
+    sc.rpos = -1;
+    sc.lpat = false;
+    sc.xmask = 0xF0F0F0F0u;
+    sc.gy0 = 0;
     while (true) {
       const int s = gk % NSTAGE;
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk);
@@ -810,73 +922,34 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         x0 = m.x0;
         y0 = m.y0;
         const i64 gx = (i64)x0 + 4 * lane;
-        const i64 gy0 = (i64)y0 + warp * RW;
-        edge = x0 < 1 || x0 + LX + 1 > G.nx || gy0 < 1 || gy0 + RW + 2 > G.ny;
-        lpat = gx == 0;
-        rpos = (G.nx - 1 >= gx && G.nx - 1 <= gx + 3) ? (int)(G.nx - 1 - gx) : -1;
-        xmask = 0;
+        sc.gy0 = (i64)y0 + sw * RW;
+        edge = x0 < 1 || x0 + LX + 1 > G.nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > G.ny;
+        sc.lpat = gx == 0;
+        sc.rpos = (G.nx - 1 >= gx && G.nx - 1 <= gx + 3) ? (int)(G.nx - 1 - gx) : -1;
+        sc.xmask = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (gx + i < G.nx) xmask |= 0xFu << (4 * (3 - i));
+          if (gx + i < G.nx) sc.xmask |= 0xF0u << (8 * i);
       }
       const T* S = sm.plane[s];
       uint32_t Sq[RW];
-      {
-        // scan the plane: code rows y0w .. y0w + RW, squares for rows y0w .. y0w + RW - 1
-        const i64 gy0 = (i64)y0 + warp * RW;
-        Row<T> up, cur;
-        if (edge) {
-          up = load_row<T, true>(S, srow0 - 1, lane, rpos, lpat);
-          cur = load_row<T, true>(S, srow0, lane, rpos, lpat);
-        } else {
-          up = load_row<T, false>(S, srow0 - 1, lane, rpos, lpat);
-          cur = load_row<T, false>(S, srow0, lane, rpos, lpat);
-        }
-        uint32_t Cprev = 0;
-#pragma unroll
-        for (int r = 0; r <= RW; ++r) {
-          Row<T> dn = edge ? load_row<T, true>(S, srow0 + r + 1, lane, rpos, lpat)
-                           : load_row<T, false>(S, srow0 + r + 1, lane, rpos, lpat);
-          if (r < RW) {
-            if constexpr (sizeof(T) == 4) {
-              maxb32 = max_abs_bits(maxb32, cur.a, cur.b, cur.c, cur.d);
-            } else {
-              maxd = fmax(maxd, fmax(fmax(fabs(cur.a), fabs(cur.b)), fmax(fabs(cur.c), fabs(cur.d))));
-              if (cur.a != cur.a || cur.b != cur.b || cur.c != cur.c || cur.d != cur.d)
-                maxd = __longlong_as_double(0x7ff8000000000000ll);
-            }
-          }
-          uint32_t C;
-          if (edge) {
-            // one-sided differences in y at the boundary rows; rows outside the grid are neutral
-            const i64 gy = gy0 + r;
-            Row<T> u2 = up, d2 = dn;
-            if (gy == 0) u2 = cur;
-            if (gy == G.ny - 1) d2 = cur;
-            C = row_code(u2, cur, d2, thr2, thr) & xmask;
-            if (gy >= G.ny) C = 0;
-          } else {
-            C = row_code(up, cur, dn, thr2, thr);
-          }
-          if (r > 0) {
-            const uint32_t Y = Cprev | C;                                   // y-pair
-            const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1) >> 12;  // next lane's position 0
-            Sq[r - 1] = (Y | (Y << 4) | nb) & 0xFFFFu;                      // x-pair
-          }
-          Cprev = C;
-          up = cur;
-          cur = dn;
-        }
+      if constexpr (sizeof(T) == 4) {
+        if (edge) scan_plane_f32<true>(S, sc, thr2, nthr2, Sq, maxb32);
+        else scan_plane_f32<false>(S, sc, thr2, nthr2, Sq, maxb32);
+      } else {
+        if (edge) scan_plane_f64<true>(S, sc, (double)thr, Sq, maxd);
+        else scan_plane_f64<false>(S, sc, (double)thr, Sq, maxd);
       }
-      // survivors: nibble all ones after the OR over the cube's corners
+      // survivors: a byte whose top nibble is all ones after the OR over the cube's corners;
+      // bit 4r + i <-> anchor row r, position i
       auto survivors_of = [&](const uint32_t* K) {
         uint32_t mask = 0;
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-          uint32_t z = K[r] & (K[r] >> 1);
-          z &= z >> 2;
-          const uint32_t mm = z & 0x1111u;
-          mask |= (((mm * 0x249u) >> 9) & 0xFu) << (4 * r);  // gather bits 0,4,8,12 -> 0..3
+          uint32_t z = K[r] & (K[r] << 1);
+          z &= z << 2;
+          const uint32_t mm = (z >> 7) & 0x01010101u;                 // bits 0, 8, 16, 24
+          mask |= (((mm * 0x204081u) >> 21) & 0xFu) << (4 * r);      // -> bits 0..3
         }
         return lane == 31 ? 0u : mask;  // the halo lane owns no anchors
       };
@@ -913,7 +986,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int pad = nb * 32 - n;
       if (pad) {
         const int slot = (nb - 1) % NB;
-        if (lane < pad) sm.qt[(n + lane) & (RING - 1)] = -1;
+        if (lane < pad) sm.qt[(n + lane) % RING] = -1;
         __syncwarp();
         if (lane == 0) {
           __threadfence_block();
