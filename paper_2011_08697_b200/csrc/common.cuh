@@ -23,6 +23,7 @@ enum Counter : int {
   CNT_INVARIANT = 3,  // link: faces whose parent cell does not hold exactly one other punctured face
   CNT_EXPORT = 4,     // slab stitch: exported boundary faces
   CNT_WORK = 5,       // K1 persistent scheduler: next work item
+  CNT_EDGES = 6,      // trajectory-graph edges emitted by K1 (one per cell holding two punctured faces)
   CNT_N = 8
 };
 

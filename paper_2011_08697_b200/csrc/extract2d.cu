@@ -255,6 +255,26 @@ __device__ __forceinline__ void masks_of(int ty, int& m1, int& m2, std::integer_
   ((ty == K ? (m1 = Face3<K>::m1, m2 = Face3<K>::m2, 0) : 0), ...);
 }
 
+// The 6 cells (3-simplices) anchored at a cube: axis permutations (p1, p2, p3) of {x=1, y=2, t=4},
+// chain w0 = 0, w1 = p1, w2 = p1|p2, w3 = 7.  Dropping w3, w2, w1 leaves the cube's own faces
+// ta = (w1, w2), tb = (w1, 7), tc = (w2, 7); dropping w0 leaves the "upper" face (w1, w2, 7), which
+// is owned by the neighbour cube anchored at v + p1 with type tf = (p2, p2|p3) (side_of in closed
+// form).  Its three 2x2 determinants are the pair determinants of ta, tb and tc.
+struct CellDef {
+  int ta, tb, tc, axis, tf, w1, w2;
+};
+constexpr int type3(int m1, int m2) { return kKuhn3.type_of[m1 | m2 << 4]; }
+constexpr CellDef make_cell(int p1, int p2, int p3) {
+  return CellDef{type3(p1, p1 | p2), type3(p1, 7), type3(p1 | p2, 7), p1, type3(p2, p2 | p3), p1, p1 | p2};
+}
+template <int C>
+struct Cell3 {
+  static constexpr int P1[6] = {1, 1, 2, 2, 4, 4};
+  static constexpr int P2[6] = {2, 4, 1, 4, 1, 2};
+  static constexpr int P3[6] = {4, 2, 4, 1, 2, 1};
+  static constexpr CellDef d = make_cell(P1[C], P2[C], P3[C]);
+};
+
 // generic face test from the exact determinant signs: point-in-simplex for the
 // face (0, m1, m2): s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
 template <int K>
@@ -312,7 +332,19 @@ __device__ __noinline__ uint32_t cube_faces_general(const Win<T>& w, const Geo& 
     pair_signs<true>(g, sp, std::make_integer_sequence<int, 12>{});
   }
   all_faces(g, s0k, sp, exists, pmask, std::make_integer_sequence<int, 12>{});
-  return pmask;
+  // upper faces of the 6 cells (meaningful for full cubes only)
+  uint32_t umask = 0;
+#define FTK_UP(C)                                                                                           \
+  {                                                                                                         \
+    constexpr CellDef d = Cell3<C>::d;                                                                      \
+    const int s0 = sos_sign(sp[d.tc], g[d.w2][0], g[d.w2][1], g[7][0], g[7][1]);                            \
+    const int s1 = -sos_sign(sp[d.tb], g[d.w1][0], g[d.w1][1], g[7][0], g[7][1]);                           \
+    const int s2 = sos_sign(sp[d.ta], g[d.w1][0], g[d.w1][1], g[d.w2][0], g[d.w2][1]);                      \
+    umask |= (uint32_t)(s0 == s1 && s1 == s2) << C;                                                         \
+  }
+  FTK_UP(0) FTK_UP(1) FTK_UP(2) FTK_UP(3) FTK_UP(4) FTK_UP(5)
+#undef FTK_UP
+  return pmask | umask << 16;
 }
 
 // int32 fast path: interior cube with both planes, |q| < 2^29 on the window, no zero determinant.
@@ -365,6 +397,15 @@ __device__ __forceinline__ bool cube_faces_fast(const T* W, const Geo& G, uint32
   FTK_FACE(0) FTK_FACE(1) FTK_FACE(2) FTK_FACE(3) FTK_FACE(4) FTK_FACE(5)
   FTK_FACE(6) FTK_FACE(7) FTK_FACE(8) FTK_FACE(9) FTK_FACE(10) FTK_FACE(11)
 #undef FTK_FACE
+  // upper faces (w1, w2, 7) of the 6 cells: s0 = sgn D(w2,7), s1 = -sgn D(w1,7), s2 = sgn D(w1,w2)
+#define FTK_UP(C)                                                                            \
+  {                                                                                          \
+    constexpr CellDef d = Cell3<C>::d;                                                       \
+    const bool a = dp[d.tc] < 0, b = dp[d.tb] > 0, c = dp[d.ta] < 0;                         \
+    m |= (uint32_t)(a == b && b == c) << (16 + C);                                           \
+  }
+  FTK_UP(0) FTK_UP(1) FTK_UP(2) FTK_UP(3) FTK_UP(4) FTK_UP(5)
+#undef FTK_UP
   pmask = m;
   return true;
 }
@@ -486,22 +527,49 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   const i64 x = sm.qx[e], y = sm.qy[e], t = qtv & 0x7fffffff;
   const bool hasB = (qtv >> 31) & 1;
   const T* W = sm.win + e * WSTRIDE;
-  uint32_t pmask = 0;
+  uint32_t m = 0;
   if (valid) {
     const bool interior = x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny && hasB;
-    if (!(interior && cube_faces_fast<T>(W, G, pmask)))
-      pmask = cube_faces_general<T>(Win<T>{W, G.scale_f, G.scale}, G, x, y, hasB);
+    if (!(interior && cube_faces_fast<T>(W, G, m))) m = cube_faces_general<T>(Win<T>{W, G.scale_f, G.scale}, G, x, y, hasB);
   }
-  // spread the punctured faces over the lanes
+  const uint32_t pmask = m & 0xFFFu, umask = m >> 16;
+  // pass 2 for the 6 cells anchored at this cube: every cell lies inside one
+  // cube, so its 4 faces are tested right here; a cell holds 0 or 2 punctured faces under SoS
+  // (PAPER.md:437, 467).  A pair becomes an edge of the trajectory graph: (own record, own record)
+  // or (own record, -1 - face id of the upper face owned by the neighbour cube).
+  const bool full = valid && x + 1 < G.nx && y + 1 < G.ny && hasB;
+  uint32_t epair[6];  // per cell: 4-bit set of punctured faces (bit 0..2 own ta, tb, tc; bit 3 upper)
+  int ecnt = 0, bad = 0;
+#define FTK_CELLCNT(C)                                                                                   \
+  {                                                                                                      \
+    constexpr CellDef d = Cell3<C>::d;                                                                   \
+    const uint32_t bits = ((pmask >> d.ta) & 1u) | (((pmask >> d.tb) & 1u) << 1) |                        \
+                          (((pmask >> d.tc) & 1u) << 2) | (((umask >> C) & 1u) << 3);                     \
+    const int k = __popc(bits);                                                                          \
+    epair[C] = (full && k == 2) ? bits : 0u;                                                             \
+    ecnt += (full && k == 2) ? 1 : 0;                                                                    \
+    bad += (full && k != 0 && k != 2) ? 1 : 0;                                                           \
+  }
+  FTK_CELLCNT(0) FTK_CELLCNT(1) FTK_CELLCNT(2) FTK_CELLCNT(3) FTK_CELLCNT(4) FTK_CELLCNT(5)
+#undef FTK_CELLCNT
+  if (bad) atomicAdd(&P.counters[CNT_INVARIANT], (unsigned long long)bad);
+  // spread the punctured faces over the lanes; reserve record and edge slots
   const int cnt = __popc(pmask);
-  int incl = cnt;
+  int incl = cnt, eincl = ecnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+    const int ve = __shfl_up_sync(0xffffffffu, eincl, o);
+    if (lane >= o) {
+      incl += v;
+      eincl += ve;
+    }
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int etotal = __shfl_sync(0xffffffffu, eincl, 31);
   if (total == 0) return;
+  unsigned long long ebase = 0;
+  if (lane == 0 && etotal) ebase = atomicAdd(&P.counters[CNT_EDGES], (unsigned long long)etotal);
   uint16_t* items = sm.items[ew];
   {
     int pos = incl - cnt;
@@ -515,6 +583,34 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   unsigned long long obase = 0;
   if (lane == 0) obase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
   obase = __shfl_sync(0xffffffffu, obase, 0);
+  ebase = __shfl_sync(0xffffffffu, ebase, 0);
+  if (ecnt) {
+    // record index of own face type ty = obase + (first slot of this lane) + rank of ty in pmask
+    const long long rbase = (long long)obase + (incl - cnt);
+    auto rec_of = [&](int ty) { return rbase + __popc(pmask & ((1u << ty) - 1u)); };
+    unsigned long long eslot = ebase + (unsigned long long)(eincl - ecnt);
+#define FTK_EDGE(C)                                                                                        \
+  if (epair[C]) {                                                                                          \
+    constexpr CellDef d = Cell3<C>::d;                                                                     \
+    const uint32_t bits = epair[C];                                                                        \
+    const int tys[3] = {d.ta, d.tb, d.tc};                                                                 \
+    long long a = -1, b = -1;                                                                              \
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) if ((bits >> q) & 1u) {                                  \
+      if (a < 0) a = rec_of(tys[q]); else b = rec_of(tys[q]);                                              \
+    }                                                                                                      \
+    if (bits & 8u) {                                                                                       \
+      const i64 fx = x + (d.axis & 1), fy = y + ((d.axis >> 1) & 1), ft = t + ((d.axis >> 2) & 1);         \
+      b = -1 - (((ft * G.ny + fy) * G.nx + fx) * 12 + d.tf);                                               \
+    }                                                                                                      \
+    if (eslot < (unsigned long long)P.capacity) {                                                          \
+      P.edges[2 * eslot] = a;                                                                              \
+      P.edges[2 * eslot + 1] = b;                                                                          \
+    }                                                                                                      \
+    ++eslot;                                                                                               \
+  }
+    FTK_EDGE(0) FTK_EDGE(1) FTK_EDGE(2) FTK_EDGE(3) FTK_EDGE(4) FTK_EDGE(5)
+#undef FTK_EDGE
+  }
   __syncwarp();
   for (int i = lane; i < total; i += 32) {
     const int it = items[i];

@@ -19,6 +19,7 @@ struct ExtractParams {
   ftk_cp* out;
   i64 capacity;
   unsigned long long* counters;  // Counter enum
+  long long* edges;    // [capacity][2] trajectory-graph edges: (record, record or -1 - face_id)
   bool force_generic;  // testing: disable TMA
 };
 

@@ -26,22 +26,22 @@ int set_cuda_error(cudaError_t e, const char* what) {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t counters, keys, vals, fid, parent, total;
+  size_t counters, table, edges, fid, parent, total;
   u64 hcap;
 };
 
 static Layout layout(i64 capacity) {
   Layout L;
   u64 h = 1024;
-  while (h < (u64)(2 * (capacity > 0 ? capacity : 1))) h <<= 1;
+  while (h < (u64)(capacity + capacity / 2)) h <<= 1;
   L.hcap = h;
   size_t off = 0;
   L.counters = off;
   off = align_up(off + CNT_N * sizeof(u64), 256);
-  L.keys = off;
-  off = align_up(off + h * sizeof(i64), 256);
-  L.vals = off;
-  off = align_up(off + h * sizeof(int), 256);
+  L.table = off;
+  off = align_up(off + h * sizeof(HashSlot), 256);
+  L.edges = off;
+  off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
   L.fid = off;
   off = align_up(off + (size_t)capacity * sizeof(i64), 256);
   L.parent = off;
@@ -138,6 +138,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.out = d_out;
   EP.capacity = capacity;
   EP.counters = counters;
+  EP.edges = reinterpret_cast<long long*>(ws + L.edges);
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
   ev.rec(1, stream);
   st = desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream);
@@ -148,9 +149,10 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     TP.rec = d_out;
     TP.capacity = capacity;
     TP.counters = counters;
-    TP.keys = reinterpret_cast<i64*>(ws + L.keys);
-    TP.vals = reinterpret_cast<int*>(ws + L.vals);
-    TP.hmask = L.hcap - 1;
+    TP.table = reinterpret_cast<HashSlot*>(ws + L.table);
+    TP.table_cap = L.hcap;
+    TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
+    TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
     TP.fid = reinterpret_cast<i64*>(ws + L.fid);
     TP.parent = reinterpret_cast<int*>(ws + L.parent);
     const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
@@ -174,7 +176,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
   if ((i64)host_cnt[CNT_NOUT] > capacity) return FTK_ERR_CAPACITY;
-  if (track && host_cnt[CNT_INVARIANT]) {
+  if (host_cnt[CNT_INVARIANT]) {
     g_last_error = "cells with a punctured-face count not in {0, 2}: " + std::to_string(host_cnt[CNT_INVARIANT]);
     return FTK_ERR_INVARIANT;
   }

@@ -1,14 +1,18 @@
 // track.cu -- pass 2 of Alg. 1: join the punctured faces of every cell.
 //
-// Instead of visiting all cells, every punctured face visits its (at most two) parent cells in
-// closed form (side_of) and looks up the cell's other d faces in a
-// GPU hash table of punctured face ids.  Under SoS each cell holds 0 or 2 punctured faces
-// (PAPER.md:437, 467), so a face finds exactly one partner per existing parent cell; anything
-// else is counted as an invariant violation.
+// K1 already evaluated every cell (each cell lies inside one cube) and emitted the trajectory-graph
+// edges (record i, record j) or (record i, -1 - face id of a face owned by a neighbour cube).  Here:
 //
-// Union-find (K5/K6, north_star (4)): lock-free hooking with atomicCAS, the root with the larger
-// face_id is hooked under the smaller one, then path compression; every component's final root
-// is its minimum face_id, which becomes the trajectory label -- independent of scheduling.
+//   K3  a GPU hash table face id -> record index, sized from the device-side record count
+//       (nextpow2(1.5 n) 16-byte slots, linear probing),
+//   K4  edge resolution + lock-free union-find (north_star (4)): the root with the larger face id is
+//       hooked under the smaller one with atomicCAS, path halving on finds,
+//   K6  labels: every record gets the face id of its root = the minimum face id of its trajectory,
+//       independent of scheduling.
+//
+// Optional verification (FTK_VERIFY_LINK): every punctured face re-derives its (at most two) parent
+// cells in closed form (side_of) and checks that each holds exactly one
+// other punctured face -- an independent check of K1's cell evaluation.
 #include <utility>
 
 #include "common.cuh"
@@ -18,7 +22,7 @@
 namespace ftk {
 namespace trk {
 
-constexpr i64 EMPTY = -1;
+constexpr long long EMPTY = -1;
 
 __constant__ KuhnTables<3> cK3 = kKuhn3;
 __constant__ KuhnTables<4> cK4 = kKuhn4;
@@ -37,31 +41,47 @@ __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   return n < P.capacity ? n : P.capacity;
 }
 
+// slots used for n records: nextpow2(1.5 n), at least 1024, at most table_cap
+__device__ __forceinline__ u64 table_mask(const TrackParams& P) {
+  const i64 n = n_records(P);
+  u64 h = 1024;
+  while (h < (u64)(n + n / 2) && h < P.table_cap) h <<= 1;
+  return h - 1;
+}
+
+__global__ void k_clear(const __grid_constant__ TrackParams P) {
+  const u64 hm = table_mask(P);
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
+    P.table[i].key = EMPTY;
+}
+
 __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
   const i64 n = n_records(P);
+  const u64 hm = table_mask(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const i64 key = P.rec[i].face_id;
+    const long long key = P.rec[i].face_id;
     P.fid[i] = key;
     P.parent[i] = (int)i;
-    u64 h = mix((u64)key) & P.hmask;
+    u64 h = mix((u64)key) & hm;
     while (true) {
-      const i64 prev = (i64)atomicCAS(reinterpret_cast<u64*>(&P.keys[h]), (u64)EMPTY, (u64)key);
+      const long long prev =
+          (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&P.table[h].key), (u64)EMPTY, (u64)key);
       if (prev == EMPTY || prev == key) {
-        P.vals[h] = (int)i;
+        P.table[h].val = i;
         break;
       }
-      h = (h + 1) & P.hmask;
+      h = (h + 1) & hm;
     }
   }
 }
 
-__device__ __forceinline__ int lookup(const TrackParams& P, i64 key) {
-  u64 h = mix((u64)key) & P.hmask;
+__device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long long key) {
+  u64 h = mix((u64)key) & hm;
   while (true) {
-    const i64 k = P.keys[h];
-    if (k == key) return P.vals[h];
-    if (k == EMPTY) return -1;
-    h = (h + 1) & P.hmask;
+    const HashSlot s = P.table[h];
+    if (s.key == key) return s.val;
+    if (s.key == EMPTY) return -1;
+    h = (h + 1) & hm;
   }
 }
 
@@ -91,6 +111,32 @@ __device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int
   }
 }
 
+__global__ void k_edges(const __grid_constant__ TrackParams P) {
+  const i64 nrec = n_records(P);
+  const i64 ne0 = (i64)P.counters[CNT_EDGES];
+  const i64 ne = ne0 < P.capacity ? ne0 : P.capacity;
+  const u64 hm = table_mask(P);
+  for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (i64)gridDim.x * blockDim.x) {
+    const long long a = P.edges[2 * e];
+    long long b = P.edges[2 * e + 1];
+    if (b < 0) b = lookup(P, hm, -1 - b);  // face owned by the neighbour cube
+    if (a < 0 || b < 0 || a >= nrec || b >= nrec) {
+      atomicAdd(&P.counters[CNT_INVARIANT], 1ull);  // a cell's partner face was never emitted
+      continue;
+    }
+    uf_unite(P.parent, P.fid, (int)a, (int)b);
+  }
+}
+
+__global__ void k_label(const __grid_constant__ TrackParams P) {
+  const i64 n = n_records(P);
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const int r = uf_find(P.parent, (int)i);
+    P.rec[i].label = P.fid[r];
+  }
+}
+
+// ------------------------------------------------------------------------- closed-form verifier
 template <int D>
 struct Geo {
   i64 ext[4];   // extents in axis order x, y, [z,] t (t global)
@@ -123,11 +169,10 @@ __device__ __forceinline__ i64 encode(const Geo<D>& G, const i64* v, int m_idx) 
   return I * T + ty;
 }
 
-// Visit one parent cell given as a chain of D+1 cumulative masks w[0..D] relative to anchor A;
-// return the number of OTHER punctured faces found and the last one's index.
+// number of OTHER punctured faces of the cell given as a chain of D+1 cumulative masks w[0..D]
 template <int D>
-__device__ __forceinline__ int visit_cell(const TrackParams& P, const Geo<D>& G, const i64* A, const int* w,
-                                          i64 self, int& partner) {
+__device__ __forceinline__ int visit_cell(const TrackParams& P, u64 hm, const Geo<D>& G, const i64* A, const int* w,
+                                          i64 self) {
   int hits = 0;
 #pragma unroll
   for (int j = 0; j <= D; ++j) {
@@ -153,25 +198,22 @@ __device__ __forceinline__ int visit_cell(const TrackParams& P, const Geo<D>& G,
     }
     const i64 f = encode<D>(G, anc, idx);
     if (f == self) continue;
-    const int r = lookup(P, f);
-    if (r >= 0) {
-      ++hits;
-      partner = r;
-    }
+    hits += lookup(P, hm, f) >= 0;
   }
   return hits;
 }
 
 template <int D>
-__global__ void k_link(const __grid_constant__ TrackParams P, const Geo<D> G) {
+__global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) {
   const i64 n = n_records(P);
+  const u64 hm = table_mask(P);
   constexpr int FULL = (1 << D) - 1;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i64 self = P.fid[i];
     i64 v[4];
     int type;
     decode<D>(G, self, v, type);
-    int m[4] = {0, 0, 0, 0};  // m[1..D-1]
+    int m[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int k = 1; k < D; ++k) m[k] = D == 3 ? cK3.masks[type][k - 1] : cK4.masks[type][k - 1];
     const int U = m[D - 1];
@@ -179,20 +221,15 @@ __global__ void k_link(const __grid_constant__ TrackParams P, const Geo<D> G) {
     if (U != FULL) {
       const int cbit = FULL & ~U;
       const int c = __ffs(cbit) - 1;
-      // parent 1: append v_last + e_c (same anchor), exists iff v0[c] <= N_c - 2
-      if (v[c] + 1 <= G.ext[c] - 1) {
+      if (v[c] + 1 <= G.ext[c] - 1) {  // parent 1: append v_last + e_c (same anchor)
         int w[5];
         w[0] = 0;
 #pragma unroll
         for (int k = 1; k < D; ++k) w[k] = m[k];
         w[D] = FULL;
-        int partner = -1;
-        const int h = visit_cell<D>(P, G, v, w, self, partner);
-        if (h != 1) bad = 1;
-        else if (P.fid[partner] > self) uf_unite(P.parent, P.fid, (int)i, partner);
+        bad |= visit_cell<D>(P, hm, G, v, w, self) != 1;
       }
-      // parent 2: prepend v0 - e_c (anchor moves down), exists iff v0[c] >= 1
-      if (v[c] >= 1) {
+      if (v[c] >= 1) {  // parent 2: prepend v0 - e_c (anchor moves down)
         i64 A[4];
 #pragma unroll
         for (int a = 0; a < D; ++a) A[a] = v[a] - (a == c ? 1 : 0);
@@ -200,14 +237,10 @@ __global__ void k_link(const __grid_constant__ TrackParams P, const Geo<D> G) {
         w[0] = 0;
 #pragma unroll
         for (int k = 1; k <= D; ++k) w[k] = cbit | m[k - 1];
-        int partner = -1;
-        const int h = visit_cell<D>(P, G, A, w, self, partner);
-        if (h != 1) bad = 1;
-        else if (P.fid[partner] > self) uf_unite(P.parent, P.fid, (int)i, partner);
+        bad |= visit_cell<D>(P, hm, G, A, w, self) != 1;
       }
     } else {
-      // the face spans all axes: exactly one step has two axes {a, b}; the two parent cells
-      // split it as a-then-b and b-then-a, same anchor, both always exist
+      // the face spans all axes: one step has two axes {a, b}; the parents split it both ways
       int step = 0, pair = 0;
 #pragma unroll
       for (int k = 1; k < D; ++k) {
@@ -226,23 +259,10 @@ __global__ void k_link(const __grid_constant__ TrackParams P, const Geo<D> G) {
           if (k == step) w[o++] = m[k - 1] | (which ? b : a);
           w[o++] = m[k];
         }
-        w[D] = m[D - 1];
-        // rebuild: chain = m0, ..., m_{step-1}, m_{step-1}|x, m_step, ..., m_{D-1}
-        int partner = -1;
-        const int h = visit_cell<D>(P, G, v, w, self, partner);
-        if (h != 1) bad = 1;
-        else if (P.fid[partner] > self) uf_unite(P.parent, P.fid, (int)i, partner);
+        bad |= visit_cell<D>(P, hm, G, v, w, self) != 1;
       }
     }
     if (bad) atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
-  }
-}
-
-__global__ void k_label(const __grid_constant__ TrackParams P) {
-  const i64 n = n_records(P);
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const int r = uf_find(P.parent, (int)i);
-    P.rec[i].label = P.fid[r];
   }
 }
 
@@ -254,23 +274,28 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int threads = 256, blocks = sms * 8;
-  FTK_CUDA_TRY(cudaMemsetAsync(P.keys, 0xff, (size_t)(P.hmask + 1) * sizeof(i64), stream));
+  k_clear<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
   k_hash_insert<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
-  if (ndim == 2) {
-    Geo<3> G;
-    G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[3];
-    G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1];
-    k_link<3><<<blocks, threads, 0, stream>>>(P, G);
-  } else {
-    Geo<4> G;
-    G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[2]; G.ext[3] = ext[3];
-    G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1]; G.stride[3] = ext[0] * ext[1] * ext[2];
-    k_link<4><<<blocks, threads, 0, stream>>>(P, G);
-  }
+  k_edges<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   k_label<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
+  if (P.verify) {
+    if (ndim == 2) {
+      Geo<3> G;
+      G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[3];
+      G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1];
+      k_verify<3><<<blocks, threads, 0, stream>>>(P, G);
+    } else {
+      Geo<4> G;
+      G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[2]; G.ext[3] = ext[3];
+      G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1]; G.stride[3] = ext[0] * ext[1] * ext[2];
+      k_verify<4><<<blocks, threads, 0, stream>>>(P, G);
+    }
+    FTK_CUDA_TRY(cudaGetLastError());
+  }
   return FTK_OK;
 }
 

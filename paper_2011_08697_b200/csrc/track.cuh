@@ -5,15 +5,22 @@
 
 namespace ftk {
 
+struct HashSlot {
+  long long key;  // face id, -1 = empty
+  long long val;  // record index
+};
+
 struct TrackParams {
   ftk_cp* rec;                   // records from pass 1
   i64 capacity;
-  unsigned long long* counters;  // CNT_NOUT holds the record count
-  i64* keys;                     // hash table keys [hmask + 1] (face ids, -1 = empty)
-  int* vals;                     // hash table values (record index)
-  u64 hmask;
+  unsigned long long* counters;  // CNT_NOUT holds the record count, CNT_EDGES the edge count
+  HashSlot* table;               // face id -> record index; [table_cap] slots
+  u64 table_cap;                 // power of two >= 1.5 * capacity; the kernels use
+                                 // nextpow2(1.5 * n) <= table_cap slots, n = records found
   i64* fid;                      // [capacity] face ids (compact copy, union-find keys)
   int* parent;                   // [capacity] union-find parents
+  const long long* edges;        // [capacity][2] edges from K1
+  bool verify;                   // also re-derive every face's parent cells in closed form
 };
 
 // ext = {nx, ny, nz, nt_global}

@@ -112,6 +112,18 @@ def test_generic_loader_matches_tma(ftk, oracle_lib):
     assert _sorted(a).tobytes() == _sorted(b).tobytes()
 
 
+def test_closed_form_link_verification(ftk, oracle_lib):
+    """K1 pairs faces per cell; the independent closed-form side_of verifier (FTK_VERIFY_LINK)
+    re-derives every punctured face's parent cells and finds exactly one partner in each."""
+    os.environ["FTK_VERIFY_LINK"] = "1"
+    try:
+        for f in (fi.Woven(150, 140, 40, sigma=0.08).generate(), fi.random_degenerate((6, 37, 150), seed=4)):
+            s = 26 if f.abs().max() < 2 and f.dtype == torch.float32 and (f != f.round()).any() else 0
+            run_pair(ftk, oracle_lib, f, s)
+    finally:
+        del os.environ["FTK_VERIFY_LINK"]
+
+
 def test_extract_window_with_ghost(ftk, oracle_lib):
     w = fi.Woven(96, 80, 30, sigma=0.02)
     f = w.generate()
