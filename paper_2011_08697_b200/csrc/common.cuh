@@ -24,7 +24,8 @@ enum Counter : int {
   CNT_EXPORT = 4,     // slab stitch: exported boundary faces
   CNT_WORK = 5,       // K1 persistent scheduler: next work item
   CNT_EDGES = 6,      // trajectory-graph edges emitted by K1 (one per cell holding two punctured faces)
-  CNT_N = 8
+  CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
+  CNT_N = 32
 };
 
 // Correctly rounded (round-half-even) int128 -> double; the oracle's reading of step 5

@@ -94,6 +94,26 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// optional cycle accounting (build with -DFTK_K1_PROF=1): per role, cycles spent per activity
+#ifndef FTK_K1_PROF
+#define FTK_K1_PROF 0
+#endif
+enum ProfSlot { PF_SCAN = 0, PF_WFULL, PF_ENQ, PF_WRING, PF_EXWAIT, PF_EXFACE, PF_EXREC, PF_PRODWAIT, PF_OTHER, PF_N };
+struct Prof {
+  unsigned long long acc[PF_N];
+  unsigned long long t;
+  __device__ void start() {
+    if (FTK_K1_PROF) t = clock64();
+  }
+  __device__ void lap(int slot) {
+    if (FTK_K1_PROF) {
+      const unsigned long long n = clock64();
+      acc[slot] += n - t;
+      t = n;
+    }
+  }
+};
+
 struct f2 {
   unsigned long long v;
 };
@@ -125,7 +145,13 @@ constexpr int TX = 124;             // anchors owned per tile in x: lane 31 is a
                                     // only complete lane 30's cubes (a cube needs its x+1 corners)
 constexpr int RW = 4;               // anchor rows per scan warp
 constexpr int NSW = 8;              // scan warps
-constexpr int NEW = 3;              // exact warps
+#ifndef FTK_K1_NEW
+#define FTK_K1_NEW 3
+#endif
+#ifndef FTK_K1_DYN
+#define FTK_K1_DYN 1
+#endif
+constexpr int NEW = FTK_K1_NEW;     // exact warps
 constexpr int NWARPS = NSW + 1 + NEW;
 // Roles by warp id.  A warp runs on SMSP (id % 4): the exact warps get SMSP 3 to themselves (ids
 // 3, 7, 11) so their large code does not evict the scan loop from the per-SMSP instruction cache;
@@ -159,9 +185,14 @@ constexpr int ROWS = TY + 3;        // y0-1 .. y0+33
 constexpr int NSTAGE = FTK_K1_NSTAGE;
 constexpr int NB = FTK_K1_NB;       // window-ring batch slots (32 cubes each)
 constexpr int RING = NB * 32;
-constexpr int WSTRIDE = 33;         // values per queued window (4x4x2 = 32, odd stride: no bank conflicts)
+// Ring entry (32-bit words): [0, 32) the cube's 4x4x2 window W[pl*16 + r*4 + c] at
+// (x - 1 + c, y - 1 + r, t + pl) -- as exact int32 q values for fast entries (fp32 input, interior
+// cube, |q| < 2^29), else as raw values; [32, 48) the 8 corner gradients (fast entries).
+template <typename T>
+constexpr int ws_words() { return sizeof(T) == 4 ? 49 : 66; }  // odd stride for fp32: no bank conflicts
 constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
 constexpr int TCHUNK = 32;          // anchor timesteps per work item
+constexpr int SLIST = 32;           // survivors enqueued per pass (one per lane)
 
 template <typename T>
 constexpr int stage_elems() {       // plane tile padded to a multiple of 128 bytes (TMA alignment)
@@ -180,15 +211,18 @@ struct StageMeta {                  // written by the producer before the plane 
 template <typename T>
 struct alignas(128) Smem {
   T plane[NSTAGE][stage_elems<T>()];
-  T win[RING * WSTRIDE];           // queued survivor windows: W[pl*16 + r*4 + c] = f(x-1+c, y-1+r, t+pl)
-  int qx[RING], qy[RING], qt[RING];  // cube anchor; qt bit 31: the t+1 plane exists
+  uint32_t ring[RING * ws_words<T>()];  // queued survivor cubes (see ws_words)
+  int qx[RING], qy[RING], qt[RING];  // cube anchor; qt bit 31: the t+1 plane exists, bit 30: fast entry
   uint16_t items[NEW][MAXITEMS];   // punctured faces of a batch: entry | type << 5
+  uint16_t slist[NSW][SLIST];      // per scan warp: survivors being enqueued (xl | yl << 8)
+  int scount[NSW];
   StageMeta meta[NSTAGE];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
   int wfill[NB];                   // entries ever written into each batch slot (monotone)
   volatile int wcons[NB];          // generations of each batch slot consumed by the exact warps
   int tail;                        // window-ring entries reserved so far
+  int next_batch;                  // dynamic batch assignment to the exact warps
   int scan_done;
   volatile int nbatch;             // batches in total, -1 until the scan warps are done
   unsigned long long surv;
@@ -213,17 +247,27 @@ struct Geo {
 };
 
 template <typename T>
-struct Win {  // W[pl*16 + r*4 + c] = f(x - 1 + c, y - 1 + r, t + pl)
-  const T* W;
+struct Win {  // window value (pl, c, r) = q at (x - 1 + c, y - 1 + r, t + pl)
+  const uint32_t* W;
+  bool isq;   // fast entry: exact int32 q values and precomputed gradients
   float sf;
   double sd;
-  __device__ __forceinline__ i64 q(int pl, int c, int r) const { return quant(W[pl * 16 + r * 4 + c], sf, sd); }
+  __device__ __forceinline__ i64 q(int pl, int c, int r) const {
+    const int k = pl * 16 + r * 4 + c;
+    if (isq) return (i64)(int)W[k];
+    return quant(reinterpret_cast<const T*>(W)[k], sf, sd);
+  }
 };
 
 // exact gradient (2x the derivative, one-sided doubled at the spatial boundary; R7) at
 // cube corner c (bit0 x, bit1 y, bit2 t)
 template <typename T>
 __device__ __forceinline__ void corner_grad(const Win<T>& w, const Geo& G, i64 x, i64 y, int c, i64& gx, i64& gy) {
+  if (w.isq) {  // fast entries are interior cubes: central differences precomputed by the scan warp
+    gx = (int)w.W[32 + 2 * c];
+    gy = (int)w.W[33 + 2 * c];
+    return;
+  }
   const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
   const i64 xc = x + cx, yc = y + cy;
   if (xc == 0) gx = 2 * (w.q(pl, cx + 2, cy + 1) - w.q(pl, cx + 1, cy + 1));
@@ -274,6 +318,20 @@ struct Cell3 {
   static constexpr int P3[6] = {4, 2, 4, 1, 2, 1};
   static constexpr CellDef d = make_cell(P1[C], P2[C], P3[C]);
 };
+
+template <int... C>
+constexpr int cell_code(int c, std::integer_sequence<int, C...>) {
+  int r = 0;
+  ((c == C ? (r = Cell3<C>::d.ta | Cell3<C>::d.tb << 4 | Cell3<C>::d.tc << 8 | Cell3<C>::d.axis << 12 |
+                  Cell3<C>::d.tf << 16, 0) : 0), ...);
+  return r;
+}
+__constant__ int cCell[6] = {cell_code(0, std::make_integer_sequence<int, 6>{}),
+                             cell_code(1, std::make_integer_sequence<int, 6>{}),
+                             cell_code(2, std::make_integer_sequence<int, 6>{}),
+                             cell_code(3, std::make_integer_sequence<int, 6>{}),
+                             cell_code(4, std::make_integer_sequence<int, 6>{}),
+                             cell_code(5, std::make_integer_sequence<int, 6>{})};
 
 // generic face test from the exact determinant signs: point-in-simplex for the
 // face (0, m1, m2): s_k = (-1)^(k+2) sos(rows != k); punctured iff s_0 = s_1 = s_2.
@@ -347,31 +405,14 @@ __device__ __noinline__ uint32_t cube_faces_general(const Win<T>& w, const Geo& 
   return pmask | umask << 16;
 }
 
-// int32 fast path: interior cube with both planes, |q| < 2^29 on the window, no zero determinant.
-// Returns false when the general path is needed.
-template <typename T>
-__device__ __forceinline__ bool cube_faces_fast(const T* W, const Geo& G, uint32_t& pmask) {
-  // the 24 window values the 8 corner gradients use (the 4 window corners per plane are not needed)
-  float mx = 0.f;
-  int q[2][4][4];
-#pragma unroll
-  for (int pl = 0; pl < 2; ++pl)
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if ((r == 0 || r == 3) && (c == 0 || c == 3)) continue;
-        const T f = W[pl * 16 + r * 4 + c];
-        mx = fmaxf(mx, fabsf((float)f));
-        q[pl][r][c] = (int)quant(f, G.scale_f, G.scale);
-      }
-  if (!(mx < (float)G.qmax)) return false;  // also catches NaN
+// int32 fast path: fast entry (interior cube with both planes, |q| < 2^29), gradients precomputed
+// by the scan warp.  Returns false on a zero determinant (the SoS chains are in the general path).
+__device__ __forceinline__ bool cube_faces_fast(const uint32_t* E, uint32_t& pmask) {
   int g[8][2];
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
-    g[c][0] = q[pl][cy + 1][cx + 2] - q[pl][cy + 1][cx];
-    g[c][1] = q[pl][cy + 2][cx + 1] - q[pl][cy][cx + 1];
+    g[c][0] = (int)E[32 + 2 * c];
+    g[c][1] = (int)E[33 + 2 * c];
   }
   // determinants (0, k) and (m1, m2): |g| < 2^30 so |det| < 2^61
   i64 d0[8], dp[12];
@@ -437,8 +478,8 @@ __device__ __noinline__ void hessian_global(const ExtractParams& P, const Geo& G
 #define FTK_REC_INL __forceinline__
 #endif
 template <typename T>
-__device__ FTK_REC_INL void emit_record(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y, i64 t, int ty,
-                            unsigned long long slot) {
+__device__ __noinline__ void emit_record_general(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y,
+                                                 i64 t, int ty, unsigned long long slot) {
   int m[3] = {0, 0, 0};
   masks_of(ty, m[1], m[2], std::make_integer_sequence<int, 12>{});
   i64 gv[3][2];
@@ -516,23 +557,103 @@ __device__ FTK_REC_INL void emit_record(const Win<T>& w, const Geo& G, const Ext
   }
 }
 
+__device__ __forceinline__ void store_record(const ExtractParams& P, unsigned long long slot, long long fid, double lx,
+                                             double ly, double lt, int type, uint32_t flags) {
+  if (slot < (unsigned long long)P.capacity) {
+    ftk_cp* r = P.out + slot;
+    r->face_id = fid;
+    r->label = -1;
+    r->x = lx;
+    r->y = ly;
+    r->z = 0.0;
+    r->t = lt;
+    r->type = type;
+    r->flags = flags;
+  }
+}
+
+// Record of a punctured face: fast entries (interior cube, |g| < 2^30) in int64 -- |D_k| < 2^61 and
+// |sum D| < 2^63, converted exactly as the int128 path would -- else the general int128 path.
+template <typename T>
+__device__ __forceinline__ void emit_record(const Win<T>& w, const Geo& G, const ExtractParams& P, i64 x, i64 y, i64 t,
+                                            int ty, unsigned long long slot) {
+  if (!w.isq) {
+    emit_record_general<T>(w, G, P, x, y, t, ty, slot);
+    return;
+  }
+  int m[3] = {0, 0, 0};
+  masks_of(ty, m[1], m[2], std::make_integer_sequence<int, 12>{});
+  int g[3][2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g[k][0] = (int)w.W[32 + 2 * m[k]];
+    g[k][1] = (int)w.W[33 + 2 * m[k]];
+  }
+  // mu_k = D_k / sum D, D_k = (-1)^(k+2) det(rows != k)
+  const i64 D0 = (i64)g[1][0] * g[2][1] - (i64)g[1][1] * g[2][0];
+  const i64 D1 = (i64)g[0][1] * g[2][0] - (i64)g[0][0] * g[2][1];
+  const i64 D2 = (i64)g[0][0] * g[1][1] - (i64)g[0][1] * g[1][0];
+  const i64 S = D0 + D1 + D2;
+  double mu[3];
+  uint32_t flags = 0;
+  if (S == 0) {
+    mu[0] = mu[1] = mu[2] = 1.0 / 3.0;
+    flags |= FTK_CP_DEGENERATE_LOC;
+  } else {
+    const double sd = __ll2double_rn(S);
+    mu[0] = __ddiv_rn(__ll2double_rn(D0), sd);
+    mu[1] = __ddiv_rn(__ll2double_rn(D1), sd);
+    mu[2] = __ddiv_rn(__ll2double_rn(D2), sd);
+  }
+  double px[3], py[3], pt[3], Hd[3][3];
+  const int* q = reinterpret_cast<const int*>(w.W);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int mx = m[k] & 1, my = (m[k] >> 1) & 1, pl = (m[k] >> 2) & 1;
+    px[k] = (double)(x + mx);
+    py[k] = (double)(y + my);
+    pt[k] = (double)(t + pl);
+    // interior vertex: the Hessian stencil centre is the vertex itself, window (mx+1, my+1)
+    const int* Q = q + pl * 16 + (my + 1) * 4 + (mx + 1);
+    Hd[k][0] = __ll2double_rn(4ll * ((i64)Q[1] - 2ll * Q[0] + Q[-1]));
+    Hd[k][1] = __ll2double_rn((i64)Q[5] - Q[-3] - Q[3] + Q[-5]);
+    Hd[k][2] = __ll2double_rn(4ll * ((i64)Q[4] - 2ll * Q[0] + Q[-4]));
+  }
+  const double lx = dot3_nofma(mu, px[0], px[1], px[2]);
+  const double ly = dot3_nofma(mu, py[0], py[1], py[2]);
+  const double lt = dot3_nofma(mu, pt[0], pt[1], pt[2]);
+  const double a = dot3_nofma(mu, Hd[0][0], Hd[1][0], Hd[2][0]);
+  const double b = dot3_nofma(mu, Hd[0][1], Hd[1][1], Hd[2][1]);
+  const double d = dot3_nofma(mu, Hd[0][2], Hd[1][2], Hd[2][2]);
+  const double det = __dsub_rn(__dmul_rn(a, d), __dmul_rn(b, b));
+  const int type = det < 0 ? FTK_CP_SADDLE : (det > 0 ? (a > 0 ? FTK_CP_MIN : FTK_CP_MAX) : FTK_CP_DEGENERATE);
+  const int span = m[2];
+  if (!(span & 4)) flags |= FTK_CP_ORDINAL;
+  if (span != 7) {  // interior in x and y: only t can be on the boundary
+    const int c = 7 & ~span;
+    if (c == 4 && (t == 0 || t == G.ntg - 1)) flags |= FTK_CP_BOUNDARY;
+  }
+  store_record(P, slot, ((t * G.ny + y) * G.nx + x) * 12 + ty, lx, ly, lt, type, flags);
+}
+
 // One batch of 32 ring entries (one cube per lane): face tests, then the punctured faces spread
 // over the lanes for the record stage.
 template <typename T>
-__device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G, const ExtractParams& P) {
+__device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G, const ExtractParams& P, Prof& pf) {
   const int lane = threadIdx.x & 31;
   const int e = base_entry + lane;
   const int qtv = sm.qt[e];
   const bool valid = qtv != -1;
-  const i64 x = sm.qx[e], y = sm.qy[e], t = qtv & 0x7fffffff;
+  const i64 x = sm.qx[e], y = sm.qy[e], t = qtv & 0x3fffffff;
   const bool hasB = (qtv >> 31) & 1;
-  const T* W = sm.win + e * WSTRIDE;
+  const uint32_t* E = sm.ring + e * ws_words<T>();
+  const bool isq = (qtv >> 30) & 1;
   uint32_t m = 0;
   if (valid) {
-    const bool interior = x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny && hasB;
-    if (!(interior && cube_faces_fast<T>(W, G, m))) m = cube_faces_general<T>(Win<T>{W, G.scale_f, G.scale}, G, x, y, hasB);
+    if (!(isq && cube_faces_fast(E, m))) m = cube_faces_general<T>(Win<T>{E, isq, G.scale_f, G.scale}, G, x, y, hasB);
   }
   const uint32_t pmask = m & 0xFFFu, umask = m >> 16;
+  pf.lap(PF_EXFACE);
   // pass 2 for the 6 cells anchored at this cube: every cell lies inside one
   // cube, so its 4 faces are tested right here; a cell holds 0 or 2 punctured faces under SoS
   // (PAPER.md:437, 467).  A pair becomes an edge of the trajectory graph: (own record, own record)
@@ -587,36 +708,39 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   if (ecnt) {
     // record index of own face type ty = obase + (first slot of this lane) + rank of ty in pmask
     const long long rbase = (long long)obase + (incl - cnt);
-    auto rec_of = [&](int ty) { return rbase + __popc(pmask & ((1u << ty) - 1u)); };
     unsigned long long eslot = ebase + (unsigned long long)(eincl - ecnt);
-#define FTK_EDGE(C)                                                                                        \
-  if (epair[C]) {                                                                                          \
-    constexpr CellDef d = Cell3<C>::d;                                                                     \
-    const uint32_t bits = epair[C];                                                                        \
-    const int tys[3] = {d.ta, d.tb, d.tc};                                                                 \
-    long long a = -1, b = -1;                                                                              \
-    _Pragma("unroll") for (int q = 0; q < 3; ++q) if ((bits >> q) & 1u) {                                  \
-      if (a < 0) a = rec_of(tys[q]); else b = rec_of(tys[q]);                                              \
-    }                                                                                                      \
-    if (bits & 8u) {                                                                                       \
-      const i64 fx = x + (d.axis & 1), fy = y + ((d.axis >> 1) & 1), ft = t + ((d.axis >> 2) & 1);         \
-      b = -1 - (((ft * G.ny + fy) * G.nx + fx) * 12 + d.tf);                                               \
-    }                                                                                                      \
-    if (eslot < (unsigned long long)P.capacity) {                                                          \
-      P.edges[2 * eslot] = a;                                                                              \
-      P.edges[2 * eslot + 1] = b;                                                                          \
-    }                                                                                                      \
-    ++eslot;                                                                                               \
-  }
-    FTK_EDGE(0) FTK_EDGE(1) FTK_EDGE(2) FTK_EDGE(3) FTK_EDGE(4) FTK_EDGE(5)
-#undef FTK_EDGE
+#pragma unroll 1
+    for (int C = 0; C < 6; ++C) {
+      const uint32_t bits = epair[C];
+      if (!bits) continue;
+      const int cd = cCell[C];  // ta | tb << 4 | tc << 8 | axis << 12 | tf << 16
+      long long a = -1, b = -1;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if ((bits >> q) & 1u) {
+          const int ty = (cd >> (4 * q)) & 15;
+          const long long r = rbase + __popc(pmask & ((1u << ty) - 1u));
+          if (a < 0) a = r; else b = r;
+        }
+      if (bits & 8u) {
+        const int axis = (cd >> 12) & 7, tf = (cd >> 16) & 15;
+        const i64 fx = x + (axis & 1), fy = y + ((axis >> 1) & 1), ft = t + ((axis >> 2) & 1);
+        b = -1 - (((ft * G.ny + fy) * G.nx + fx) * 12 + tf);
+      }
+      if (eslot < (unsigned long long)P.capacity) {
+        P.edges[2 * eslot] = a;
+        P.edges[2 * eslot + 1] = b;
+      }
+      ++eslot;
+    }
   }
   __syncwarp();
   for (int i = lane; i < total; i += 32) {
     const int it = items[i];
     const int le = base_entry + (it & 31), ty = it >> 5;
-    const Win<T> w2{sm.win + le * WSTRIDE, G.scale_f, G.scale};
-    emit_record<T>(w2, G, P, sm.qx[le], sm.qy[le], sm.qt[le] & 0x7fffffff, ty, obase + i);
+    const int lqt = sm.qt[le];
+    const Win<T> w2{sm.ring + le * ws_words<T>(), ((lqt >> 30) & 1) != 0, G.scale_f, G.scale};
+    emit_record<T>(w2, G, P, sm.qx[le], sm.qy[le], lqt & 0x3fffffff, ty, obase + i);
   }
   __syncwarp();
 }
@@ -814,6 +938,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     sm.maxbits32 = 0;
     sm.maxbits64 = 0;
     sm.tail = 0;
+    sm.next_batch = 0;
     sm.scan_done = 0;
     sm.nbatch = -1;
     for (int s = 0; s < NSTAGE; ++s) {
@@ -827,13 +952,19 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  Prof pf;
+#pragma unroll
+  for (int i = 0; i < PF_N; ++i) pf.acc[i] = 0;
+  pf.start();
 
   if (warp == PRODUCER) {
     // ------------------------------------------------------------------ producer warp
     const T* field = reinterpret_cast<const T*>(P.field);
     int gk = 0;  // planes issued so far (ring position)
     auto acquire = [&](int s) {
+      pf.lap(PF_OTHER);
       if (gk >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
+      pf.lap(PF_PRODWAIT);
     };
     while (true) {
       long long item = 0;
@@ -889,6 +1020,11 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     // ------------------------------------------------------------------ exact warps
     const int ew = exact_index(warp);
     for (int b = ew;; b += NEW) {
+      if (FTK_K1_DYN) {
+        int nb2 = 0;
+        if (lane == 0) nb2 = atomicAdd(&sm.next_batch, 1);
+        b = __shfl_sync(0xffffffffu, nb2, 0);
+      }
       const int j = b % NB;
       bool go = true;
       const int target = 32 * (b / NB + 1);
@@ -906,8 +1042,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       }
       if (!go) break;
       __threadfence_block();
-      process_batch<T>(sm, ew, j * 32, G, P);
+      pf.lap(PF_EXWAIT);
+#ifndef FTK_K1_DIAG_NOEXACT
+#define FTK_K1_DIAG_NOEXACT 0
+#endif
+      if (!FTK_K1_DIAG_NOEXACT) process_batch<T>(sm, ew, j * 32, G, P, pf);
       __syncwarp();
+      pf.lap(PF_EXREC);
       if (lane == 0) {
         __threadfence_block();  // our reads of the slot happen before it is handed back
         sm.wcons[j] = b / NB + 1;
@@ -922,79 +1063,119 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     double maxd = 0.0;
     unsigned long long mysurv = 0;
     uint32_t prevSq[RW];
-    // window copy: lane k copies element k = (pl, r, c) of the 4x4x2 window
-    const int c_pl = lane >> 4, c_r = (lane >> 2) & 3, c_c = lane & 3;
-    const int c_off = (c_r - 1 + YOFF) * PITCH + (c_c - 1 + XOFF);
+    const float qmaxf = (float)G.qmax;
     const int sw = scan_index(warp);     // scan-warp index: anchor rows sw*RW .. sw*RW + RW - 1
     const int srow0 = YOFF + sw * RW;    // smem row of this warp's first anchor row
 
     // hand the survivors (bit 4r + j <-> row r, position 3 - j) to the exact warps: reserve ring
     // entries, copy each cube's 4x4x2 window (planes A = t, B = t+1), publish per batch slot
+    // hand the survivors (bit 4r + i <-> anchor row r, position i) to the exact warps.  They are
+    // appended to a per-warp list, ring entries are reserved for the whole list, and lane i then
+    // copies survivor i's 4x4x2 window (planes A = t, B = t+1) -- for fast entries as exact int32
+    // q values plus the 8 corner gradients -- so one pass costs the same for 1 or 32 survivors.
+    uint16_t* slist = sm.slist[sw];
     auto enqueue = [&](uint32_t mask, const T* A, const T* B, int t, int x0, int y0) {
-      const int cnt = __popc(mask);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) return;
-      mysurv += total;
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&sm.tail, total);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      const int tflag = (int)((uint32_t)t | (B ? 0x80000000u : 0u));
+      if (!__any_sync(0xffffffffu, mask != 0)) return;
       const T* B2 = B ? B : A;
-      int e = base, pending = 0;
-      // claim the first slot
-      auto claim = [&](int ee) {
-        const int bat = ee >> 5, slot = bat % NB;
-        if (bat >= NB && sm.wcons[slot] < bat / NB) {
-          const unsigned long long t0 = gtimer_ns();
-          while (sm.wcons[slot] < bat / NB) {
-            __nanosleep(32);
-            if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(2, bat, ee);
-          }
-          __threadfence_block();
-        }
-      };
-      auto publish = [&](int ee, int n) {  // n entries ending before ee in one batch slot
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          atomicAdd(&sm.wfill[((ee - 1) >> 5) % NB], n);
-        }
-      };
-      claim(e);
+      const int tflag = (int)((uint32_t)t | (B ? 0x80000000u : 0u));
       while (true) {
-        const uint32_t have = __ballot_sync(0xffffffffu, mask != 0);
-        if (!have) break;
-        const int myb = mask ? __ffs(mask) - 1 : 0;
-        mask &= mask - 1;
-        uint32_t h = have;
-        while (h) {
-          const int L = __ffs(h) - 1;
-          h &= h - 1;
-          const int b = __shfl_sync(0xffffffffu, myb, L);
-          const int xl = 4 * L + (b & 3), yl = sw * RW + (b >> 2);
-          const int pos = e % RING;
-          sm.win[pos * WSTRIDE + lane] = (c_pl ? B2 : A)[yl * PITCH + xl + c_off];
-          if (lane == 0) {
-            sm.qx[pos] = x0 + xl;
-            sm.qy[pos] = y0 + yl;
-            sm.qt[pos] = tflag;
+        // list up to SLIST survivors
+        if (lane == 0) sm.scount[sw] = 0;
+        __syncwarp();
+        const int cnt = min(__popc(mask), 32);
+        int off = 0;
+        if (cnt) off = atomicAdd(&sm.scount[sw], cnt);
+        __syncwarp();
+        const int n0 = *(volatile int*)&sm.scount[sw];
+        const int n = min(n0, SLIST);
+        {
+          int r = off;
+          while (mask && r < SLIST) {
+            const int bb = __ffs(mask) - 1;
+            mask &= mask - 1;
+            slist[r++] = (uint16_t)((4 * lane + (bb & 3)) | ((sw * RW + (bb >> 2)) << 8));
           }
-          ++e;
-          ++pending;
-          if ((e & 31) == 0) {  // batch slot complete for this warp
-            publish(e, pending);
-            pending = 0;
-            if (e < base + total) claim(e);
+          // survivors beyond the list capacity stay in `mask` for the next pass
+        }
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&sm.tail, n);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        mysurv += n;
+        // claim every batch slot the range [base, base + n) touches
+        for (int bat = base >> 5; bat <= (base + n - 1) >> 5; ++bat) {
+          const int slot = bat % NB;
+          if (bat >= NB && sm.wcons[slot] < bat / NB) {
+            pf.lap(PF_ENQ);
+            const unsigned long long t0 = gtimer_ns();
+            while (sm.wcons[slot] < bat / NB) {
+              __nanosleep(32);
+              if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(2, bat, base);
+            }
+            pf.lap(PF_WRING);
           }
         }
+        __threadfence_block();
+        __syncwarp();
+#ifndef FTK_K1_DIAG_NOCOPY
+#define FTK_K1_DIAG_NOCOPY 0
+#endif
+        if (lane < n && !FTK_K1_DIAG_NOCOPY) {
+          const int code = slist[lane];
+          const int xl = code & 255, yl = code >> 8;
+          const int pos = (base + lane) % RING;
+          uint32_t* ent = sm.ring + pos * ws_words<T>();
+          const T* sa = A + (yl - 1 + YOFF) * PITCH + (xl - 1 + XOFF);
+          const T* sb = B2 + (yl - 1 + YOFF) * PITCH + (xl - 1 + XOFF);
+          bool fast = false;
+          if constexpr (sizeof(T) == 4) {
+            float v[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = (k < 16 ? sa : sb)[((k >> 2) & 3) * PITCH + (k & 3)];
+            const long long ax = (long long)x0 + xl, ay = (long long)y0 + yl;
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
+            fast = B != nullptr && ax >= 1 && ax + 2 < G.nx && ay >= 1 && ay + 2 < G.ny && mx < qmaxf;
+            if (fast) {
+              int q[32];
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                q[k] = __float2int_rn(__fmul_rn(v[k], G.scale_f));  // |v 2^s| < 2^29: exact
+                ent[k] = (uint32_t)q[k];
+              }
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {  // central differences at corner c: window (cx+1, cy+1)
+                const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
+                ent[32 + 2 * c] = (uint32_t)(q[pl * 16 + (cy + 1) * 4 + cx + 2] - q[pl * 16 + (cy + 1) * 4 + cx]);
+                ent[33 + 2 * c] = (uint32_t)(q[pl * 16 + (cy + 2) * 4 + cx + 1] - q[pl * 16 + cy * 4 + cx + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) ent[k] = __float_as_uint(v[k]);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              reinterpret_cast<T*>(ent)[k] = (k < 16 ? sa : sb)[((k >> 2) & 3) * PITCH + (k & 3)];
+          }
+          sm.qx[pos] = x0 + xl;
+          sm.qy[pos] = y0 + yl;
+          sm.qt[pos] = tflag | (fast ? 0x40000000 : 0);
+        }
+        __threadfence_block();
+        __syncwarp();
+        // publish per batch slot
+        if (lane == 0) {
+          int e = base;
+          while (e < base + n) {
+            const int end = min(base + n, ((e >> 5) + 1) << 5);
+            atomicAdd(&sm.wfill[(e >> 5) % NB], end - e);
+            e = end;
+          }
+        }
+        if (n0 <= SLIST) break;
+        // more survivors than the list holds: lanes keep the unlisted ones in `mask`
       }
-      if (pending) publish(e, pending);
     };
 
     int gk = 0;
@@ -1011,7 +1192,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     sc.gy0 = 0;
     while (true) {
       const int s = gk % NSTAGE;
+      pf.lap(PF_OTHER);
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk);
+      pf.lap(PF_WFULL);
       const StageMeta m = sm.meta[s];
       if (m.done) break;
       if (m.k == 0) {
@@ -1036,6 +1219,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         if (edge) scan_plane_f64<true>(S, sc, (double)thr, Sq, maxd);
         else scan_plane_f64<false>(S, sc, (double)thr, Sq, maxd);
       }
+      pf.lap(PF_SCAN);
       // survivors: a byte whose top nibble is all ones after the OR over the cube's corners;
       // bit 4r + i <-> anchor row r, position i
       auto survivors_of = [&](const uint32_t* K) {
@@ -1049,16 +1233,18 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
         return lane == 31 ? 0u : mask;  // the halo lane owns no anchors
       };
-      if (m.k > 0) {
+      // pass 0: anchors at p-1 (cube = planes p-1, p); pass 1: anchors on the last timestep (no
+      // t+1 corners: the OR runs over the plane only)
+      const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
+#pragma unroll 1
+      for (int pass = (m.k > 0 ? 0 : 1); pass < (lastg ? 2 : 1); ++pass) {
         uint32_t K[RW];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) K[r] = prevSq[r] | Sq[r];
-        enqueue(survivors_of(K), sm.plane[prev_s], S, m.p - 1, x0, y0);
+        for (int r = 0; r < RW; ++r) K[r] = pass == 0 ? (prevSq[r] | Sq[r]) : Sq[r];
+        enqueue(survivors_of(K), pass == 0 ? sm.plane[prev_s] : S, pass == 0 ? S : nullptr, pass == 0 ? m.p - 1 : m.p,
+                x0, y0);
       }
-      if (m.p == P.nt_global - 1 && m.p < m.tb) {
-        // anchors on the last timestep: no t+1 corners, the OR runs over the plane only
-        enqueue(survivors_of(Sq), S, nullptr, m.p, x0, y0);
-      }
+      pf.lap(PF_ENQ);
       __syncwarp();
       if (lane == 0) {
         if (m.k > 0) mbar_arrive(&sm.empty[prev_s]);          // plane p-1 no longer needed
@@ -1104,6 +1290,11 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       atomicMax(&sm.maxbits32, maxb32);
       atomicMax(&sm.maxbits64, (unsigned long long)__double_as_longlong(maxd));
     }
+  }
+  if (FTK_K1_PROF && lane == 0) {
+    pf.lap(PF_OTHER);
+#pragma unroll
+    for (int i = 0; i < PF_N; ++i) atomicAdd(&P.counters[CNT_PROF + i], pf.acc[i]);
   }
   __syncthreads();
   if (tid == 0) {
@@ -1171,7 +1362,7 @@ int launch_extract2d(const ExtractParams& P, cudaStream_t stream) {
   const size_t esz = P.dtype == FTK_F32 ? 4 : 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(P.field) % 16 == 0) && ((P.nx * esz) % 16 == 0);
   const bool tma = aligned && get_encode() != nullptr && !P.force_generic;
-  if (P.nx >= (1ll << 31) - 256 || P.ny >= (1ll << 31) - 64 || P.nt_global >= (1ll << 31)) return FTK_ERR_INVALID_ARG;
+  if (P.nx >= (1ll << 31) - 256 || P.ny >= (1ll << 31) - 64 || P.nt_global >= (1ll << 30)) return FTK_ERR_INVALID_ARG;
   if (P.dtype == FTK_F32) return tma ? launch_t<float, true>(P, stream) : launch_t<float, false>(P, stream);
   return tma ? launch_t<double, true>(P, stream) : launch_t<double, false>(P, stream);
 }

@@ -164,6 +164,13 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, sizeof host_cnt, cudaMemcpyDeviceToHost, stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
+  if (getenv("FTK_PRINT_PROF")) {
+    const char* names[] = {"scan", "wait_full", "enqueue", "wait_ring", "exact_wait", "exact_faces",
+                           "exact_records", "producer_wait", "other"};
+    fprintf(stderr, "K1 cycle accounting (sum over warps, Gcycles):");
+    for (int i = 0; i < 9; ++i) fprintf(stderr, " %s=%.3f", names[i], host_cnt[CNT_PROF + i] * 1e-9);
+    fprintf(stderr, " edges=%llu\n", host_cnt[CNT_EDGES]);
+  }
   if (ev.on) {
     cudaEventElapsedTime(&g_ms[0], ev.e[1], ev.e[2]);
     cudaEventElapsedTime(&g_ms[1], ev.e[2], ev.e[3]);
