@@ -70,7 +70,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def __enter__(self):
         if self.ok:
@@ -232,6 +232,15 @@ def run_ours(args):
         stop.record(stream)
         torch.cuda.synchronize(dev)
     ms_total = start.elapsed_time(stop)
+    if clk.ok and len(clk.samples) < 5:
+        # short timed regions: keep the GPU busy with the same step and sample again
+        with ClockSampler(dev.index or 0) as clk2:
+            t_end = time.perf_counter() + 0.3
+            while time.perf_counter() < t_end:
+                ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+            torch.cuda.synchronize(dev)
+        clk.samples += clk2.samples
+        clk.reasons |= clk2.reasons
     if world > 1:
         t = torch.tensor([ms_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -298,7 +307,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
