@@ -109,10 +109,6 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   int st = validate(desc);
   if (st) return st;
   if (!d_field || !n_out || !d_ws || capacity < 0 || (capacity > 0 && !d_out)) return FTK_ERR_INVALID_ARG;
-  if (desc->ndim == 3) {
-    g_last_error = "3D+t path not built yet";
-    return FTK_ERR_INVALID_ARG;
-  }
   const Layout L = layout(capacity);
   if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
   char* ws = static_cast<char*>(d_ws);
@@ -190,7 +186,6 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   return FTK_OK;
 }
 
-int launch_extract3d(const ExtractParams&, cudaStream_t) { return FTK_ERR_INVALID_ARG; }
 
 }  // namespace ftk
 

@@ -190,3 +190,49 @@ def test_c2_full_size_sampled_parity(ftk, oracle_lib):
     nb = np.add.reduceat(bnd.astype(np.int64), starts)
     assert set(np.unique(nb).tolist()) <= {2}
     assert 2.5e6 < len(rec) < 3.2e6
+
+
+# ----------------------------------------------------------------------------------- 3D + t
+@pytest.mark.parametrize("signs", [(1, 1, 1), (1, -1, 1), (-1, -1, 1), (-1, -1, -1)])
+def test_moving_extremum_3d_parity(ftk, oracle_lib, signs):
+    me = fi.MovingExtremum((20, 19, 18), 6, c0=(6.0, 7.0, 9.0), v=(1.5, 1.25, -0.75), signs=signs)
+    d, n = run_pair(ftk, oracle_lib, me.generate(), me.scale_log2)
+    assert n >= 6
+
+
+@pytest.mark.parametrize("shape,L,sigma", [
+    ((5, 18, 20, 24), 15.0, 0.0),     # ragged tiles in x, y, z
+    ((4, 13, 11, 37), None, 0.08),    # heavy noise, ragged
+])
+def test_woven3d_parity(ftk, oracle_lib, shape, L, sigma):
+    nt, nz, ny, nx = shape
+    w = fi.Woven(nx, ny, nt, L=L, sigma=sigma, nz=nz)
+    run_pair(ftk, oracle_lib, w.generate(), 26)
+
+
+def test_degenerate_3d_parity(ftk, oracle_lib):
+    for seed in range(2):
+        f = fi.random_degenerate((3, 5, 6, 7), seed=seed)
+        run_pair(ftk, oracle_lib, f, 0)
+
+
+def test_c3_closed_form_full_size(ftk, oracle_lib):
+    """C3 (128^3 x 32, moving minimum): exactly one punctured ordinal face per
+    timestep, located at c(t), type MIN, one trajectory; plus a sampled oracle window."""
+    cfg = fi.CONFIGS["C3"]
+    me = cfg.make()
+    f = me.generate(device="cuda")
+    rec = ftk.to_numpy(ftk.track(f, cfg.scale_log2))
+    ordn = rec[(rec["flags"] & ftk.CP_ORDINAL) != 0]
+    assert len(ordn) == 32
+    for r in ordn:
+        c = me.center(r["t"])
+        assert abs(r["x"] - c[0]) < 1e-9 and abs(r["y"] - c[1]) < 1e-9 and abs(r["z"] - c[2]) < 1e-9
+    assert set(rec["type"].tolist()) == {ftk.MIN}
+    assert len(set(rec["label"].tolist())) == 1
+    nt = 32
+    t_of = rec["face_id"] // 60 // (128 ** 3)
+    ta, tb = 15, 17
+    sub = f[ta: tb + 1].cpu()
+    ref, _ = oracle_lib.extract(sub.numpy(), cfg.scale_log2, t0=ta, nt_global=nt, ta=ta, tb=tb)
+    compare(rec[(t_of >= ta) & (t_of < tb)], ref, labels=False)
