@@ -208,27 +208,31 @@ def run_ours(args):
     field = w.generate(t0=t0, nt=nbuf, device=dev)
     desc = ftk.make_desc(tuple(field.shape), field.dtype, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost)
     faces = ftk.num_faces(desc)
-    comm = None  # multi-GPU stitch: see paper_2011_08697_b200/dist.py (labels local without it)
+    # multi-GPU: trajectories crossing slab seams are stitched inside ftk_cp_track (NCCL allgather of
+    # the seam pairs, host union, device relabel)
+    comm = ftk.Comm(rank, world, device=dev) if world > 1 else None
+    cptr = comm.ptr if comm is not None else None
 
     stream = torch.cuda.current_stream(dev)
     ftk.set_profiling(True)
-    rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, return_buffers=True)
+    rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, comm=cptr, return_buffers=True)
     n_punct = rec.shape[0]
     # warmup
     for _ in range(args.warmup):
-        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    k1_ms, p2_ms = [], []
+    k1_ms, p2_ms, st_ms = [], [], []
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index or 0) as clk:
         start.record(stream)
         for _ in range(args.steps):
-            ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+            ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
             ms4, st3 = ftk.last_timings()
             k1_ms.append(ms4[0])
             p2_ms.append(ms4[1])
+            st_ms.append(ms4[2])
         stop.record(stream)
         torch.cuda.synchronize(dev)
     ms_total = start.elapsed_time(stop)
@@ -237,7 +241,7 @@ def run_ours(args):
         with ClockSampler(dev.index or 0) as clk2:
             t_end = time.perf_counter() + 0.3
             while time.perf_counter() < t_end:
-                ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf)
+                ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
             torch.cuda.synchronize(dev)
         clk.samples += clk2.samples
         clk.reasons |= clk2.reasons
@@ -286,13 +290,15 @@ def run_ours(args):
                    "punctured_per_step": int(n_punct), "input": f"{field.dtype}".replace("torch.", ""),
                    "arith": "exact int64/int128 predicates, fixed-order f64 location/type, f32 prefilter",
                    "l2": "input (%.2f GB) larger than L2 (126 MB); no flush" % (field.numel() * esz / 1e9),
-                   "k1_ms": k1_avg, "pass2_ms": sum(p2_ms) / len(p2_ms)},
+                   "k1_ms": k1_avg, "pass2_ms": sum(p2_ms) / len(p2_ms),
+                   **({"stitch_ms": sum(st_ms) / len(st_ms)} if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "k_extract2d (K1)", "alg_bytes_per_launch": alg_bytes},
         "clocks": clk.summary(),
         "e2e": e2e,
-        "gpu_launches": 4 * args.steps,
+        # K1 + k_clear + k_hash_insert + k_edges + k_label; slabs add k_export and k_relabel
+        "gpu_launches": (5 + (2 if world > 1 else 0)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
@@ -300,6 +306,7 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
     return 0
 

@@ -141,6 +141,25 @@ FTK_API int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d
 FTK_API int ftk_set_profiling(int enable);
 FTK_API int ftk_last_timings(float* ms4, int64_t* stats3);
 
+/* Slab stitch, exposed step by step (ftk_cp_track with a communicator runs all of it internally).
+ * After a track call on a time slab (FTK_GHOST_PLANE and/or t0 > 0) the workspace holds two lists of
+ * (face id, local label) pairs: A = faces on the ghost plane that close a cell of this slab, with the
+ * label of their partner; B = this slab's punctured ordinal faces on its first plane.
+ * ftk_stitch_export copies them to host arrays (pairs, row-major [n][2]).  Gathered over all slabs
+ * (any transport), ftk_stitch_resolve (host only) unions the labels -- every A pair joins its label
+ * with the owner slab's label of the same face id (B) -- and returns, for the labels in `mine`, the
+ * sorted map old label -> global label (entries that change only); global labels are the minimum
+ * face id of the global trajectory, identical to a single-domain run.  ftk_relabel applies a map to
+ * device records (capacity = the one the workspace was sized for).  FTK_ERR_INVARIANT: an A face
+ * without an owner record. */
+FTK_API int ftk_stitch_export(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t capacity, int64_t* h_A,
+                              int64_t capA, int64_t* nA, int64_t* h_B, int64_t capB, int64_t* nB,
+                              ftk_stream stream);
+FTK_API int ftk_stitch_resolve(const int64_t* A, int64_t nA, const int64_t* B, int64_t nB, const int64_t* mine,
+                               int64_t nmine, int64_t* map_old, int64_t* map_new, int64_t* nmap);
+FTK_API int ftk_relabel(ftk_cp* d_out, int64_t n, const int64_t* h_map_old, const int64_t* h_map_new, int64_t nmap,
+                        void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream);
+
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);

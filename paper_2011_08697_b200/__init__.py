@@ -36,7 +36,8 @@ assert RECORD_DTYPE.itemsize == RECORD_BYTES
 EXPORTS = [
     "ftk_abi_version", "ftk_strerror", "ftk_last_error", "ftk_num_faces", "ftk_workspace_size",
     "ftk_cp_extract", "ftk_cp_track", "ftk_cp_track_host", "ftk_set_profiling", "ftk_last_timings",
-    "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy",
+    "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
+    "ftk_relabel",
 ]
 
 
@@ -83,6 +84,9 @@ def lib() -> ctypes.CDLL:
         L.ftk_comm_get_unique_id.argtypes = [P]
         L.ftk_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         L.ftk_comm_destroy.argtypes = [P]
+        L.ftk_stitch_export.argtypes = [PD, P, ctypes.c_size_t, I64, P, I64, P, P, I64, P, P]
+        L.ftk_stitch_resolve.argtypes = [P, I64, P, I64, P, I64, P, P, P]
+        L.ftk_relabel.argtypes = [P, I64, P, P, I64, P, ctypes.c_size_t, I64, P]
         _lib = L
     return _lib
 
@@ -227,3 +231,75 @@ def last_timings():
     st = (ctypes.c_int64 * 3)()
     lib().ftk_last_timings(ms, st)
     return list(ms), list(st)
+
+
+# ----------------------------------------------------------------------------- time slabs
+def _np_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+def stitch_export(field: torch.Tensor, scale_log2: int, t0: int, nt_global: int, ghost: bool, buffers: Buffers):
+    """After track() on a slab with these buffers: the slab's (A, B) pair lists as int64 [n, 2]."""
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost)
+    nA, nB = ctypes.c_int64(0), ctypes.c_int64(0)
+    args = lambda a, b, ca, cb: [ctypes.byref(desc), ctypes.c_void_p(buffers.workspace.data_ptr()),
+                                 buffers.workspace.numel(), buffers.capacity, _np_ptr(a), ca, ctypes.byref(nA),
+                                 _np_ptr(b), cb, ctypes.byref(nB), ctypes.c_void_p(_stream_ptr(field.device))]
+    st = lib().ftk_stitch_export(*args(None, None, 0, 0))
+    if st not in (OK, ERR_CAPACITY):
+        _check(st, "ftk_stitch_export")
+    A = np.zeros((nA.value, 2), np.int64)
+    B = np.zeros((nB.value, 2), np.int64)
+    _check(lib().ftk_stitch_export(*args(A, B, nA.value, nB.value)), "ftk_stitch_export")
+    return A, B
+
+
+def stitch_resolve(A: np.ndarray, B: np.ndarray, mine: np.ndarray):
+    """Host-side union over all slabs' gathered pairs; returns (old labels, new labels) for `mine`."""
+    A = np.ascontiguousarray(A, np.int64).reshape(-1, 2)
+    B = np.ascontiguousarray(B, np.int64).reshape(-1, 2)
+    mine = np.ascontiguousarray(mine, np.int64).reshape(-1)
+    old = np.zeros(max(len(mine), 1), np.int64)
+    new = np.zeros(max(len(mine), 1), np.int64)
+    n = ctypes.c_int64(0)
+    _check(lib().ftk_stitch_resolve(_np_ptr(A), len(A), _np_ptr(B), len(B), _np_ptr(mine), len(mine), _np_ptr(old),
+                                    _np_ptr(new), ctypes.byref(n)), "ftk_stitch_resolve")
+    return old[: n.value], new[: n.value]
+
+
+def relabel(rec: torch.Tensor, old: np.ndarray, new: np.ndarray, buffers: Buffers):
+    """Apply a label map to device records (rec: int64 [n, 7] view into buffers.records)."""
+    old = np.ascontiguousarray(old, np.int64)
+    new = np.ascontiguousarray(new, np.int64)
+    _check(lib().ftk_relabel(ctypes.c_void_p(rec.data_ptr()), rec.shape[0], _np_ptr(old), _np_ptr(new), len(old),
+                             ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
+                             buffers.capacity, ctypes.c_void_p(_stream_ptr(rec.device))), "ftk_relabel")
+
+
+class Comm:
+    """NCCL communicator of the library (one process per GPU).  The 128-byte unique id is created by
+    rank 0 and broadcast with torch.distributed (the process group's own backend)."""
+
+    def __init__(self, rank: int, world: int, group=None, device=None):
+        import torch.distributed as dist
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().ftk_comm_get_unique_id(uid), "ftk_comm_get_unique_id")
+        backend = dist.get_backend(group)
+        dev = device if backend == "nccl" else "cpu"
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0, group=group)
+        uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        self.ptr = ctypes.c_void_p()
+        _check(lib().ftk_comm_init(ctypes.byref(self.ptr), rank, world, uid), "ftk_comm_init")
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.ptr:
+            lib().ftk_comm_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+
+def slab_bounds(nt_global: int, world: int):
+    """Contiguous time slabs: rank r owns timesteps [b[r], b[r+1]) and reads one ghost plane."""
+    return [nt_global * r // world for r in range(world + 1)]

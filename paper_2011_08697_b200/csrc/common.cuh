@@ -21,9 +21,11 @@ enum Counter : int {
   CNT_SURVIVORS = 1,  // cubes surviving the sign prefilter
   CNT_MAXBITS = 2,    // max over |f| as IEEE bits (float bits for f32, double bits for f64)
   CNT_INVARIANT = 3,  // link: faces whose parent cell does not hold exactly one other punctured face
-  CNT_EXPORT = 4,     // slab stitch: exported boundary faces
+  CNT_EXPORT = 4,     // slab stitch: exported cross pairs (A list)
   CNT_WORK = 5,       // K1 persistent scheduler: next work item
   CNT_EDGES = 6,      // trajectory-graph edges emitted by K1 (one per cell holding two punctured faces)
+  CNT_CROSS = 7,      // slab stitch: edges whose partner face lies on the ghost plane
+  CNT_EXPORT_B = 8,   // slab stitch: own ordinal faces on the first owned plane
   CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
   CNT_N = 32
 };

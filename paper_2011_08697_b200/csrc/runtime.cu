@@ -1,7 +1,13 @@
 // runtime.cu -- host side of the C-ABI (include/ftk_cp.h): validation, workspace layout, stream
 // ordering of K1 (pass 1) and pass 2, error mapping, profiling events.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <unordered_map>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -26,7 +32,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t counters, table, edges, fid, parent, total;
+  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, total;
   u64 hcap;
 };
 
@@ -46,6 +52,14 @@ static Layout layout(i64 capacity) {
   off = align_up(off + (size_t)capacity * sizeof(i64), 256);
   L.parent = off;
   off = align_up(off + (size_t)capacity * sizeof(int), 256);
+  L.cross = off;  // slab stitch lists, [capacity][2] each
+  off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
+  L.exportA = off;
+  off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
+  L.exportB = off;
+  off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
+  L.map = off;  // relabel map: [2 capacity] old labels, then [2 capacity] new labels
+  off = align_up(off + (size_t)capacity * 4 * sizeof(long long), 256);
   L.total = off;
   return L;
 }
@@ -151,9 +165,20 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
     TP.fid = reinterpret_cast<i64*>(ws + L.fid);
     TP.parent = reinterpret_cast<int*>(ws + L.parent);
+    TP.T = desc->ndim == 2 ? 12 : 60;
+    TP.plane = desc->n[0] * desc->n[1] * desc->n[2];
+    TP.ghost_t = (desc->flags & FTK_GHOST_PLANE) ? desc->t0 + desc->nt - 1 : -1;
+    TP.first_t = desc->t0 > 0 ? desc->t0 : -1;
+    TP.cross = reinterpret_cast<long long*>(ws + L.cross);
+    TP.exportA = reinterpret_cast<long long*>(ws + L.exportA);
+    TP.exportB = reinterpret_cast<long long*>(ws + L.exportB);
     const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
     st = launch_track(TP, desc->ndim, ext, stream);
     if (st) return st;
+    if (TP.ghost_t >= 0 || TP.first_t >= 0) {
+      st = launch_export(TP, stream);
+      if (st) return st;
+    }
   }
   ev.rec(3, stream);
   unsigned long long host_cnt[CNT_N];
@@ -178,7 +203,9 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   g_stats[2] = (int64_t)host_cnt[CNT_NOUT];
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
-  if ((i64)host_cnt[CNT_NOUT] > capacity) return FTK_ERR_CAPACITY;
+  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity ||
+      (i64)host_cnt[CNT_CROSS] > capacity || (i64)host_cnt[CNT_EXPORT_B] > capacity)
+    return FTK_ERR_CAPACITY;
   if (host_cnt[CNT_INVARIANT]) {
     g_last_error = "cells with a punctured-face count not in {0, 2}: " + std::to_string(host_cnt[CNT_INVARIANT]);
     return FTK_ERR_INVARIANT;
@@ -186,6 +213,203 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   return FTK_OK;
 }
 
+
+// ------------------------------------------------------------------------------ slab stitch
+// Host resolver: A = (face id F owned by another slab, label of its partner), B = (face id F, label of F
+// on its owner slab), gathered from every slab.  Every A pair joins its label with the owner's label
+// of F; labels are face ids, so the union keeps the minimum = the min face id of the global component.
+static int stitch_resolve(const long long* A, i64 nA, const long long* B, i64 nB, const long long* mine, i64 nmine,
+                          long long* map_old, long long* map_new, i64* nmap) {
+  std::unordered_map<long long, long long> owner;
+  owner.reserve((size_t)nB * 2 + 16);
+  for (i64 i = 0; i < nB; ++i) owner[B[2 * i]] = B[2 * i + 1];
+  std::unordered_map<long long, long long> parent;
+  parent.reserve((size_t)(nA + nB) * 2 + 16);
+  auto find = [&](long long x) {
+    auto it = parent.find(x);
+    if (it == parent.end()) return x;
+    long long r = x;
+    while (true) {
+      auto jt = parent.find(r);
+      if (jt == parent.end() || jt->second == r) break;
+      r = jt->second;
+    }
+    while (x != r) {  // path compression
+      long long& px = parent[x];
+      const long long nx = px;
+      px = r;
+      x = nx;
+    }
+    return r;
+  };
+  int bad = 0;
+  for (i64 i = 0; i < nA; ++i) {
+    auto it = owner.find(A[2 * i]);
+    if (it == owner.end()) {
+      ++bad;
+      continue;
+    }
+    const long long a = find(A[2 * i + 1]), b = find(it->second);
+    if (a == b) continue;
+    if (a < b) parent[b] = a; else parent[a] = b;
+  }
+  std::vector<std::pair<long long, long long>> m;
+  m.reserve((size_t)nmine);
+  for (i64 i = 0; i < nmine; ++i) {
+    const long long r = find(mine[i]);
+    if (r != mine[i]) m.emplace_back(mine[i], r);
+  }
+  std::sort(m.begin(), m.end());
+  m.erase(std::unique(m.begin(), m.end()), m.end());
+  for (size_t i = 0; i < m.size(); ++i) {
+    map_old[i] = m[i].first;
+    map_new[i] = m[i].second;
+  }
+  *nmap = (i64)m.size();
+  if (bad) {
+    g_last_error = "slab stitch: " + std::to_string(bad) + " cross faces without an owner record";
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
+static int read_exports(const ftk_desc* desc, void* d_ws, int64_t capacity, std::vector<long long>& A,
+                        std::vector<long long>& B, cudaStream_t s) {
+  const Layout L = layout(capacity);
+  char* ws = static_cast<char*>(d_ws);
+  unsigned long long cnt[CNT_N];
+  FTK_CUDA_TRY(cudaMemcpyAsync(cnt, ws + L.counters, sizeof cnt, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  const i64 nA = (i64)cnt[CNT_CROSS], nB = (i64)cnt[CNT_EXPORT_B];
+  if (nA > capacity || nB > capacity) return FTK_ERR_CAPACITY;
+  A.resize((size_t)nA * 2);
+  B.resize((size_t)nB * 2);
+  if (nA) FTK_CUDA_TRY(cudaMemcpyAsync(A.data(), ws + L.exportA, A.size() * 8, cudaMemcpyDeviceToHost, s));
+  if (nB) FTK_CUDA_TRY(cudaMemcpyAsync(B.data(), ws + L.exportB, B.size() * 8, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  (void)desc;
+  return FTK_OK;
+}
+
+static int apply_map(ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity, const long long* map_old,
+                     const long long* map_new, i64 nmap, cudaStream_t s) {
+  if (nmap <= 0) return FTK_OK;
+  if (nmap > 2 * capacity) return FTK_ERR_CAPACITY;
+  const Layout L = layout(capacity);
+  char* ws = static_cast<char*>(d_ws);
+  long long* d_old = reinterpret_cast<long long*>(ws + L.map);
+  long long* d_new = d_old + 2 * capacity;
+  FTK_CUDA_TRY(cudaMemcpyAsync(d_old, map_old, (size_t)nmap * 8, cudaMemcpyHostToDevice, s));
+  FTK_CUDA_TRY(cudaMemcpyAsync(d_new, map_new, (size_t)nmap * 8, cudaMemcpyHostToDevice, s));
+  int st = launch_relabel(d_out, n, d_old, d_new, nmap, s);
+  if (st) return st;
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  return FTK_OK;
+}
+
+// ---- NCCL, loaded at ftk_comm_init (torch's libnccl.so.2 when torch is already loaded)
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      g_last_error = std::string("dlopen libnccl.so.2: ") + dlerror();
+      return false;
+    }
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    return getUniqueId && commInitRank && allGather && commDestroy && getErrorString;
+  }
+};
+static NcclApi g_nccl;
+
+}  // namespace ftk
+
+struct ftk_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  long long* d_send = nullptr;  // library-owned exchange buffers, grown on demand
+  long long* d_recv = nullptr;
+  size_t cap_pairs = 0;
+};
+
+namespace ftk {
+
+static int nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return FTK_OK;
+  g_last_error = std::string(what) + ": " + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "nccl error");
+  return FTK_ERR_NCCL;
+}
+
+// exchange this slab's A and B lists with every slab (two allgathers over NVLink), resolve, relabel
+static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity,
+                       cudaStream_t s) {
+  std::vector<long long> A, B;
+  int st = read_exports(desc, d_ws, capacity, A, B, s);
+  if (st) return st;
+  const long long nA = (long long)A.size() / 2, nB = (long long)B.size() / 2;
+  // counts
+  if (c->cap_pairs < 1) {
+    c->cap_pairs = 1024;
+    FTK_CUDA_TRY(cudaMalloc(&c->d_send, c->cap_pairs * 2 * 8));
+    FTK_CUDA_TRY(cudaMalloc(&c->d_recv, c->cap_pairs * 2 * 8 * c->world));
+  }
+  long long mycnt[2] = {nA, nB};
+  FTK_CUDA_TRY(cudaMemcpyAsync(c->d_send, mycnt, 16, cudaMemcpyHostToDevice, s));
+  st = nccl_check(g_nccl.allGather(c->d_send, c->d_recv, 2, ncclInt64, c->comm, s), "ncclAllGather(counts)");
+  if (st) return st;
+  std::vector<long long> counts((size_t)c->world * 2);
+  FTK_CUDA_TRY(cudaMemcpyAsync(counts.data(), c->d_recv, counts.size() * 8, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  long long maxA = 0, maxB = 0;
+  for (int r = 0; r < c->world; ++r) {
+    maxA = std::max(maxA, counts[2 * r]);
+    maxB = std::max(maxB, counts[2 * r + 1]);
+  }
+  const size_t per = (size_t)(maxA + maxB);  // pairs per rank, padded
+  if (per > c->cap_pairs) {
+    cudaFree(c->d_send);
+    cudaFree(c->d_recv);
+    c->cap_pairs = per * 2;
+    FTK_CUDA_TRY(cudaMalloc(&c->d_send, c->cap_pairs * 2 * 8));
+    FTK_CUDA_TRY(cudaMalloc(&c->d_recv, c->cap_pairs * 2 * 8 * c->world));
+  }
+  std::vector<long long> sendbuf(per * 2, -1);
+  std::copy(A.begin(), A.end(), sendbuf.begin());
+  std::copy(B.begin(), B.end(), sendbuf.begin() + (size_t)maxA * 2);
+  if (per) {
+    FTK_CUDA_TRY(cudaMemcpyAsync(c->d_send, sendbuf.data(), per * 16, cudaMemcpyHostToDevice, s));
+    st = nccl_check(g_nccl.allGather(c->d_send, c->d_recv, per * 2, ncclInt64, c->comm, s), "ncclAllGather(pairs)");
+    if (st) return st;
+  }
+  std::vector<long long> all(per * 2 * c->world);
+  if (per) FTK_CUDA_TRY(cudaMemcpyAsync(all.data(), c->d_recv, all.size() * 8, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<long long> GA, GB;
+  for (int r = 0; r < c->world; ++r) {
+    const long long* base = all.data() + (size_t)r * per * 2;
+    GA.insert(GA.end(), base, base + counts[2 * r] * 2);
+    GB.insert(GB.end(), base + maxA * 2, base + maxA * 2 + counts[2 * r + 1] * 2);
+  }
+  std::vector<long long> mine;
+  for (long long i = 0; i < nA; ++i) mine.push_back(A[2 * i + 1]);
+  for (long long i = 0; i < nB; ++i) mine.push_back(B[2 * i + 1]);
+  std::vector<long long> mo(mine.size() + 1), mn(mine.size() + 1);
+  i64 nmap = 0;
+  st = stitch_resolve(GA.data(), (i64)GA.size() / 2, GB.data(), (i64)GB.size() / 2, mine.data(), (i64)mine.size(),
+                      mo.data(), mn.data(), &nmap);
+  if (st) return st;
+  return apply_map(d_out, n, d_ws, capacity, mo.data(), mn.data(), nmap, s);
+}
 
 }  // namespace ftk
 
@@ -251,11 +475,60 @@ int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int
 
 int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
                  void* d_ws, size_t ws_bytes, ftk_stream stream, ftk_comm* comm) {
-  if (comm) {
-    g_last_error = "multi-GPU stitch not built yet";
-    return FTK_ERR_NCCL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int st = run(desc, d_field, d_out, capacity, n_out, d_ws, ws_bytes, s, true);
+  if (st || !comm || comm->world <= 1) return st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_profiling) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
   }
-  return run(desc, d_field, d_out, capacity, n_out, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), true);
+  st = stitch_nccl(comm, desc, d_out, *n_out, d_ws, capacity, s);
+  if (g_profiling) {
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&g_ms[2], e0, e1);
+    g_ms[3] += g_ms[2];
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return st;
+}
+
+int ftk_stitch_export(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t capacity, int64_t* h_A,
+                      int64_t capA, int64_t* nA, int64_t* h_B, int64_t capB, int64_t* nB, ftk_stream stream) {
+  int st = validate(desc);
+  if (st) return st;
+  if (!d_ws || !nA || !nB || ws_bytes < layout(capacity).total) return FTK_ERR_INVALID_ARG;
+  std::vector<long long> A, B;
+  st = read_exports(desc, d_ws, capacity, A, B, reinterpret_cast<cudaStream_t>(stream));
+  if (st) return st;
+  *nA = (int64_t)A.size() / 2;
+  *nB = (int64_t)B.size() / 2;
+  if (*nA > capA || *nB > capB) return FTK_ERR_CAPACITY;
+  if (h_A) std::copy(A.begin(), A.end(), h_A);
+  if (h_B) std::copy(B.begin(), B.end(), h_B);
+  return FTK_OK;
+}
+
+int ftk_stitch_resolve(const int64_t* A, int64_t nA, const int64_t* B, int64_t nB, const int64_t* mine,
+                       int64_t nmine, int64_t* map_old, int64_t* map_new, int64_t* nmap) {
+  if ((nA && !A) || (nB && !B) || (nmine && !mine) || !nmap || (nmine && (!map_old || !map_new)))
+    return FTK_ERR_INVALID_ARG;
+  i64 n = 0;
+  const int st = stitch_resolve(reinterpret_cast<const long long*>(A), nA, reinterpret_cast<const long long*>(B), nB,
+                                reinterpret_cast<const long long*>(mine), nmine,
+                                reinterpret_cast<long long*>(map_old), reinterpret_cast<long long*>(map_new), &n);
+  *nmap = n;
+  return st;
+}
+
+int ftk_relabel(ftk_cp* d_out, int64_t n, const int64_t* h_map_old, const int64_t* h_map_new, int64_t nmap,
+                void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+  if (!d_ws || ws_bytes < layout(capacity).total || (nmap && (!h_map_old || !h_map_new))) return FTK_ERR_INVALID_ARG;
+  return apply_map(d_out, n, d_ws, capacity, reinterpret_cast<const long long*>(h_map_old),
+                   reinterpret_cast<const long long*>(h_map_new), nmap, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, ftk_cp* d_out, ftk_cp* h_out,
@@ -288,17 +561,39 @@ int ftk_last_timings(float* ms4, int64_t* stats3) {
 }
 
 int ftk_comm_get_unique_id(uint8_t id[128]) {
-  (void)id;
-  g_last_error = "NCCL communicator not built yet";
-  return FTK_ERR_NCCL;
+  if (!id) return FTK_ERR_INVALID_ARG;
+  if (!g_nccl.load()) return FTK_ERR_NCCL;
+  ncclUniqueId u;
+  const int st = nccl_check(g_nccl.getUniqueId(&u), "ncclGetUniqueId");
+  if (st) return st;
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id, &u, 128);
+  return FTK_OK;
 }
+
 int ftk_comm_init(ftk_comm** comm, int rank, int world, const uint8_t id[128]) {
-  (void)comm; (void)rank; (void)world; (void)id;
-  g_last_error = "NCCL communicator not built yet";
-  return FTK_ERR_NCCL;
+  if (!comm || !id || world < 1 || rank < 0 || rank >= world) return FTK_ERR_INVALID_ARG;
+  if (!g_nccl.load()) return FTK_ERR_NCCL;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ftk_comm* c = new ftk_comm();
+  c->rank = rank;
+  c->world = world;
+  const int st = nccl_check(g_nccl.commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+  if (st) {
+    delete c;
+    return st;
+  }
+  *comm = c;
+  return FTK_OK;
 }
+
 int ftk_comm_destroy(ftk_comm* comm) {
-  (void)comm;
+  if (!comm) return FTK_OK;
+  if (comm->comm && g_nccl.commDestroy) g_nccl.commDestroy(comm->comm);
+  cudaFree(comm->d_send);
+  cudaFree(comm->d_recv);
+  delete comm;
   return FTK_OK;
 }
 

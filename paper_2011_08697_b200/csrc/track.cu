@@ -119,7 +119,19 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (i64)gridDim.x * blockDim.x) {
     const long long a = P.edges[2 * e];
     long long b = P.edges[2 * e + 1];
-    if (b < 0) b = lookup(P, hm, -1 - b);  // face owned by the neighbour cube
+    if (b < 0) {
+      const long long f = -1 - b;
+      b = lookup(P, hm, f);  // face owned by the neighbour cube
+      if (b < 0 && P.ghost_t >= 0 && f / P.T / P.plane == P.ghost_t && a >= 0 && a < nrec) {
+        // partner owned by the next time slab: stitched after the local labels are known
+        const unsigned long long c = atomicAdd(&P.counters[CNT_CROSS], 1ull);
+        if (c < (unsigned long long)P.capacity) {
+          P.cross[2 * c] = a;
+          P.cross[2 * c + 1] = f;
+        }
+        continue;
+      }
+    }
     if (a < 0 || b < 0 || a >= nrec || b >= nrec) {
       atomicAdd(&P.counters[CNT_INVARIANT], 1ull);  // a cell's partner face was never emitted
       continue;
@@ -133,6 +145,45 @@ __global__ void k_label(const __grid_constant__ TrackParams P) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const int r = uf_find(P.parent, (int)i);
     P.rec[i].label = P.fid[r];
+  }
+}
+
+// ------------------------------------------------------------------------- slab stitch (K7, K9)
+// K7: export (ghost-plane face id, local label of its partner) for every cross edge (A list) and
+// (face id, local label) for every own ordinal face on the first owned plane (B list).
+__global__ void k_export(const __grid_constant__ TrackParams P) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 i0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const i64 nc0 = (i64)P.counters[CNT_CROSS];
+  const i64 nc = nc0 < P.capacity ? nc0 : P.capacity;
+  for (i64 c = i0; c < nc; c += stride) {
+    P.exportA[2 * c] = P.cross[2 * c + 1];
+    P.exportA[2 * c + 1] = P.rec[P.cross[2 * c]].label;
+  }
+  if (P.first_t < 0) return;
+  const i64 n = n_records(P);
+  for (i64 i = i0; i < n; i += stride) {
+    const long long f = P.fid[i];
+    if (f / P.T / P.plane == P.first_t && (P.rec[i].flags & FTK_CP_ORDINAL)) {
+      const unsigned long long k = atomicAdd(&P.counters[CNT_EXPORT_B], 1ull);
+      if (k < (unsigned long long)P.capacity) {
+        P.exportB[2 * k] = f;
+        P.exportB[2 * k + 1] = P.rec[i].label;
+      }
+    }
+  }
+}
+
+// K9: replace every label found in the sorted map
+__global__ void k_relabel(ftk_cp* rec, i64 n, const long long* old_l, const long long* new_l, i64 nmap) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const long long l = rec[i].label;
+    i64 lo = 0, hi = nmap;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (old_l[mid] < l) lo = mid + 1; else hi = mid;
+    }
+    if (lo < nmap && old_l[lo] == l) rec[i].label = new_l[lo];
   }
 }
 
@@ -267,6 +318,28 @@ __global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) 
 }
 
 }  // namespace trk
+
+int launch_export(const TrackParams& P, cudaStream_t stream) {
+  using namespace trk;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_export<<<sms * 4, 256, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+int launch_relabel(ftk_cp* rec, i64 n, const long long* old_labels, const long long* new_labels, i64 nmap,
+                   cudaStream_t stream) {
+  using namespace trk;
+  if (n <= 0 || nmap <= 0) return FTK_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_relabel<<<sms * 4, 256, 0, stream>>>(rec, n, old_labels, new_labels, nmap);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
 
 int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t stream) {
   using namespace trk;

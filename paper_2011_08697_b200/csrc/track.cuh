@@ -21,7 +21,20 @@ struct TrackParams {
   int* parent;                   // [capacity] union-find parents
   const long long* edges;        // [capacity][2] edges from K1
   bool verify;                   // also re-derive every face's parent cells in closed form
+  // time slabs (multi-GPU stitch)
+  int T;                         // face types per cube (12 / 60)
+  i64 plane;                     // vertices per timestep (nx * ny * nz)
+  i64 ghost_t;                   // global t of the ghost plane, -1 without one
+  i64 first_t;                   // global t of the first owned plane if t0 > 0, else -1
+  long long* cross;              // [capacity][2] (record, face id on the ghost plane)
+  long long* exportA;            // [capacity][2] (face id on the ghost plane, local label)
+  long long* exportB;            // [capacity][2] (own ordinal face id on the first plane, local label)
 };
+
+// map: sorted old labels (old[i] < old[i+1]) -> new labels
+int launch_relabel(ftk_cp* rec, i64 n, const long long* old_labels, const long long* new_labels, i64 nmap,
+                   cudaStream_t stream);
+int launch_export(const TrackParams& P, cudaStream_t stream);
 
 // ext = {nx, ny, nz, nt_global}
 int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t stream);
