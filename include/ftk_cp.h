@@ -44,8 +44,10 @@ typedef enum {
   FTK_ERR_INVALID_ARG = 1, /* bad descriptor / null pointer / workspace too small */
   FTK_ERR_RANGE = 2,       /* some |q| = |rint(f * 2^s)| >= 2^59 (2D) or 2^38 (3D), or a non-
                               finite input: the exact integer predicates could overflow */
-  FTK_ERR_CAPACITY = 3,    /* more records than `capacity`: *n_out = required count, contents
-                              unspecified; the call is idempotent, retry with a larger buffer */
+  FTK_ERR_CAPACITY = 3,    /* more records than `capacity` (or, 2D, more prefilter-surviving cubes
+                              than the workspace's survivor list of max(1024, capacity) entries):
+                              *n_out = the capacity to retry with, contents unspecified; the call
+                              is idempotent, retry with larger buffers */
   FTK_ERR_CUDA = 4,        /* a CUDA runtime error (message via ftk_last_error()) */
   FTK_ERR_NCCL = 5,        /* an NCCL error in the multi-GPU stitch */
   FTK_ERR_INVARIANT = 6,   /* a cell with a punctured-face count not in {0, 2}; impossible under
@@ -108,7 +110,9 @@ FTK_API const char* ftk_last_error(void);
  * classifies; used for the faces/s metric.  Host-only arithmetic. */
 FTK_API int ftk_num_faces(const ftk_desc* desc, int64_t* n_faces);
 
-/* Device workspace needed by extract/track for up to `capacity` records. */
+/* Device workspace needed by extract/track for up to `capacity` records.  It includes (2D) a
+ * list of max(1024, capacity) prefilter-surviving cubes, handed from the scan kernel to the exact
+ * kernel. */
 FTK_API int ftk_workspace_size(const ftk_desc* desc, int64_t capacity, size_t* bytes);
 
 /* Pass 1: test every owned face, write the punctured ones to d_out[0 .. *n_out)

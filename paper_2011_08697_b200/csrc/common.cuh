@@ -26,6 +26,8 @@ enum Counter : int {
   CNT_EDGES = 6,      // trajectory-graph edges emitted by K1 (one per cell holding two punctured faces)
   CNT_CROSS = 7,      // slab stitch: edges whose partner face lies on the ghost plane
   CNT_EXPORT_B = 8,   // slab stitch: own ordinal faces on the first owned plane
+  CNT_WIN = 9,        // 2D K1a: survivor-list entries reserved (chunks of FTK_K1_CHUNK; may exceed wcap)
+  CNT_HMASK = 10,     // pass 2: hash-table slot mask in use (set before the first insert)
   CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
   CNT_N = 32
 };
@@ -52,6 +54,22 @@ __device__ __forceinline__ double i128_to_double_rn(i128 v) {
 
 __device__ __forceinline__ int sgn128(i128 v) { return (v > 0) - (v < 0); }
 __device__ __forceinline__ int sgn64(i64 v) { return (v > 0) - (v < 0); }
+
+// Hash of a face id for the pass-2 table (face id -> record index; open addressing, linear probing).
+__host__ __device__ __forceinline__ u64 hash_mix(u64 k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+// slots for up to n keys: nextpow2(1.5 n), at least 1024, at most cap (a power of two)
+__host__ __device__ __forceinline__ u64 hash_slots(long long n, u64 cap) {
+  u64 h = 1024;
+  while (h < (u64)(n + n / 2) && h < cap) h <<= 1;
+  return h;
+}
 
 // Exact 2x2 determinant | ua va ; ub vb | in int128.
 __device__ __forceinline__ i128 det2(i64 ua, i64 va, i64 ub, i64 vb) {

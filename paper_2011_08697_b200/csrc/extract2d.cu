@@ -18,16 +18,18 @@
 //     nibble with a zero bit means one gradient component has one strict sign on every corner, so no
 //     face of the cube can contain the origin -- even under SoS (the perturbation is infinitesimal).
 //     Grid boundaries are handled by patching the neighbour values in registers (one-sided
-//     differences) and masking codes of positions outside the grid.  For each surviving cube
-//     (~0.45% on the woven field) the warp copies its 4x4x2 window of raw values into a CTA window
-//     ring (1 LDS + 1 STS per lane) and moves on.
+//     differences) and masking codes of positions outside the grid.  The plane stage is released as
+//     soon as all scan warps are through it; the anchors of the surviving cubes (~0.5% on the woven
+//     field, ~2 per warp and plane) go into a CTA survivor queue (3 words each).
 //
-//   3 exact warps -- take the ring in batches of 32 cubes (one per lane): exact int32 quantization
-//     and gradients, the 19 distinct 2x2 determinants of the cube's 12 faces, SoS point-in-simplex
-//     (an exact int64/int128 path covers boundary cubes, zero determinants and
-//     large values); the punctured faces are then spread over the lanes and each gets its Eq. 2
-//     location and Hessian type in fixed-order FP64 (no FMA), written with one global atomic per
-//     batch.
+//   3 exact warps -- take the queue in batches of 32 cubes (one per lane), fetch each cube's 4x4x2
+//     window from global memory (it was streamed through L2 microseconds earlier), exact int32
+//     quantization and gradients, the 19 distinct 2x2 determinants of the cube's 12 faces, SoS
+//     point-in-simplex (an exact int64/int128 path covers boundary cubes, zero
+//     determinants and large values); the punctured faces are then spread over the lanes and each gets
+//     its Eq. 2 location and Hessian type in fixed-order FP64 (no FMA), written with one global atomic
+//     per batch.  Exact work never holds a plane stage, so the TMA pipeline keeps NSTAGE-1 planes in
+//     flight per CTA whatever the survivor density.
 #include <cuda.h>
 
 #include <algorithm>
@@ -58,13 +60,30 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count = 1) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+#ifndef FTK_K1_HINT
+#define FTK_K1_HINT 0
+#endif
+#ifndef FTK_K1_MBSLEEP
+#define FTK_K1_MBSLEEP 32     // scan warps waiting for a plane
+#endif
+#ifndef FTK_K1_PRODSLEEP
+#define FTK_K1_PRODSLEEP 256  // the producer waiting for a free stage
+#endif
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t done;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
+  if (FTK_K1_HINT) {  // suspend-time hint (ns)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)FTK_K1_HINT)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
   return done != 0;
 }
 __device__ __forceinline__ unsigned long long gtimer_ns() {
@@ -79,11 +98,35 @@ __device__ __noinline__ void wait_timeout(int what, int a, int b) {
            threadIdx.x >> 5);
   __trap();
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what, int a) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what, int a, int sleep_ns) {
   if (mbar_try(bar, parity)) return;
+  // back off: a spinning warp takes issue slots from the scan warps on its SMSP
   const unsigned long long t0 = gtimer_ns();
-  while (!mbar_try(bar, parity))
-    if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
+  int spins = 0;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(sleep_ns);
+    if ((++spins & 15) == 0) {
+      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
+    }
+  }
+}
+// the producer's wait for a free stage: try_wait with a suspend-time hint, so the warp sleeps in
+// hardware until the phase completes (no issue slots spent) -- bounded by the same 2 s trap
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, int what, int a) {
+  const unsigned long long t0 = gtimer_ns();
+  int spins = 0;
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (done) return;
+    if ((++spins & 15) == 0) {
+      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
+    }
+  }
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
@@ -98,7 +141,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 #ifndef FTK_K1_PROF
 #define FTK_K1_PROF 0
 #endif
-enum ProfSlot { PF_SCAN = 0, PF_WFULL, PF_ENQ, PF_WRING, PF_EXWAIT, PF_EXFACE, PF_EXREC, PF_PRODWAIT, PF_OTHER, PF_N };
+enum ProfSlot { PF_SCAN = 0, PF_WFULL, PF_ENQ, PF_WRING, PF_EXWAIT, PF_EXLOAD, PF_EXFACE, PF_EXREC, PF_PRODWAIT, PF_OTHER, PF_N };
 struct Prof {
   unsigned long long acc[PF_N];
   unsigned long long t;
@@ -143,56 +186,31 @@ __device__ __forceinline__ uint32_t push_sign(uint32_t W, uint32_t bits) { retur
 constexpr int LX = 128;             // x positions scanned per warp row (32 lanes x 4)
 constexpr int TX = 124;             // anchors owned per tile in x: lane 31 is a halo lane whose codes
                                     // only complete lane 30's cubes (a cube needs its x+1 corners)
-constexpr int RW = 4;               // anchor rows per scan warp
+#ifndef FTK_K1_RW
+#define FTK_K1_RW 8
+#endif
+constexpr int RW = FTK_K1_RW;       // anchor rows per scan warp (4 or 8)
 constexpr int NSW = 8;              // scan warps
-#ifndef FTK_K1_NEW
-#define FTK_K1_NEW 3
-#endif
-#ifndef FTK_K1_DYN
-#define FTK_K1_DYN 1
-#endif
-constexpr int NEW = FTK_K1_NEW;     // exact warps
-constexpr int NWARPS = NSW + 1 + NEW;
-// Roles by warp id.  A warp runs on SMSP (id % 4): the exact warps get SMSP 3 to themselves (ids
-// 3, 7, 11) so their large code does not evict the scan loop from the per-SMSP instruction cache;
-// the producer is id 10; ids 0-2, 4-6, 8-9 scan.
-#ifndef FTK_K1_REMAP
-#define FTK_K1_REMAP 0
-#endif
-#if FTK_K1_REMAP
-constexpr int PRODUCER = 10;
-__host__ __device__ constexpr bool is_exact(int w) { return (w & 3) == 3; }
-__host__ __device__ constexpr int exact_index(int w) { return w >> 2; }
-__host__ __device__ constexpr int scan_index(int w) { return w - (w >> 2); }
-#else
-constexpr int PRODUCER = NSW;
-__host__ __device__ constexpr bool is_exact(int w) { return w > NSW; }
-__host__ __device__ constexpr int exact_index(int w) { return w - NSW - 1; }
-__host__ __device__ constexpr int scan_index(int w) { return w; }
-#endif
-constexpr int NTHREADS = NWARPS * 32;
+constexpr int PRODUCER = NSW;       // warp id of the TMA producer
+constexpr int NTHREADS = (NSW + 1) * 32;
 constexpr int TY = RW * NSW;        // 32 anchor rows per tile
 constexpr int XOFF = 4;             // smem column of x0
 constexpr int YOFF = 1;             // smem row of y0
 constexpr int PITCH = LX + 8;       // x0-4 .. x0+131
 constexpr int ROWS = TY + 3;        // y0-1 .. y0+33
 #ifndef FTK_K1_NSTAGE
-#define FTK_K1_NSTAGE 3
+#define FTK_K1_NSTAGE (RW == 8 ? 3 : 5)
 #endif
-#ifndef FTK_K1_NB
-#define FTK_K1_NB 8
+#ifndef FTK_K1_MINB
+#define FTK_K1_MINB 2
 #endif
-constexpr int NSTAGE = FTK_K1_NSTAGE;
-constexpr int NB = FTK_K1_NB;       // window-ring batch slots (32 cubes each)
-constexpr int RING = NB * 32;
-// Ring entry (32-bit words): [0, 32) the cube's 4x4x2 window W[pl*16 + r*4 + c] at
-// (x - 1 + c, y - 1 + r, t + pl) -- as exact int32 q values for fast entries (fp32 input, interior
-// cube, |q| < 2^29), else as raw values; [32, 48) the 8 corner gradients (fast entries).
-template <typename T>
-constexpr int ws_words() { return sizeof(T) == 4 ? 49 : 66; }  // odd stride for fp32: no bank conflicts
-constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
+#ifndef FTK_K1_CHUNK
+#define FTK_K1_CHUNK 32
+#endif
+constexpr int CHUNK = FTK_K1_CHUNK; // window-buffer entries a scan warp reserves at a time
 constexpr int TCHUNK = 32;          // anchor timesteps per work item
-constexpr int SLIST = 32;           // survivors enqueued per pass (one per lane)
+template <typename T>
+constexpr int nstage() { return sizeof(T) == 4 ? FTK_K1_NSTAGE : 3; }
 
 template <typename T>
 constexpr int stage_elems() {       // plane tile padded to a multiple of 128 bytes (TMA alignment)
@@ -209,25 +227,39 @@ struct StageMeta {                  // written by the producer before the plane 
 };
 
 template <typename T>
-struct alignas(128) Smem {
+struct alignas(128) ScanSmem {
+  static constexpr int NSTAGE = nstage<T>();
   T plane[NSTAGE][stage_elems<T>()];
-  uint32_t ring[RING * ws_words<T>()];  // queued survivor cubes (see ws_words)
-  int qx[RING], qy[RING], qt[RING];  // cube anchor; qt bit 31: the t+1 plane exists, bit 30: fast entry
-  uint16_t items[NEW][MAXITEMS];   // punctured faces of a batch: entry | type << 5
-  uint16_t slist[NSW][SLIST];      // per scan warp: survivors being enqueued (xl | yl << 8)
-  int scount[NSW];
   StageMeta meta[NSTAGE];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
-  int wfill[NB];                   // entries ever written into each batch slot (monotone)
-  volatile int wcons[NB];          // generations of each batch slot consumed by the exact warps
-  int tail;                        // window-ring entries reserved so far
-  int next_batch;                  // dynamic batch assignment to the exact warps
-  int scan_done;
-  volatile int nbatch;             // batches in total, -1 until the scan warps are done
   unsigned long long surv;
   unsigned int maxbits32;
   unsigned long long maxbits64;
+};
+
+// K1b: a batch of 32 cubes per warp.  Entry (32-bit words): [0, 32) the cube's 4x4x2 window
+// W[pl*16 + r*4 + c] at (x - 1 + c, y - 1 + r, t + pl) -- as exact int32 q values for fast entries
+// (fp32 input, interior cube, |q| < 2^29), else as raw values; [32, 48) the 8 corner gradients
+// (fast entries).
+template <typename T>
+constexpr int ws_words() { return sizeof(T) == 4 ? 49 : 66; }  // odd stride for fp32: no bank conflicts
+constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
+constexpr int EXW = 8;              // warps per K1b block
+
+struct BatchBuf {                   // one warp's batch in shared memory
+  uint32_t* ring;                   // [32][ws_words]
+  int* qx;
+  int* qy;
+  int* qt;                          // t | (t+1 exists) << 31 | fast << 30, -1: no cube
+  uint16_t* items;                  // punctured faces of the batch: entry | type << 5
+};
+
+template <typename T>
+struct ExSmem {
+  uint32_t ring[EXW * 32 * ws_words<T>()];
+  int qx[EXW * 32], qy[EXW * 32], qt[EXW * 32];
+  uint16_t items[EXW][MAXITEMS];
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -239,11 +271,23 @@ __device__ __forceinline__ i64 quant(float f, float scale_f, double) {
 }
 __device__ __forceinline__ i64 quant(double f, float, double scale) { return __double2ll_rn(__dmul_rn(f, scale)); }
 
+// pass-2 bookkeeping of a new record (2D track): compact face id, union-find root, hash insert
+// (face ids are unique: the first empty slot of the probe sequence is claimed)
+__device__ __forceinline__ void register_record(const ExtractParams& P, unsigned long long slot, long long fid,
+                                                unsigned long long hm) {
+  P.fid[slot] = fid;
+  if (P.table) {
+    u64 h = hash_mix((u64)fid) & hm;
+    while (atomicCAS(&P.table[h], -1, (int)slot) != -1) h = (h + 1) & hm;
+  }
+}
+
 struct Geo {
   i64 nx, ny, ntg;   // grid extents (t = global)
   float scale_f;
   double scale;
   double qmax;       // |f| below this quantizes to |q| < 2^29 (int32 fast path)
+  unsigned long long hm;  // pass-2 hash-table slot mask (2D track)
 };
 
 template <typename T>
@@ -294,9 +338,17 @@ struct Face3 {
   static constexpr int m1 = kKuhn3.masks[K][0];
   static constexpr int m2 = kKuhn3.masks[K][1];
 };
+// the masks of face type ty as 3-bit fields of two packed constants (two shifts, no branches)
+template <int... K>
+constexpr unsigned long long pack_masks(int which, std::integer_sequence<int, K...>) {
+  return ((((unsigned long long)(which == 1 ? Face3<K>::m1 : Face3<K>::m2)) << (3 * K)) | ...);
+}
+constexpr unsigned long long kM1 = pack_masks(1, std::make_integer_sequence<int, 12>{});
+constexpr unsigned long long kM2 = pack_masks(2, std::make_integer_sequence<int, 12>{});
 template <int... K>
 __device__ __forceinline__ void masks_of(int ty, int& m1, int& m2, std::integer_sequence<int, K...>) {
-  ((ty == K ? (m1 = Face3<K>::m1, m2 = Face3<K>::m2, 0) : 0), ...);
+  m1 = (int)((kM1 >> (3 * ty)) & 7);
+  m2 = (int)((kM2 >> (3 * ty)) & 7);
 }
 
 // The 6 cells (3-simplices) anchored at a cube: axis permutations (p1, p2, p3) of {x=1, y=2, t=4},
@@ -547,6 +599,7 @@ __device__ __noinline__ void emit_record_general(const Win<T>& w, const Geo& G, 
   if (slot < (unsigned long long)P.capacity) {
     ftk_cp* r = P.out + slot;
     r->face_id = ((t * G.ny + y) * G.nx + x) * 12 + ty;
+    register_record(P, slot, r->face_id, G.hm);
     r->label = -1;
     r->x = lx;
     r->y = ly;
@@ -557,11 +610,12 @@ __device__ __noinline__ void emit_record_general(const Win<T>& w, const Geo& G, 
   }
 }
 
-__device__ __forceinline__ void store_record(const ExtractParams& P, unsigned long long slot, long long fid, double lx,
-                                             double ly, double lt, int type, uint32_t flags) {
+__device__ __forceinline__ void store_record(const ExtractParams& P, unsigned long long hm, unsigned long long slot,
+                                             long long fid, double lx, double ly, double lt, int type, uint32_t flags) {
   if (slot < (unsigned long long)P.capacity) {
     ftk_cp* r = P.out + slot;
     r->face_id = fid;
+    register_record(P, slot, fid, hm);
     r->label = -1;
     r->x = lx;
     r->y = ly;
@@ -633,20 +687,20 @@ __device__ __forceinline__ void emit_record(const Win<T>& w, const Geo& G, const
     const int c = 7 & ~span;
     if (c == 4 && (t == 0 || t == G.ntg - 1)) flags |= FTK_CP_BOUNDARY;
   }
-  store_record(P, slot, ((t * G.ny + y) * G.nx + x) * 12 + ty, lx, ly, lt, type, flags);
+  store_record(P, G.hm, slot, ((t * G.ny + y) * G.nx + x) * 12 + ty, lx, ly, lt, type, flags);
 }
 
-// One batch of 32 ring entries (one cube per lane): face tests, then the punctured faces spread
-// over the lanes for the record stage.
+// One batch of 32 entries (one cube per lane): face tests, then the punctured faces spread over the
+// lanes for the record stage.
 template <typename T>
-__device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G, const ExtractParams& P, Prof& pf) {
+__device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractParams& P, Prof& pf) {
   const int lane = threadIdx.x & 31;
-  const int e = base_entry + lane;
-  const int qtv = sm.qt[e];
+  const int e = lane;
+  const int qtv = bb.qt[e];
   const bool valid = qtv != -1;
-  const i64 x = sm.qx[e], y = sm.qy[e], t = qtv & 0x3fffffff;
+  const i64 x = bb.qx[e], y = bb.qy[e], t = qtv & 0x3fffffff;
   const bool hasB = (qtv >> 31) & 1;
-  const uint32_t* E = sm.ring + e * ws_words<T>();
+  const uint32_t* E = bb.ring + e * ws_words<T>();
   const bool isq = (qtv >> 30) & 1;
   uint32_t m = 0;
   if (valid) {
@@ -668,11 +722,36 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
                           (((pmask >> d.tc) & 1u) << 2) | (((umask >> C) & 1u) << 3);                     \
     const int k = __popc(bits);                                                                          \
     epair[C] = (full && k == 2) ? bits : 0u;                                                             \
-    ecnt += (full && k == 2) ? 1 : 0;                                                                    \
+    ecnt += (full && k == 2 && (bits & 8u)) ? 1 : 0;                                                     \
     bad += (full && k != 0 && k != 2) ? 1 : 0;                                                           \
   }
   FTK_CELLCNT(0) FTK_CELLCNT(1) FTK_CELLCNT(2) FTK_CELLCNT(3) FTK_CELLCNT(4) FTK_CELLCNT(5)
 #undef FTK_CELLCNT
+  // Pairs of two own faces are joined right here: a union-find over the cube's 12 face types
+  // (4-bit parent fields; the root is the smallest type = the smallest face id), written into the
+  // global parent array once the records have slots.  Only pairs with the upper face (owned by a
+  // neighbour cube) become trajectory-graph edges for pass 2.
+  unsigned long long lp = 0xBA9876543210ull;
+  auto lfind = [&](int ty) {
+    int p = (int)((lp >> (4 * ty)) & 15);
+    while (p != ty) {
+      ty = p;
+      p = (int)((lp >> (4 * ty)) & 15);
+    }
+    return ty;
+  };
+#pragma unroll
+  for (int C = 0; C < 6; ++C) {
+    const uint32_t bits = epair[C];
+    if (bits && !(bits & 8u)) {
+      const int cd = cCell[C];
+      const int t1 = (bits & 1u) ? (cd & 15) : ((cd >> 4) & 15);
+      const int t2 = (bits & 4u) ? ((cd >> 8) & 15) : ((cd >> 4) & 15);
+      const int r1 = lfind(t1), r2 = lfind(t2);
+      const int lo = min(r1, r2), hi = max(r1, r2);
+      lp = (lp & ~(15ull << (4 * hi))) | ((unsigned long long)lo << (4 * hi));
+    }
+  }
   if (bad) atomicAdd(&P.counters[CNT_INVARIANT], (unsigned long long)bad);
   // spread the punctured faces over the lanes; reserve record and edge slots
   const int cnt = __popc(pmask);
@@ -691,7 +770,7 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   if (total == 0) return;
   unsigned long long ebase = 0;
   if (lane == 0 && etotal) ebase = atomicAdd(&P.counters[CNT_EDGES], (unsigned long long)etotal);
-  uint16_t* items = sm.items[ew];
+  uint16_t* items = bb.items;
   {
     int pos = incl - cnt;
     uint32_t pm = pmask;
@@ -705,28 +784,30 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   if (lane == 0) obase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
   obase = __shfl_sync(0xffffffffu, obase, 0);
   ebase = __shfl_sync(0xffffffffu, ebase, 0);
+  // record index of own face type ty = obase + (first slot of this lane) + rank of ty in pmask
+  const long long rbase = (long long)obase + (incl - cnt);
+  if (P.parent) {
+    uint32_t pm = pmask;
+    while (pm) {
+      const int ty = __ffs(pm) - 1;
+      pm &= pm - 1;
+      const long long r = rbase + __popc(pmask & ((1u << ty) - 1u));
+      const int root = lfind(ty);
+      if (r < P.capacity) P.parent[r] = (int)(rbase + __popc(pmask & ((1u << root) - 1u)));
+    }
+  }
   if (ecnt) {
-    // record index of own face type ty = obase + (first slot of this lane) + rank of ty in pmask
-    const long long rbase = (long long)obase + (incl - cnt);
     unsigned long long eslot = ebase + (unsigned long long)(eincl - ecnt);
 #pragma unroll 1
     for (int C = 0; C < 6; ++C) {
       const uint32_t bits = epair[C];
-      if (!bits) continue;
+      if (!(bits & 8u)) continue;
       const int cd = cCell[C];  // ta | tb << 4 | tc << 8 | axis << 12 | tf << 16
-      long long a = -1, b = -1;
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if ((bits >> q) & 1u) {
-          const int ty = (cd >> (4 * q)) & 15;
-          const long long r = rbase + __popc(pmask & ((1u << ty) - 1u));
-          if (a < 0) a = r; else b = r;
-        }
-      if (bits & 8u) {
-        const int axis = (cd >> 12) & 7, tf = (cd >> 16) & 15;
-        const i64 fx = x + (axis & 1), fy = y + ((axis >> 1) & 1), ft = t + ((axis >> 2) & 1);
-        b = -1 - (((ft * G.ny + fy) * G.nx + fx) * 12 + tf);
-      }
+      const int ty = (bits & 1u) ? (cd & 15) : ((bits & 2u) ? ((cd >> 4) & 15) : ((cd >> 8) & 15));
+      const long long a = rbase + __popc(pmask & ((1u << ty) - 1u));
+      const int axis = (cd >> 12) & 7, tf = (cd >> 16) & 15;
+      const i64 fx = x + (axis & 1), fy = y + ((axis >> 1) & 1), ft = t + ((axis >> 2) & 1);
+      const long long b = -1 - (((ft * G.ny + fy) * G.nx + fx) * 12 + tf);
       if (eslot < (unsigned long long)P.capacity) {
         P.edges[2 * eslot] = a;
         P.edges[2 * eslot + 1] = b;
@@ -737,10 +818,10 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
   __syncwarp();
   for (int i = lane; i < total; i += 32) {
     const int it = items[i];
-    const int le = base_entry + (it & 31), ty = it >> 5;
-    const int lqt = sm.qt[le];
-    const Win<T> w2{sm.ring + le * ws_words<T>(), ((lqt >> 30) & 1) != 0, G.scale_f, G.scale};
-    emit_record<T>(w2, G, P, sm.qx[le], sm.qy[le], lqt & 0x3fffffff, ty, obase + i);
+    const int le = it & 31, ty = it >> 5;
+    const int lqt = bb.qt[le];
+    const Win<T> w2{bb.ring + le * ws_words<T>(), ((lqt >> 30) & 1) != 0, G.scale_f, G.scale};
+    emit_record<T>(w2, G, P, bb.qx[le], bb.qy[le], lqt & 0x3fffffff, ty, obase + i);
   }
   __syncwarp();
 }
@@ -749,17 +830,18 @@ __device__ void process_batch(Smem<T>& sm, int ew, int base_entry, const Geo& G,
 // Scan
 //
 // Code layout: position i (0..3) of a lane lives in byte i; the byte's top nibble holds, from bit 7
-// down, NOT(dx >= thr), NOT(dx <= -thr), NOT(dy >= thr), NOT(dy <= -thr) -- the sign bits of
-// dx - thr, -thr - dx, dy - thr, -thr - dy (1 = that strict sign condition does not hold).  ORing
-// codes over corners and testing for an all-ones nibble finds the cubes with no one-signed
-// component.  Low nibbles are always zero; out-of-grid positions get 0 (OR-neutral).
+// down, (dx > thr), (dx < -thr), (dy > thr), (dy < -thr) -- the sign bits of thr - dx, dx + thr,
+// thr - dy, dy + thr (1 = that strict sign of the gradient component is established).  ANDing the
+// codes over a cube's corners leaves a bit set iff that component has that sign on every corner, so
+// the cubes to keep are the ones whose byte is ZERO after the AND (found with the exact zero-byte
+// test below: low nibbles are always zero).  Positions outside the grid get 0xF0 (AND-neutral).
 // ---------------------------------------------------------------------------------------------
 struct ScanCtx {
   int srow0;       // smem row of the warp's first anchor row
   int lane;
   int rpos;        // position (0..3) of x = nx - 1 in this lane, else -1
   bool lpat;       // x = 0 is this lane's position 0
-  uint32_t xmask;  // top-nibble mask of the lane's in-grid positions
+  uint32_t xmask;  // top-nibble mask of the lane's in-grid positions (0xF0 per in-grid byte)
   long long gy0;   // global y of the warp's first anchor row
   long long ny;
 };
@@ -780,19 +862,21 @@ __device__ __forceinline__ uint32_t gather_code(const f2 (&c)[8]) {
 
 __device__ __forceinline__ uint32_t code_f32(const float4 u, const float4 v, const float4 d, float l, float r,
                                              f2 thr2, f2 nthr2) {
-  const f2 dx01 = sub2(pack2(v.y, v.z), pack2(l, v.x));
-  const f2 dx23 = sub2(pack2(v.w, r), pack2(v.y, v.z));
+  // x differences in scalar FADDs (their operands are not register-pair aligned; the results are
+  // placed in pairs by the register allocator), y differences in paired FADD2s
+  const f2 dx01 = pack2(__fsub_rn(v.y, l), __fsub_rn(v.z, v.x));
+  const f2 dx23 = pack2(__fsub_rn(v.w, v.y), __fsub_rn(r, v.z));
   const f2 dy01 = sub2(pack2(d.x, d.y), pack2(u.x, u.y));
   const f2 dy23 = sub2(pack2(d.z, d.w), pack2(u.z, u.w));
   f2 c[8];
-  c[0] = sub2(dx01, thr2);   // dx - thr
-  c[1] = sub2(dx23, thr2);
-  c[2] = sub2(nthr2, dx01);  // -thr - dx
-  c[3] = sub2(nthr2, dx23);
-  c[4] = sub2(dy01, thr2);
-  c[5] = sub2(dy23, thr2);
-  c[6] = sub2(nthr2, dy01);
-  c[7] = sub2(nthr2, dy23);
+  c[0] = sub2(thr2, dx01);   // thr - dx < 0  <=>  dx > thr
+  c[1] = sub2(thr2, dx23);
+  c[2] = sub2(dx01, nthr2);  // dx + thr < 0  <=>  dx < -thr
+  c[3] = sub2(dx23, nthr2);
+  c[4] = sub2(thr2, dy01);
+  c[5] = sub2(thr2, dy23);
+  c[6] = sub2(dy01, nthr2);
+  c[7] = sub2(dy23, nthr2);
   return gather_code(c);
 }
 
@@ -811,47 +895,52 @@ __device__ __forceinline__ uint32_t max_abs_bits(uint32_t m, float a, float b, f
 template <bool EDGE>
 __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c, f2 thr2, f2 nthr2,
                                                uint32_t (&Sq)[RW], uint32_t& maxb) {
-  constexpr int NR = RW + 3;  // rows srow0-1 .. srow0+RW+1
-  float4 v[NR];
-  float l[NR], r[NR];
+  // rows srow0-1 .. srow0+RW+1, rolled through a 3-row window: code row k needs rows k (up), k+1
+  // (centre, with its x neighbours l, r) and k+2 (down); square row k ANDs code rows k, k+1
   const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
   const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
-#pragma unroll
-  for (int i = 0; i < NR; ++i) {
+  auto load = [&](int i, float4& v, float& l, float& r) {
     const int row = c.srow0 - 1 + i;
-    v[i] = *reinterpret_cast<const float4*>(S + row * PITCH + XOFF + 4 * c.lane);
+    v = *reinterpret_cast<const float4*>(S + row * PITCH + XOFF + 4 * c.lane);
     const float h = S[row * PITCH + hcol];  // tile halo (used by lanes 0 and 31)
-    const float up = __shfl_up_sync(0xffffffffu, v[i].w, 1);
-    const float dn = __shfl_down_sync(0xffffffffu, v[i].x, 1);
-    l[i] = lane0 ? h : up;
-    r[i] = lane31 ? h : dn;
+    const float up = __shfl_up_sync(0xffffffffu, v.w, 1);
+    const float dn = __shfl_down_sync(0xffffffffu, v.x, 1);
+    l = lane0 ? h : up;
+    r = lane31 ? h : dn;
     if (EDGE) {
-      if (c.lpat) l[i] = v[i].x;
-      if (c.rpos == 0) v[i].y = v[i].x;
-      if (c.rpos == 1) v[i].z = v[i].y;
-      if (c.rpos == 2) v[i].w = v[i].z;
-      if (c.rpos == 3) r[i] = v[i].w;
+      if (c.lpat) l = v.x;
+      if (c.rpos == 0) v.y = v.x;
+      if (c.rpos == 1) v.z = v.y;
+      if (c.rpos == 2) v.w = v.z;
+      if (c.rpos == 3) r = v.w;
     }
-  }
+  };
+  float4 v0, v1, v2;
+  float l0, r0, l1, r1, l2, r2;
+  load(0, v0, l0, r0);
+  load(1, v1, l1, r1);
+  uint32_t Cprev = 0;
 #pragma unroll
-  for (int i = 1; i <= RW; ++i) maxb = max_abs_bits(maxb, v[i].x, v[i].y, v[i].z, v[i].w);
-  uint32_t C[RW + 1];
-#pragma unroll
-  for (int k = 0; k <= RW; ++k) {  // code row k = rows i = k (up), k+1 (centre), k+2 (down)
+  for (int k = 0; k <= RW; ++k) {
+    load(k + 2, v2, l2, r2);
+    if (k >= 1 && k <= RW) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);  // owned rows 1..RW
+    uint32_t C;
     if (EDGE) {
       const long long gy = c.gy0 + k;
-      const float4 u = gy == 0 ? v[k + 1] : v[k];
-      const float4 d = gy == c.ny - 1 ? v[k + 1] : v[k + 2];
-      C[k] = gy >= c.ny ? 0u : code_f32(u, v[k + 1], d, l[k + 1], r[k + 1], thr2, nthr2) & c.xmask;
+      const float4 u = gy == 0 ? v1 : v0;
+      const float4 d = gy == c.ny - 1 ? v1 : v2;
+      C = gy >= c.ny ? 0xF0F0F0F0u : code_f32(u, v1, d, l1, r1, thr2, nthr2) | (~c.xmask & 0xF0F0F0F0u);
     } else {
-      C[k] = code_f32(v[k], v[k + 1], v[k + 2], l[k + 1], r[k + 1], thr2, nthr2);
+      C = code_f32(v0, v1, v2, l1, r1, thr2, nthr2);
     }
-  }
-#pragma unroll
-  for (int k = 0; k < RW; ++k) {
-    const uint32_t Y = C[k] | C[k + 1];                      // y-pair
-    const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0 = byte 0
-    Sq[k] = Y | (Y >> 8) | (nb << 24);                       // x-pair
+    if (k >= 1) {
+      const uint32_t Y = Cprev & C;                             // y-pair
+      const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0 = byte 0
+      Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));                 // x-pair
+    }
+    Cprev = C;
+    v0 = v1; l0 = l1; r0 = r1;
+    v1 = v2; l1 = l2; r1 = r2;
   }
 }
 
@@ -897,39 +986,34 @@ __device__ __forceinline__ void scan_plane_f64(const double* S, const ScanCtx& c
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const double dx = f[k + 1][q + 2] - f[k + 1][q], dy = f[id][q + 1] - f[iu][q + 1];
-      const uint32_t nib = (sbit(dx - thr) << 3) | (sbit(-thr - dx) << 2) | (sbit(dy - thr) << 1) | sbit(-thr - dy);
+      const uint32_t nib = (sbit(thr - dx) << 3) | (sbit(dx + thr) << 2) | (sbit(thr - dy) << 1) | sbit(dy + thr);
       W |= nib << (8 * q + 4);
     }
-    C[k] = (EDGE && gy >= c.ny) ? 0u : (EDGE ? W & c.xmask : W);
+    C[k] = (EDGE && gy >= c.ny) ? 0xF0F0F0F0u : (EDGE ? W | (~c.xmask & 0xF0F0F0F0u) : W);
   }
 #pragma unroll
   for (int k = 0; k < RW; ++k) {
-    const uint32_t Y = C[k] | C[k + 1];
+    const uint32_t Y = C[k] & C[k + 1];
     const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
-    Sq[k] = Y | (Y >> 8) | (nb << 24);
+    Sq[k] = Y & ((Y >> 8) | (nb << 24));
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// The kernel
+// K1a: the scan kernel
 // ---------------------------------------------------------------------------------------------
 template <typename T, bool TMA>
-__global__ void __launch_bounds__(NTHREADS, 2)
-    k_extract2d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
+__global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
+    k_scan2d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t mis = smem_u32(smem_raw) & 127u;  // dynamic smem is only 16-byte aligned
-  Smem<T>& sm = *reinterpret_cast<Smem<T>*>(smem_raw + (mis ? 128 - mis : 0));
+  ScanSmem<T>& sm = *reinterpret_cast<ScanSmem<T>*>(smem_raw + (mis ? 128 - mis : 0));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NSTAGE = ScanSmem<T>::NSTAGE;
 
-  Geo G;
-  G.nx = P.nx;
-  G.ny = P.ny;
-  G.ntg = P.nt_global;
-  G.scale = P.scale;
-  G.scale_f = (float)P.scale;
-  G.qmax = ldexp(1.0, 29) / P.scale - 1.0 / P.scale;  // |f| < qmax -> |rint(f 2^s)| < 2^29
+  const i64 nx = P.nx, ny = P.ny;
   constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
-  const int ntx = (int)((G.nx + TX - 1) / TX), nty = (int)((G.ny + TY - 1) / TY);
+  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
   const int ntz = (int)((P.tb - P.ta + TCHUNK - 1) / TCHUNK);
   const long long nitems = (long long)ntx * nty * ntz;
 
@@ -937,17 +1021,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     sm.surv = 0;
     sm.maxbits32 = 0;
     sm.maxbits64 = 0;
-    sm.tail = 0;
-    sm.next_batch = 0;
-    sm.scan_done = 0;
-    sm.nbatch = -1;
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], NSW);
-    }
-    for (int b = 0; b < NB; ++b) {
-      sm.wfill[b] = 0;
-      sm.wcons[b] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -963,7 +1039,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     int gk = 0;  // planes issued so far (ring position)
     auto acquire = [&](int s) {
       pf.lap(PF_OTHER);
-      if (gk >= NSTAGE) mbar_wait(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
+      if (gk >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
       pf.lap(PF_PRODWAIT);
     };
     while (true) {
@@ -997,12 +1073,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           }
         } else {
           // generic loader for unaligned shapes: guarded element loads (zero outside the grid)
-          const T* src = field + (ta + k - P.t0) * G.nx * G.ny;
+          const T* src = field + (ta + k - P.t0) * nx * ny;
           T* dst = sm.plane[s];
           for (int idx = lane; idx < ROWS * PITCH; idx += 32) {
             const int rr = idx / PITCH, cc = idx - rr * PITCH;
             const i64 yy = y0 - YOFF + rr, xx = x0 - XOFF + cc;
-            dst[idx] = (yy >= 0 && yy < G.ny && xx >= 0 && xx < G.nx) ? src[yy * G.nx + xx] : (T)0;
+            dst[idx] = (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ? src[yy * nx + xx] : (T)0;
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.full[s]);
@@ -1016,44 +1092,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       sm.meta[s].done = 1;
       mbar_arrive(&sm.full[s]);
     }
-  } else if (is_exact(warp)) {
-    // ------------------------------------------------------------------ exact warps
-    const int ew = exact_index(warp);
-    for (int b = ew;; b += NEW) {
-      if (FTK_K1_DYN) {
-        int nb2 = 0;
-        if (lane == 0) nb2 = atomicAdd(&sm.next_batch, 1);
-        b = __shfl_sync(0xffffffffu, nb2, 0);
-      }
-      const int j = b % NB;
-      bool go = true;
-      const int target = 32 * (b / NB + 1);
-      if (*(volatile int*)&sm.wfill[j] < target) {
-        const unsigned long long t0 = gtimer_ns();
-        while (*(volatile int*)&sm.wfill[j] < target) {
-          const int nbf = sm.nbatch;
-          if (nbf >= 0 && b >= nbf) {
-            go = false;
-            break;
-          }
-          __nanosleep(64);
-          if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(4, b, nbf);
-        }
-      }
-      if (!go) break;
-      __threadfence_block();
-      pf.lap(PF_EXWAIT);
-#ifndef FTK_K1_DIAG_NOEXACT
-#define FTK_K1_DIAG_NOEXACT 0
-#endif
-      if (!FTK_K1_DIAG_NOEXACT) process_batch<T>(sm, ew, j * 32, G, P, pf);
-      __syncwarp();
-      pf.lap(PF_EXREC);
-      if (lane == 0) {
-        __threadfence_block();  // our reads of the slot happen before it is handed back
-        sm.wcons[j] = b / NB + 1;
-      }
-    }
   } else {
     // ------------------------------------------------------------------ scan warps
     const T thr = (T)P.thr;
@@ -1063,129 +1101,54 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     double maxd = 0.0;
     unsigned long long mysurv = 0;
     uint32_t prevSq[RW];
-    const float qmaxf = (float)G.qmax;
-    const int sw = scan_index(warp);     // scan-warp index: anchor rows sw*RW .. sw*RW + RW - 1
+    const int sw = warp;                 // scan-warp index: anchor rows sw*RW .. sw*RW + RW - 1
     const int srow0 = YOFF + sw * RW;    // smem row of this warp's first anchor row
+    // the warp's current chunk of the window buffer: entries [cur, end)
+    long long cur = 0, end = 0;
 
-    // hand the survivors (bit 4r + j <-> row r, position 3 - j) to the exact warps: reserve ring
-    // entries, copy each cube's 4x4x2 window (planes A = t, B = t+1), publish per batch slot
-    // hand the survivors (bit 4r + i <-> anchor row r, position i) to the exact warps.  They are
-    // appended to a per-warp list, ring entries are reserved for the whole list, and lane i then
-    // copies survivor i's 4x4x2 window (planes A = t, B = t+1) -- for fast entries as exact int32
-    // q values plus the 8 corner gradients -- so one pass costs the same for 1 or 32 survivors.
-    uint16_t* slist = sm.slist[sw];
-    auto enqueue = [&](uint32_t mask, const T* A, const T* B, int t, int x0, int y0) {
-      if (!__any_sync(0xffffffffu, mask != 0)) return;
-      const T* B2 = B ? B : A;
-      const int tflag = (int)((uint32_t)t | (B ? 0x80000000u : 0u));
-      while (true) {
-        // list up to SLIST survivors
-        if (lane == 0) sm.scount[sw] = 0;
-        __syncwarp();
-        const int cnt = min(__popc(mask), 32);
-        int off = 0;
-        if (cnt) off = atomicAdd(&sm.scount[sw], cnt);
-        __syncwarp();
-        const int n0 = *(volatile int*)&sm.scount[sw];
-        const int n = min(n0, SLIST);
-        {
-          int r = off;
-          while (mask && r < SLIST) {
-            const int bb = __ffs(mask) - 1;
-            mask &= mask - 1;
-            slist[r++] = (uint16_t)((4 * lane + (bb & 3)) | ((sw * RW + (bb >> 2)) << 8));
-          }
-          // survivors beyond the list capacity stay in `mask` for the next pass
+    // Hand the survivors (bit 8i + r <-> position i, anchor row r) to K1b: their anchors go into the
+    // window buffer (K1b fetches the windows from the field), in chunks of CHUNK entries reserved
+    // with one global atomic per warp and chunk.
+    auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0) {
+      while (__any_sync(0xffffffffu, mask != 0)) {
+        if (cur == end) {
+          long long c = 0;
+          if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
+          cur = __shfl_sync(0xffffffffu, c, 0);
+          end = cur + CHUNK;
         }
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&sm.tail, n);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int n = (int)min((long long)total, end - cur);
+        int r = incl - cnt;
+        while (mask && r < n) {
+          const int bb = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const long long e = cur + r++;
+          if (e < P.wcap) {
+            P.wx[e] = x0 + 4 * lane + (bb >> 3);
+            P.wy[e] = y0 + sw * RW + (bb & 7);
+            P.wt[e] = tflag;
+          }
+        }
+        cur += n;
         mysurv += n;
-        // claim every batch slot the range [base, base + n) touches
-        for (int bat = base >> 5; bat <= (base + n - 1) >> 5; ++bat) {
-          const int slot = bat % NB;
-          if (bat >= NB && sm.wcons[slot] < bat / NB) {
-            pf.lap(PF_ENQ);
-            const unsigned long long t0 = gtimer_ns();
-            while (sm.wcons[slot] < bat / NB) {
-              __nanosleep(32);
-              if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(2, bat, base);
-            }
-            pf.lap(PF_WRING);
-          }
-        }
-        __threadfence_block();
-        __syncwarp();
-#ifndef FTK_K1_DIAG_NOCOPY
-#define FTK_K1_DIAG_NOCOPY 0
-#endif
-        if (lane < n && !FTK_K1_DIAG_NOCOPY) {
-          const int code = slist[lane];
-          const int xl = code & 255, yl = code >> 8;
-          const int pos = (base + lane) % RING;
-          uint32_t* ent = sm.ring + pos * ws_words<T>();
-          const T* sa = A + (yl - 1 + YOFF) * PITCH + (xl - 1 + XOFF);
-          const T* sb = B2 + (yl - 1 + YOFF) * PITCH + (xl - 1 + XOFF);
-          bool fast = false;
-          if constexpr (sizeof(T) == 4) {
-            float v[32];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) v[k] = (k < 16 ? sa : sb)[((k >> 2) & 3) * PITCH + (k & 3)];
-            const long long ax = (long long)x0 + xl, ay = (long long)y0 + yl;
-            float mx = 0.f;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
-            fast = B != nullptr && ax >= 1 && ax + 2 < G.nx && ay >= 1 && ay + 2 < G.ny && mx < qmaxf;
-            if (fast) {
-              int q[32];
-#pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                q[k] = __float2int_rn(__fmul_rn(v[k], G.scale_f));  // |v 2^s| < 2^29: exact
-                ent[k] = (uint32_t)q[k];
-              }
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {  // central differences at corner c: window (cx+1, cy+1)
-                const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
-                ent[32 + 2 * c] = (uint32_t)(q[pl * 16 + (cy + 1) * 4 + cx + 2] - q[pl * 16 + (cy + 1) * 4 + cx]);
-                ent[33 + 2 * c] = (uint32_t)(q[pl * 16 + (cy + 2) * 4 + cx + 1] - q[pl * 16 + cy * 4 + cx + 1]);
-              }
-            } else {
-#pragma unroll
-              for (int k = 0; k < 32; ++k) ent[k] = __float_as_uint(v[k]);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 32; ++k)
-              reinterpret_cast<T*>(ent)[k] = (k < 16 ? sa : sb)[((k >> 2) & 3) * PITCH + (k & 3)];
-          }
-          sm.qx[pos] = x0 + xl;
-          sm.qy[pos] = y0 + yl;
-          sm.qt[pos] = tflag | (fast ? 0x40000000 : 0);
-        }
-        __threadfence_block();
-        __syncwarp();
-        // publish per batch slot
-        if (lane == 0) {
-          int e = base;
-          while (e < base + n) {
-            const int end = min(base + n, ((e >> 5) + 1) << 5);
-            atomicAdd(&sm.wfill[(e >> 5) % NB], end - e);
-            e = end;
-          }
-        }
-        if (n0 <= SLIST) break;
-        // more survivors than the list holds: lanes keep the unlisted ones in `mask`
       }
     };
 
     int gk = 0;
-    int prev_s = 0;
     int x0 = -1, y0 = -1;
     bool edge = false;
     ScanCtx sc;
     sc.srow0 = srow0;
     sc.lane = lane;
-    sc.ny = G.ny;
+    sc.ny = ny;
     sc.rpos = -1;
     sc.lpat = false;
     sc.xmask = 0xF0F0F0F0u;
@@ -1193,7 +1156,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     while (true) {
       const int s = gk % NSTAGE;
       pf.lap(PF_OTHER);
-      mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk);
+      mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
       pf.lap(PF_WFULL);
       const StageMeta m = sm.meta[s];
       if (m.done) break;
@@ -1202,13 +1165,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         y0 = m.y0;
         const i64 gx = (i64)x0 + 4 * lane;
         sc.gy0 = (i64)y0 + sw * RW;
-        edge = x0 < 1 || x0 + LX + 1 > G.nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > G.ny;
+        edge = x0 < 1 || x0 + LX + 1 > nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
         sc.lpat = gx == 0;
-        sc.rpos = (G.nx - 1 >= gx && G.nx - 1 <= gx + 3) ? (int)(G.nx - 1 - gx) : -1;
+        sc.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
         sc.xmask = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (gx + i < G.nx) sc.xmask |= 0xF0u << (8 * i);
+          if (gx + i < nx) sc.xmask |= 0xF0u << (8 * i);
       }
       const T* S = sm.plane[s];
       uint32_t Sq[RW];
@@ -1219,64 +1182,36 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         if (edge) scan_plane_f64<true>(S, sc, (double)thr, Sq, maxd);
         else scan_plane_f64<false>(S, sc, (double)thr, Sq, maxd);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       pf.lap(PF_SCAN);
-      // survivors: a byte whose top nibble is all ones after the OR over the cube's corners;
-      // bit 4r + i <-> anchor row r, position i
+      // survivors: zero bytes after the AND over the cube's corners (exact zero-byte test: the
+      // low nibbles are zero, so no borrow can flag a nonzero byte); bit 8i + r <-> position i,
+      // anchor row r
       auto survivors_of = [&](const uint32_t* K) {
         uint32_t mask = 0;
 #pragma unroll
-        for (int r = 0; r < RW; ++r) {
-          uint32_t z = K[r] & (K[r] << 1);
-          z &= z << 2;
-          const uint32_t mm = (z >> 7) & 0x01010101u;                 // bits 0, 8, 16, 24
-          mask |= (((mm * 0x204081u) >> 21) & 0xFu) << (4 * r);      // -> bits 0..3
-        }
+        for (int r = 0; r < RW; ++r) mask |= (((K[r] - 0x01010101u) & ~K[r] & 0x80808080u) >> (7 - r));
         return lane == 31 ? 0u : mask;  // the halo lane owns no anchors
       };
       // pass 0: anchors at p-1 (cube = planes p-1, p); pass 1: anchors on the last timestep (no
-      // t+1 corners: the OR runs over the plane only)
+      // t+1 corners: the AND runs over the plane only)
       const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
 #pragma unroll 1
       for (int pass = (m.k > 0 ? 0 : 1); pass < (lastg ? 2 : 1); ++pass) {
         uint32_t K[RW];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) K[r] = pass == 0 ? (prevSq[r] | Sq[r]) : Sq[r];
-        enqueue(survivors_of(K), pass == 0 ? sm.plane[prev_s] : S, pass == 0 ? S : nullptr, pass == 0 ? m.p - 1 : m.p,
-                x0, y0);
+        for (int r = 0; r < RW; ++r) K[r] = pass == 0 ? (prevSq[r] & Sq[r]) : Sq[r];
+        enqueue(survivors_of(K), pass == 0 ? (int)((uint32_t)(m.p - 1) | 0x80000000u) : m.p, x0, y0);
       }
       pf.lap(PF_ENQ);
-      __syncwarp();
-      if (lane == 0) {
-        if (m.k > 0) mbar_arrive(&sm.empty[prev_s]);          // plane p-1 no longer needed
-        if (m.k == m.nplanes - 1) mbar_arrive(&sm.empty[s]);  // last plane of the item
-      }
 #pragma unroll
       for (int r = 0; r < RW; ++r) prevSq[r] = Sq[r];
-      prev_s = s;
       ++gk;
     }
-
-    // the last scan warp to finish pads the final partial batch and publishes the batch count
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&sm.scan_done, 1) == NSW - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      __threadfence_block();
-      const int n = *((volatile int*)&sm.tail);
-      const int nb = (n + 31) >> 5;
-      const int pad = nb * 32 - n;
-      if (pad) {
-        const int slot = (nb - 1) % NB;
-        if (lane < pad) sm.qt[(n + lane) % RING] = -1;
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          atomicAdd(&sm.wfill[slot], pad);
-        }
-      }
-      if (lane == 0) sm.nbatch = nb;
-    }
+    // the unused rest of the warp's chunk holds no cube
+    for (long long e = cur + lane; e < end; e += 32)
+      if (e < P.wcap) P.wt[e] = -1;
 
     // statistics
 #pragma unroll
@@ -1300,6 +1235,108 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   if (tid == 0) {
     atomicAdd(&P.counters[CNT_SURVIVORS], sm.surv);
     atomicMax(&P.counters[CNT_MAXBITS], sizeof(T) == 4 ? (unsigned long long)sm.maxbits32 : sm.maxbits64);
+  }
+}
+
+// Between K1a and K1b: size the pass-2 hash table for at most min(12 survivors, capacity) records
+// (a cube has 12 faces) and clear that many slots; K1b inserts every record it stores.
+__global__ void k_table_prep(const __grid_constant__ ExtractParams P) {
+  const long long nwin = min((long long)P.counters[CNT_WIN], (long long)P.wcap);
+  const long long bound = min(12 * nwin, (long long)P.capacity);
+  const u64 hm = hash_slots(bound, P.table_cap) - 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_HMASK] = hm;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
+    P.table[i] = -1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1b: the exact kernel -- one warp per batch of 32 window-buffer entries (grid-stride, the entry
+// count is read from the device counter K1a left behind)
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(EXW * 32, 3) k_exact2d(const __grid_constant__ ExtractParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExSmem<T>& sm = *reinterpret_cast<ExSmem<T>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Geo G;
+  G.nx = P.nx;
+  G.ny = P.ny;
+  G.ntg = P.nt_global;
+  G.scale = P.scale;
+  G.scale_f = (float)P.scale;
+  G.qmax = ldexp(1.0, 29) / P.scale - 1.0 / P.scale;  // |f| < qmax -> |rint(f 2^s)| < 2^29
+  G.hm = P.counters[CNT_HMASK];
+  const float qmaxf = (float)G.qmax;
+  BatchBuf bb{sm.ring + w * 32 * ws_words<T>(), sm.qx + w * 32, sm.qy + w * 32, sm.qt + w * 32, sm.items[w]};
+  const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
+  const long long nbat = (nwin + 31) / 32;
+  const T* field = reinterpret_cast<const T*>(P.field);
+  Prof pf;
+#pragma unroll
+  for (int i = 0; i < PF_N; ++i) pf.acc[i] = 0;
+  pf.start();
+  for (long long b = (long long)blockIdx.x * EXW + w; b < nbat; b += (long long)gridDim.x * EXW) {
+    const long long e = b * 32 + lane;
+    const int et = e < nwin ? P.wt[e] : -1;
+    uint32_t* ent = bb.ring + lane * ws_words<T>();
+    bool fast = false;
+    if (et != -1) {
+      const int x = P.wx[e], y = P.wy[e];
+      const bool hasB = et < 0;
+      // the cube's 4x4x2 window (planes t and t+1; t again when t+1 is not in the domain), zero
+      // outside the grid
+      const T* pa = field + ((i64)(et & 0x3fffffff) - P.t0) * G.nx * G.ny;
+      const T* pb = hasB ? pa + G.nx * G.ny : pa;
+      const bool inner = x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny;
+      T v[32];
+      if (inner) {
+        const T* a0 = pa + (i64)(y - 1) * G.nx + (x - 1);
+        const T* b0 = pb + (i64)(y - 1) * G.nx + (x - 1);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = __ldg((k < 16 ? a0 : b0) + ((k >> 2) & 3) * G.nx + (k & 3));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const i64 xx = x - 1 + (k & 3), yy = y - 1 + ((k >> 2) & 3);
+          v[k] = (xx >= 0 && xx < G.nx && yy >= 0 && yy < G.ny) ? __ldg((k < 16 ? pa : pb) + yy * G.nx + xx) : (T)0;
+        }
+      }
+      if constexpr (sizeof(T) == 4) {
+        float mx = 0.f;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
+        fast = hasB && inner && mx < qmaxf;
+      }
+      if (fast) {
+        int qv[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          qv[k] = __float2int_rn(__fmul_rn((float)v[k], G.scale_f));  // |v 2^s| < 2^29: exact
+          ent[k] = (uint32_t)qv[k];
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // central differences at corner c: window (cx+1, cy+1)
+          const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
+          ent[32 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 1) * 4 + cx + 2] - qv[pl * 16 + (cy + 1) * 4 + cx]);
+          ent[33 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 2) * 4 + cx + 1] - qv[pl * 16 + cy * 4 + cx + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) reinterpret_cast<T*>(ent)[k] = v[k];
+      }
+      bb.qx[lane] = x;
+      bb.qy[lane] = y;
+    }
+    bb.qt[lane] = et == -1 ? -1 : (et | (fast ? 0x40000000 : 0));
+    __syncwarp();
+    pf.lap(PF_EXLOAD);
+    process_batch<T>(bb, G, P, pf);
+    __syncwarp();
+    pf.lap(PF_EXREC);
+  }
+  if (FTK_K1_PROF && lane == 0) {
+#pragma unroll
+    for (int i = 0; i < PF_N; ++i) atomicAdd(&P.counters[CNT_PROF + i], pf.acc[i]);
   }
 }
 
@@ -1343,8 +1380,8 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return launch_t<T, false>(P, stream);
   }
-  const size_t smem = sizeof(Smem<T>) + 128;
-  auto kern = k_extract2d<T, TMA>;
+  const size_t smem = sizeof(ScanSmem<T>) + 128;
+  auto kern = k_scan2d<T, TMA>;
   FTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148, per_sm = 0;
   FTK_CUDA_TRY(cudaGetDevice(&dev));
@@ -1354,6 +1391,18 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
   kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  if (P.table) {
+    k_table_prep<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
+    FTK_CUDA_TRY(cudaGetLastError());
+  }
+  // K1b: persistent grid over the survivor list
+  const size_t xsmem = sizeof(ExSmem<T>);
+  auto xk = k_exact2d<T>;
+  FTK_CUDA_TRY(cudaFuncSetAttribute(xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
+  int xper = 0;
+  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, xk, EXW * 32, xsmem));
+  xk<<<(unsigned)(sms * std::max(xper, 1)), EXW * 32, xsmem, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }

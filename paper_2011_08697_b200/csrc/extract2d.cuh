@@ -20,6 +20,15 @@ struct ExtractParams {
   i64 capacity;
   unsigned long long* counters;  // Counter enum
   long long* edges;    // [capacity][2] trajectory-graph edges: (record, record or -1 - face_id)
+  long long* fid;      // [capacity] face id of every record (compact copy for pass 2)
+  // 2D: K1b also fills the pass-2 hash table (face id -> record) and the union-find parents
+  int* table;          // [table_cap] slots, cleared by K1's table preparation
+  unsigned long long table_cap;
+  int* parent;         // [capacity]
+  // 2D: K1a -> K1b survivor list (cubes passing the prefilter): anchors wx, wy and
+  // wt = t | (t+1 in the buffer) << 31 (-1: no cube); [wcap] each
+  int *wx, *wy, *wt;
+  i64 wcap;
   bool force_generic;  // testing: disable TMA
 };
 

@@ -384,6 +384,7 @@ __device__ void process_hypercube(const Tile<T>& A, const Tile<T>& B, bool hasB,
     if (slot < (unsigned long long)P.capacity) {
       ftk_cp* r = P.out + slot;
       r->face_id = (((t * G.nz + z) * G.ny + y) * G.nx + x) * 60 + ty;
+      P.fid[slot] = r->face_id;
       r->label = -1;
       r->x = dot4_nofma(mu, pv[0]);
       r->y = dot4_nofma(mu, pv[1]);

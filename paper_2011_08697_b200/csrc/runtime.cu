@@ -32,11 +32,17 @@ int set_cuda_error(cudaError_t e, const char* what) {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, total;
+  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, win, wx, wy, wt, total;
   u64 hcap;
+  i64 wcap;
 };
 
-static Layout layout(i64 capacity) {
+// survivor-list entries (2D K1a -> K1b): prefilter survivors run at about 0.45 per punctured face on
+// smooth fields; more survivors than capacity -> FTK_ERR_CAPACITY + retry
+static i64 window_cap(i64 capacity) { return std::max<i64>(1024, capacity); }
+
+static Layout layout(i64 capacity, int esz = 8) {
+  (void)esz;
   Layout L;
   u64 h = 1024;
   while (h < (u64)(capacity + capacity / 2)) h <<= 1;
@@ -45,7 +51,7 @@ static Layout layout(i64 capacity) {
   L.counters = off;
   off = align_up(off + CNT_N * sizeof(u64), 256);
   L.table = off;
-  off = align_up(off + h * sizeof(HashSlot), 256);
+  off = align_up(off + h * sizeof(int), 256);
   L.edges = off;
   off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
   L.fid = off;
@@ -60,9 +66,19 @@ static Layout layout(i64 capacity) {
   off = align_up(off + (size_t)capacity * 2 * sizeof(long long), 256);
   L.map = off;  // relabel map: [2 capacity] old labels, then [2 capacity] new labels
   off = align_up(off + (size_t)capacity * 4 * sizeof(long long), 256);
+  L.wcap = window_cap(capacity);
+  L.win = off;
+  L.wx = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.wy = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.wt = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
   L.total = off;
   return L;
 }
+
+static int esz_of(const ftk_desc* d) { return d->dtype == FTK_F32 ? 4 : 8; }
 
 static int validate(const ftk_desc* d) {
   if (!d) return FTK_ERR_INVALID_ARG;
@@ -123,7 +139,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   int st = validate(desc);
   if (st) return st;
   if (!d_field || !n_out || !d_ws || capacity < 0 || (capacity > 0 && !d_out)) return FTK_ERR_INVALID_ARG;
-  const Layout L = layout(capacity);
+  const Layout L = layout(capacity, esz_of(desc));
   if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
   char* ws = static_cast<char*>(d_ws);
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
@@ -149,6 +165,17 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.capacity = capacity;
   EP.counters = counters;
   EP.edges = reinterpret_cast<long long*>(ws + L.edges);
+  EP.fid = reinterpret_cast<long long*>(ws + L.fid);
+  // experiment: K1b inserts into the pass-2 table itself (its CAS latency lands on K1b's record
+  // path, slower than the separate insert kernel on C2)
+  const bool k1_insert = track && desc->ndim == 2 && getenv("FTK_K1B_INSERT") != nullptr;
+  EP.table = k1_insert ? reinterpret_cast<int*>(ws + L.table) : nullptr;
+  EP.table_cap = L.hcap;
+  EP.parent = reinterpret_cast<int*>(ws + L.parent);
+  EP.wx = reinterpret_cast<int*>(ws + L.wx);
+  EP.wy = reinterpret_cast<int*>(ws + L.wy);
+  EP.wt = reinterpret_cast<int*>(ws + L.wt);
+  EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
   ev.rec(1, stream);
   st = desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream);
@@ -159,10 +186,12 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     TP.rec = d_out;
     TP.capacity = capacity;
     TP.counters = counters;
-    TP.table = reinterpret_cast<HashSlot*>(ws + L.table);
+    TP.table = reinterpret_cast<int*>(ws + L.table);
     TP.table_cap = L.hcap;
     TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
     TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
+    TP.inserted = k1_insert;
+    TP.prelinked = desc->ndim == 2;
     TP.fid = reinterpret_cast<i64*>(ws + L.fid);
     TP.parent = reinterpret_cast<int*>(ws + L.parent);
     TP.T = desc->ndim == 2 ? 12 : 60;
@@ -186,10 +215,10 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
   if (getenv("FTK_PRINT_PROF")) {
-    const char* names[] = {"scan", "wait_full", "enqueue", "wait_ring", "exact_wait", "exact_faces",
+    const char* names[] = {"scan", "wait_full", "enqueue", "wait_ring", "exact_wait", "exact_load", "exact_faces",
                            "exact_records", "producer_wait", "other"};
     fprintf(stderr, "K1 cycle accounting (sum over warps, Gcycles):");
-    for (int i = 0; i < 9; ++i) fprintf(stderr, " %s=%.3f", names[i], host_cnt[CNT_PROF + i] * 1e-9);
+    for (int i = 0; i < 10; ++i) fprintf(stderr, " %s=%.3f", names[i], host_cnt[CNT_PROF + i] * 1e-9);
     fprintf(stderr, " edges=%llu\n", host_cnt[CNT_EDGES]);
   }
   if (ev.on) {
@@ -203,6 +232,10 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   g_stats[2] = (int64_t)host_cnt[CNT_NOUT];
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
+  if ((i64)host_cnt[CNT_WIN] > L.wcap) {  // survivors beyond the window buffer were not tested
+    *n_out = std::max<int64_t>(*n_out, (int64_t)host_cnt[CNT_WIN]);
+    return FTK_ERR_CAPACITY;
+  }
   if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity ||
       (i64)host_cnt[CNT_CROSS] > capacity || (i64)host_cnt[CNT_EXPORT_B] > capacity)
     return FTK_ERR_CAPACITY;
@@ -464,7 +497,7 @@ int ftk_workspace_size(const ftk_desc* d, int64_t capacity, size_t* bytes) {
   int st = validate(d);
   if (st) return st;
   if (!bytes || capacity < 0) return FTK_ERR_INVALID_ARG;
-  *bytes = layout(capacity).total;
+  *bytes = layout(capacity, esz_of(d)).total;
   return FTK_OK;
 }
 
@@ -500,7 +533,7 @@ int ftk_stitch_export(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t
                       int64_t capA, int64_t* nA, int64_t* h_B, int64_t capB, int64_t* nB, ftk_stream stream) {
   int st = validate(desc);
   if (st) return st;
-  if (!d_ws || !nA || !nB || ws_bytes < layout(capacity).total) return FTK_ERR_INVALID_ARG;
+  if (!d_ws || !nA || !nB || ws_bytes < layout(capacity, esz_of(desc)).total) return FTK_ERR_INVALID_ARG;
   std::vector<long long> A, B;
   st = read_exports(desc, d_ws, capacity, A, B, reinterpret_cast<cudaStream_t>(stream));
   if (st) return st;
@@ -526,7 +559,7 @@ int ftk_stitch_resolve(const int64_t* A, int64_t nA, const int64_t* B, int64_t n
 
 int ftk_relabel(ftk_cp* d_out, int64_t n, const int64_t* h_map_old, const int64_t* h_map_new, int64_t nmap,
                 void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
-  if (!d_ws || ws_bytes < layout(capacity).total || (nmap && (!h_map_old || !h_map_new))) return FTK_ERR_INVALID_ARG;
+  if (!d_ws || ws_bytes < layout(capacity).win || (nmap && (!h_map_old || !h_map_new))) return FTK_ERR_INVALID_ARG;
   return apply_map(d_out, n, d_ws, capacity, reinterpret_cast<const long long*>(h_map_old),
                    reinterpret_cast<const long long*>(h_map_new), nmap, reinterpret_cast<cudaStream_t>(stream));
 }

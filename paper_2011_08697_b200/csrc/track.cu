@@ -4,7 +4,8 @@
 // edges (record i, record j) or (record i, -1 - face id of a face owned by a neighbour cube).  Here:
 //
 //   K3  a GPU hash table face id -> record index, sized from the device-side record count
-//       (nextpow2(1.5 n) 16-byte slots, linear probing),
+//       (nextpow2(1.5 n) 4-byte slots holding record indices -- the key of a slot is fid[record],
+//       written by K1 -- linear probing; ~17 MB for 2.7 M records, resident in L2),
 //   K4  edge resolution + lock-free union-find (north_star (4)): the root with the larger face id is
 //       hooked under the smaller one with atomicCAS, path halving on finds,
 //   K6  labels: every record gets the face id of its root = the minimum face id of its trajectory,
@@ -22,65 +23,46 @@
 namespace ftk {
 namespace trk {
 
-constexpr long long EMPTY = -1;
+constexpr int EMPTY = -1;
 
 __constant__ KuhnTables<3> cK3 = kKuhn3;
 __constant__ KuhnTables<4> cK4 = kKuhn4;
 
-__device__ __forceinline__ u64 mix(u64 k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdull;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ull;
-  k ^= k >> 33;
-  return k;
-}
+__device__ __forceinline__ u64 mix(u64 k) { return hash_mix(k); }
 
 __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   const i64 n = (i64)P.counters[CNT_NOUT];
   return n < P.capacity ? n : P.capacity;
 }
 
-// slots used for n records: nextpow2(1.5 n), at least 1024, at most table_cap
-__device__ __forceinline__ u64 table_mask(const TrackParams& P) {
-  const i64 n = n_records(P);
-  u64 h = 1024;
-  while (h < (u64)(n + n / 2) && h < P.table_cap) h <<= 1;
-  return h - 1;
-}
+// the slot mask chosen by whoever cleared the table (k_clear here, or K1's table preparation)
+__device__ __forceinline__ u64 table_mask(const TrackParams& P) { return P.counters[CNT_HMASK]; }
 
 __global__ void k_clear(const __grid_constant__ TrackParams P) {
-  const u64 hm = table_mask(P);
+  const u64 hm = hash_slots(n_records(P), P.table_cap) - 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_HMASK] = hm;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
-    P.table[i].key = EMPTY;
+    P.table[i] = EMPTY;
 }
 
 __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
   const i64 n = n_records(P);
   const u64 hm = table_mask(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const long long key = P.rec[i].face_id;
-    P.fid[i] = key;
-    P.parent[i] = (int)i;
+    const long long key = P.fid[i];
+    if (!P.prelinked) P.parent[i] = (int)i;
     u64 h = mix((u64)key) & hm;
-    while (true) {
-      const long long prev =
-          (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&P.table[h].key), (u64)EMPTY, (u64)key);
-      if (prev == EMPTY || prev == key) {
-        P.table[h].val = i;
-        break;
-      }
-      h = (h + 1) & hm;
-    }
+    // face ids are unique among the records: claim the first empty slot of the probe sequence
+    while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) h = (h + 1) & hm;
   }
 }
 
 __device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long long key) {
   u64 h = mix((u64)key) & hm;
   while (true) {
-    const HashSlot s = P.table[h];
-    if (s.key == key) return s.val;
-    if (s.key == EMPTY) return -1;
+    const int r = P.table[h];
+    if (r == EMPTY) return -1;
+    if (P.fid[r] == key) return r;
     h = (h + 1) & hm;
   }
 }
@@ -347,10 +329,12 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int threads = 256, blocks = sms * 8;
-  k_clear<<<blocks, threads, 0, stream>>>(P);
-  FTK_CUDA_TRY(cudaGetLastError());
-  k_hash_insert<<<blocks, threads, 0, stream>>>(P);
-  FTK_CUDA_TRY(cudaGetLastError());
+  if (!P.inserted) {  // 3D: K1 does not fill the table
+    k_clear<<<blocks, threads, 0, stream>>>(P);
+    FTK_CUDA_TRY(cudaGetLastError());
+    k_hash_insert<<<blocks, threads, 0, stream>>>(P);
+    FTK_CUDA_TRY(cudaGetLastError());
+  }
   k_edges<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   k_label<<<blocks, threads, 0, stream>>>(P);

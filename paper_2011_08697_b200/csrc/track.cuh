@@ -5,22 +5,22 @@
 
 namespace ftk {
 
-struct HashSlot {
-  long long key;  // face id, -1 = empty
-  long long val;  // record index
-};
-
 struct TrackParams {
   ftk_cp* rec;                   // records from pass 1
   i64 capacity;
   unsigned long long* counters;  // CNT_NOUT holds the record count, CNT_EDGES the edge count
-  HashSlot* table;               // face id -> record index; [table_cap] slots
+  int* table;                    // face id -> record index: open addressing over record indices
+                                 // (-1 = empty), the key of slot r is fid[r]; [table_cap] slots
   u64 table_cap;                 // power of two >= 1.5 * capacity; the kernels use
                                  // nextpow2(1.5 * n) <= table_cap slots, n = records found
-  i64* fid;                      // [capacity] face ids (compact copy, union-find keys)
+  i64* fid;                      // [capacity] face ids of the records, written by K1 (hash keys,
+                                 // union-find keys, labels)
   int* parent;                   // [capacity] union-find parents
   const long long* edges;        // [capacity][2] edges from K1
   bool verify;                   // also re-derive every face's parent cells in closed form
+  bool inserted;                 // K1 already filled the table (experiment, FTK_K1B_INSERT)
+  bool prelinked;                // K1 initialised parent[] with its in-cube unions and emitted only
+                                 // the edges to faces of neighbour cubes (2D)
   // time slabs (multi-GPU stitch)
   int T;                         // face types per cube (12 / 60)
   i64 plane;                     // vertices per timestep (nx * ny * nz)

@@ -4,14 +4,11 @@ sys.path.insert(0, '.')
 from paper_2011_08697_b200 import build as b
 VARIANTS = {
     "base": [],
-    "static": ["FTK_K1_DYN=0"],
-    "new4": ["FTK_K1_NEW=4"],
-    "new2": ["FTK_K1_NEW=2"],
     "prof": ["FTK_K1_PROF=1"],
-    "nocopy": ["FTK_K1_PROF=1", "FTK_K1_DIAG_NOCOPY=1"],
-    "noexact": ["FTK_K1_PROF=1", "FTK_K1_DIAG_NOEXACT=1"],
-    "nocopy_noexact": ["FTK_K1_PROF=1", "FTK_K1_DIAG_NOCOPY=1", "FTK_K1_DIAG_NOEXACT=1"],
-    "prof_new4": ["FTK_K1_PROF=1", "FTK_K1_NEW=4"],
+    "rw8": ["FTK_K1_RW=8"],
+    "rw8s2": ["FTK_K1_RW=8", "FTK_K1_NSTAGE=2"],
+    "rw4s4": ["FTK_K1_NSTAGE=4"],
+    "rw4s6": ["FTK_K1_NSTAGE=6", "FTK_K1_MINB=1"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
