@@ -100,13 +100,14 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _ncu_traffic(config_name: str):
-    """dram bytes per K1 launch from the committed ncu --set full summary, if present"""
-    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+def _ncu_traffic(config_name: str, kernel: str = "k_scan2d"):
+    """dram read + write bytes per launch of `kernel` from the committed ncu --set full summary
+    (profiles/ncu_traffic.json: {config: {kernel: bytes}}), if present"""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(config_name)
+        return d.get(config_name, {}).get(kernel)
     except Exception:
         return None
 
@@ -223,13 +224,16 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    k1_ms, p2_ms, st_ms = [], [], []
+    k1_ms, p2_ms, st_ms, ka_ms, kb_ms = [], [], [], [], []
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index or 0) as clk:
         start.record(stream)
         for _ in range(args.steps):
             ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
             ms4, st3 = ftk.last_timings()
+            km = ftk.last_kernel_timings()
+            ka_ms.append(km[0])
+            kb_ms.append(km[1])
             k1_ms.append(ms4[0])
             p2_ms.append(ms4[1])
             st_ms.append(ms4[2])
@@ -257,13 +261,19 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = total_faces / (ms_step / 1000.0)
 
-    # roofline of the dominant kernel (K1): algorithmic bytes = field read once + records written
+    # roofline of the dominant kernel, the scan kernel K1a: algorithmic bytes = the
+    # field read once + the survivor list written (12 B per surviving cube); the exact kernel K1b is
+    # reported beside it (window reads of the survivors + records + edges)
     esz = field.element_size()
     k1_avg = sum(k1_ms) / len(k1_ms)
-    alg_bytes = field.numel() * esz + n_punct * ftk.RECORD_BYTES
-    achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
+    ka_avg = sum(ka_ms) / len(ka_ms)
+    kb_avg = sum(kb_ms) / len(kb_ms)
+    _, st3 = ftk.last_timings()
+    n_surv = st3[1]
+    alg_bytes = field.numel() * esz + 12 * n_surv
+    achieved = alg_bytes / (ka_avg / 1000.0) / 1e9
     peak, peak_src = _peaks()
-    traffic = _ncu_traffic(cfg.name)
+    traffic = _ncu_traffic(cfg.name, "k_scan2d")
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
     e2e = None
@@ -290,15 +300,18 @@ def run_ours(args):
                    "punctured_per_step": int(n_punct), "input": f"{field.dtype}".replace("torch.", ""),
                    "arith": "exact int64/int128 predicates, fixed-order f64 location/type, f32 prefilter",
                    "l2": "input (%.2f GB) larger than L2 (126 MB); no flush" % (field.numel() * esz / 1e9),
-                   "k1_ms": k1_avg, "pass2_ms": sum(p2_ms) / len(p2_ms),
+                   "k1_ms": k1_avg, "k1a_scan_ms": ka_avg, "k1b_exact_ms": kb_avg,
+                   "survivors_per_step": int(n_surv), "pass2_ms": sum(p2_ms) / len(p2_ms),
                    **({"stitch_ms": sum(st_ms) / len(st_ms)} if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_extract2d (K1)", "alg_bytes_per_launch": alg_bytes},
+                     "kernel": "k_scan2d (K1a, prefilter scan)", "alg_bytes_per_launch": alg_bytes,
+                     "k_exact2d": {"ms": kb_avg, "alg_bytes_per_launch": 128 * n_surv + n_punct * ftk.RECORD_BYTES,
+                                   "traffic": _ncu_traffic(cfg.name, "k_exact2d")}},
         "clocks": clk.summary(),
         "e2e": e2e,
-        # K1 + k_clear + k_hash_insert + k_edges + k_label; slabs add k_export and k_relabel
-        "gpu_launches": (5 + (2 if world > 1 else 0)) * args.steps,
+        # K1a + K1b + k_clear + k_hash_insert + k_edges + k_label; slabs add k_export and k_relabel
+        "gpu_launches": (6 + (2 if world > 1 else 0)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)

@@ -144,6 +144,10 @@ FTK_API int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d
  * sign prefilter, stats[2] = punctured faces. */
 FTK_API int ftk_set_profiling(int enable);
 FTK_API int ftk_last_timings(float* ms4, int64_t* stats3);
+/* Per-kernel device times (ms) of this thread's last profiled call: [0] scan kernel K1a (2D; the
+ * whole pass 1 in 3D), [1] exact kernel K1b (2D, else 0), [2] pass 2, [3] stitch.  Fills
+ * min(n, 4) entries; FTK_ERR_INVALID_ARG for a null pointer. */
+FTK_API int ftk_last_kernel_timings(float* ms, int n);
 
 /* Slab stitch, exposed step by step (ftk_cp_track with a communicator runs all of it internally).
  * After a track call on a time slab (FTK_GHOST_PLANE and/or t0 > 0) the workspace holds two lists of

@@ -36,6 +36,7 @@ assert RECORD_DTYPE.itemsize == RECORD_BYTES
 EXPORTS = [
     "ftk_abi_version", "ftk_strerror", "ftk_last_error", "ftk_num_faces", "ftk_workspace_size",
     "ftk_cp_extract", "ftk_cp_track", "ftk_cp_track_host", "ftk_set_profiling", "ftk_last_timings",
+    "ftk_last_kernel_timings",
     "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
     "ftk_relabel",
 ]
@@ -81,6 +82,7 @@ def lib() -> ctypes.CDLL:
         L.ftk_cp_track_host.argtypes = [PD, P, P, P, P, I64, P, P, ctypes.c_size_t, P]
         L.ftk_set_profiling.argtypes = [ctypes.c_int]
         L.ftk_last_timings.argtypes = [P, P]
+        L.ftk_last_kernel_timings.argtypes = [P, ctypes.c_int]
         L.ftk_comm_get_unique_id.argtypes = [P]
         L.ftk_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         L.ftk_comm_destroy.argtypes = [P]
@@ -223,6 +225,13 @@ def to_numpy(rec: torch.Tensor) -> np.ndarray:
 
 def set_profiling(enable: bool):
     lib().ftk_set_profiling(1 if enable else 0)
+
+
+def last_kernel_timings():
+    """[K1a scan, K1b exact, pass 2, stitch] device ms of the last profiled call (2D; 3D: K1 in [0])"""
+    ms = (ctypes.c_float * 4)()
+    _check(lib().ftk_last_kernel_timings(ms, 4), "ftk_last_kernel_timings")
+    return list(ms)
 
 
 def last_timings():

@@ -246,6 +246,9 @@ template <typename T>
 constexpr int ws_words() { return sizeof(T) == 4 ? 49 : 66; }  // odd stride for fp32: no bank conflicts
 constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
 constexpr int EXW = 8;              // warps per K1b block
+#ifndef FTK_X_MINB
+#define FTK_X_MINB 3
+#endif
 
 struct BatchBuf {                   // one warp's batch in shared memory
   uint32_t* ring;                   // [32][ws_words]
@@ -740,7 +743,7 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
     }
     return ty;
   };
-#pragma unroll
+#pragma unroll 1
   for (int C = 0; C < 6; ++C) {
     const uint32_t bits = epair[C];
     if (bits && !(bits & 8u)) {
@@ -1254,7 +1257,7 @@ __global__ void k_table_prep(const __grid_constant__ ExtractParams P) {
 // count is read from the device counter K1a left behind)
 // ---------------------------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(EXW * 32, 3) k_exact2d(const __grid_constant__ ExtractParams P) {
+__global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_constant__ ExtractParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ExSmem<T>& sm = *reinterpret_cast<ExSmem<T>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1392,6 +1395,7 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
   kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, P);
   FTK_CUDA_TRY(cudaGetLastError());
+  if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
   if (P.table) {
     k_table_prep<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
     FTK_CUDA_TRY(cudaGetLastError());

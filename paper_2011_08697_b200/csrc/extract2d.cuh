@@ -30,6 +30,7 @@ struct ExtractParams {
   int *wx, *wy, *wt;
   i64 wcap;
   bool force_generic;  // testing: disable TMA
+  void* ev_mid;        // profiling: cudaEvent_t recorded between K1a and K1b (2D), or null
 };
 
 int launch_extract2d(const ExtractParams& P, cudaStream_t stream);

@@ -116,8 +116,10 @@ static int range_status(const ftk_desc* d, unsigned long long maxbits) {
   return q < bound ? FTK_OK : FTK_ERR_RANGE;
 }
 
+static thread_local float g_kms[4] = {0, 0, 0, 0};  // K1a, K1b, pass 2, stitch
+
 struct Events {
-  cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t e[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // 4: between K1a and K1b
   bool on = false;
   Events() {
     if (g_profiling) {
@@ -177,6 +179,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.wt = reinterpret_cast<int*>(ws + L.wt);
   EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
+  EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
   ev.rec(1, stream);
   st = desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream);
   if (st) return st;
@@ -226,6 +229,15 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     cudaEventElapsedTime(&g_ms[1], ev.e[2], ev.e[3]);
     g_ms[2] = 0.f;
     cudaEventElapsedTime(&g_ms[3], ev.e[0], ev.e[3]);
+    if (desc->ndim == 2 && cudaEventQuery(ev.e[4]) == cudaSuccess) {
+      cudaEventElapsedTime(&g_kms[0], ev.e[1], ev.e[4]);
+      cudaEventElapsedTime(&g_kms[1], ev.e[4], ev.e[2]);
+    } else {
+      g_kms[0] = g_ms[0];
+      g_kms[1] = 0.f;
+    }
+    g_kms[2] = g_ms[1];
+    g_kms[3] = 0.f;
   }
   ftk_num_faces(desc, &g_stats[0]);
   g_stats[1] = (int64_t)host_cnt[CNT_SURVIVORS];
@@ -523,6 +535,7 @@ int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&g_ms[2], e0, e1);
     g_ms[3] += g_ms[2];
+    g_kms[3] = g_ms[2];
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
@@ -582,6 +595,12 @@ int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, 
 
 int ftk_set_profiling(int enable) {
   g_profiling = enable;
+  return FTK_OK;
+}
+
+int ftk_last_kernel_timings(float* ms, int n) {
+  if (!ms || n < 0) return FTK_ERR_INVALID_ARG;
+  for (int i = 0; i < n && i < 4; ++i) ms[i] = g_kms[i];
   return FTK_OK;
 }
 
