@@ -44,7 +44,7 @@ typedef enum {
   FTK_ERR_INVALID_ARG = 1, /* bad descriptor / null pointer / workspace too small */
   FTK_ERR_RANGE = 2,       /* some |q| = |rint(f * 2^s)| >= 2^59 (2D) or 2^38 (3D), or a non-
                               finite input: the exact integer predicates could overflow */
-  FTK_ERR_CAPACITY = 3,    /* more records than `capacity` (or, 2D, more prefilter-surviving cubes
+  FTK_ERR_CAPACITY = 3,    /* more records than `capacity` (or more prefilter-surviving cubes
                               than the workspace's survivor list of max(1024, capacity) entries):
                               *n_out = the capacity to retry with, contents unspecified; the call
                               is idempotent, retry with larger buffers */

@@ -25,9 +25,10 @@ struct ExtractParams {
   int* table;          // [table_cap] slots, cleared by K1's table preparation
   unsigned long long table_cap;
   int* parent;         // [capacity]
-  // 2D: K1a -> K1b survivor list (cubes passing the prefilter): anchors wx, wy and
+  // K1a -> K1b survivor list (cubes passing the prefilter): anchors wx, wy, [wz] and
   // wt = t | (t+1 in the buffer) << 31 (-1: no cube); [wcap] each
   int *wx, *wy, *wt;
+  int* wz;             // 3D: anchor z
   i64 wcap;
   bool force_generic;  // testing: disable TMA
   void* ev_mid;        // profiling: cudaEvent_t recorded between K1a and K1b (2D), or null

@@ -32,6 +32,7 @@ constexpr int SX = TX + 3, SY = TY + 3, SZ = TZ + 3;  // tile with halo: x-1 .. 
 constexpr int SV = SX * SY * SZ;
 constexpr int CX = TX + 1, CY = TY + 1, CZ = TZ + 1;  // vertex codes: x .. x+TX
 constexpr int TCH = 16;                         // anchor timesteps per work item
+constexpr int CHUNK3 = 32;                      // survivor-list entries a warp reserves at a time
 
 __constant__ KuhnTables<4> cK4 = kKuhn4;
 
@@ -127,14 +128,20 @@ struct Tile {  // staged plane tile, value at global (x, y, z)
 };
 
 template <typename T>
+struct GTile {  // a plane of the field in global memory, value at global (x, y, z) (in the grid)
+  const T* S;
+  __device__ __forceinline__ T at(const Geo3& G, i64 x, i64 y, i64 z) const { return __ldg(S + (z * G.ny + y) * G.nx + x); }
+};
+
+template <typename T>
 __device__ __forceinline__ i64 quant3(T f, const Geo3& G) {
   if constexpr (sizeof(T) == 4) return __float2ll_rn(__fmul_rn(f, G.scale_f));
   else return __double2ll_rn(__dmul_rn(f, G.scale));
 }
 
 // exact gradient (2x derivative, one-sided doubled at the boundary) at vertex (x, y, z) of a tile
-template <typename T>
-__device__ void grad3(const Tile<T>& P, const Geo3& G, i64 x, i64 y, i64 z, i64* g) {
+template <typename T, typename Acc>
+__device__ void grad3(const Acc& P, const Geo3& G, i64 x, i64 y, i64 z, i64* g) {
   const i64 N[3] = {G.nx, G.ny, G.nz};
   const i64 c[3] = {x, y, z};
 #pragma unroll
@@ -255,8 +262,8 @@ constexpr Cells4 make_cells4() {
 __constant__ Cells4 cCells4 = make_cells4();
 
 // ------------------------------------------------------------------------------ exact stage
-template <typename T>
-__device__ void process_hypercube(const Tile<T>& A, const Tile<T>& B, bool hasB, const Geo3& G,
+template <typename T, typename Acc>
+__device__ void process_hypercube(const Acc& A, const Acc& B, bool hasB, const Geo3& G,
                                   const ExtractParams& P, i64 x, i64 y, i64 z, i64 t) {
   i64 g[16][3];
   uint32_t exists = 0;
@@ -265,7 +272,7 @@ __device__ void process_hypercube(const Tile<T>& A, const Tile<T>& B, bool hasB,
     const i64 cx = x + (c & 1), cy = y + ((c >> 1) & 1), cz = z + ((c >> 2) & 1);
     const bool ex = cx < G.nx && cy < G.ny && cz < G.nz && ((c & 8) == 0 || hasB);
     if (ex) {
-      grad3((c & 8) ? B : A, G, cx, cy, cz, g[c]);
+      grad3<T>((c & 8) ? B : A, G, cx, cy, cz, g[c]);
       exists |= 1u << c;
     } else {
       g[c][0] = g[c][1] = g[c][2] = 0;
@@ -432,6 +439,37 @@ __global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ Ext
   uint32_t my_max32 = 0;
   double my_maxd = 0.0;
   const int lx = tid % TX, ly = (tid / TX) % TY, lz = tid / (TX * TY);
+  const int lane = tid & 31;
+  // survivor list (K1b input): per-warp chunks of CHUNK3 entries, one global atomic per chunk
+  long long cur = 0, end = 0;
+  auto enqueue = [&](bool surv, i64 x, i64 y, i64 z, int tflag) {
+    const uint32_t ball = __ballot_sync(0xffffffffu, surv);
+    if (!ball) return;
+    const int n = __popc(ball);
+    int rank = __popc(ball & ((1u << lane) - 1u));
+    int done = 0;
+    while (done < n) {
+      if (cur == end) {
+        long long c = 0;
+        if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK3);
+        cur = __shfl_sync(0xffffffffu, c, 0);
+        end = cur + CHUNK3;
+      }
+      const int k = (int)min((long long)(n - done), end - cur);
+      if (surv && rank >= done && rank < done + k) {
+        const long long e = cur + (rank - done);
+        if (e < P.wcap) {
+          P.wx[e] = (int)x;
+          P.wy[e] = (int)y;
+          P.wz[e] = (int)z;
+          P.wt[e] = tflag;
+        }
+      }
+      cur += k;
+      done += k;
+    }
+    my_surv += surv ? 1 : 0;
+  };
 
   for (i64 item = blockIdx.x; item < nitems; item += gridDim.x) {
     i64 r = item;
@@ -445,7 +483,7 @@ __global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ Ext
     G.y0 = ty * TY;
     G.z0 = tz * TZ;
     const i64 ax = G.x0 + lx, ay = G.y0 + ly, az = G.z0 + lz;
-    uint32_t prev = 0;
+    uint32_t prev = 0x3Fu;
     for (i64 p = ta; p <= plast; ++p) {
       const int cur = (int)((p - ta) & 1);
       T* S = tile[cur];
@@ -476,8 +514,9 @@ __global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ Ext
       for (int i = tid; i < CX * CY * CZ; i += NT) {
         const int xx = i % CX, yy = (i / CX) % CY, zz = i / (CX * CY);
         const i64 vx = G.x0 + xx, vy = G.y0 + yy, vz = G.z0 + zz;
-        uint32_t cval = 0;
+        uint32_t cval = 0x3Fu;
         if (vx < G.nx && vy < G.ny && vz < G.nz) {
+          cval = 0;
           const i64 c[3] = {vx, vy, vz};
           const i64 N[3] = {G.nx, G.ny, G.nz};
 #pragma unroll
@@ -486,34 +525,29 @@ __global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ Ext
             if (c[a] > 0) lo[a] -= 1;
             if (c[a] < N[a] - 1) hi[a] += 1;
             const T d = Pt.at(G, hi[0], hi[1], hi[2]) - Pt.at(G, lo[0], lo[1], lo[2]);
-            cval |= (sbit<T>(d - thr) << (2 * a)) | (sbit<T>(-thr - d) << (2 * a + 1));
+            cval |= (sbit<T>(thr - d) << (2 * a)) | (sbit<T>(d + thr) << (2 * a + 1));
           }
         }
         code[i] = (uint8_t)cval;
       }
       __syncthreads();
-      uint32_t cube = 0;
+      uint32_t cube = 0x3Fu;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        cube |= code[((lz + ((c >> 2) & 1)) * CY + ly + ((c >> 1) & 1)) * CX + lx + (c & 1)];
+        cube &= code[((lz + ((c >> 2) & 1)) * CY + ly + ((c >> 1) & 1)) * CX + lx + (c & 1)];
       const bool inside = ax < G.nx && ay < G.ny && az < G.nz;
-      if (p > ta) {
-        // anchors at p - 1: hypercube over planes p - 1 and p
-        if (inside && ((prev | cube) & 0x3Fu) == 0x3Fu) {
-          ++my_surv;
-          process_hypercube<T>(Tile<T>{tile[cur ^ 1]}, Tile<T>{S}, true, G, P, ax, ay, az, p - 1);
-        }
-      }
-      if (p == G.ntg - 1 && p < tb) {
-        // anchors on the last timestep: no t+1 corners
-        if (inside && (cube & 0x3Fu) == 0x3Fu) {
-          ++my_surv;
-          process_hypercube<T>(Tile<T>{S}, Tile<T>{S}, false, G, P, ax, ay, az, p);
-        }
-      }
+      // anchors at p - 1 (hypercube over planes p - 1 and p), then anchors on the last timestep (no
+      // t+1 corners)
+      const bool s0 = p > ta && inside && ((prev & cube) & 0x3Fu) == 0;
+      const bool s1 = p == G.ntg - 1 && p < tb && inside && (cube & 0x3Fu) == 0;
+      enqueue(s0, ax, ay, az, (int)((uint32_t)(p - 1) | 0x80000000u));
+      enqueue(s1, ax, ay, az, (int)p);
       prev = cube;
     }
   }
+  // the unused rest of the warp's chunk holds no cube
+  for (long long e = cur + lane; e < end; e += 32)
+    if (e < P.wcap) P.wt[e] = -1;
   atomicAdd(&s_surv, my_surv);
   atomicMax(&s_max32, my_max32);
   atomicMax(&s_max64, (unsigned long long)__double_as_longlong(my_maxd));
@@ -521,6 +555,33 @@ __global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ Ext
   if (tid == 0) {
     atomicAdd(&P.counters[CNT_SURVIVORS], s_surv);
     atomicMax(&P.counters[CNT_MAXBITS], sizeof(T) == 4 ? (unsigned long long)s_max32 : s_max64);
+  }
+}
+
+// K1b (3D): one thread per surviving hypercube of the list; gradients and Hessians straight from the
+// field (L2/HBM).
+template <typename T>
+__global__ void __launch_bounds__(128) k_exact3d(const __grid_constant__ ExtractParams P) {
+  Geo3 G;
+  G.nx = P.nx;
+  G.ny = P.ny;
+  G.nz = P.nz;
+  G.ntg = P.nt_global;
+  G.scale = P.scale;
+  G.scale_f = (float)P.scale;
+  G.x0 = G.y0 = G.z0 = 0;
+  const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
+  const T* field = reinterpret_cast<const T*>(P.field);
+  const i64 plane = G.nx * G.ny * G.nz;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nwin;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int et = P.wt[e];
+    if (et == -1) continue;
+    const bool hasB = et < 0;
+    const i64 t = et & 0x3fffffff;
+    const GTile<T> A{field + (t - P.t0) * plane};
+    const GTile<T> B{hasB ? A.S + plane : A.S};
+    process_hypercube<T>(A, B, hasB, G, P, P.wx[e], P.wy[e], P.wz[e], t);
   }
 }
 
@@ -538,6 +599,11 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1) * 4);
   k_extract3d<T><<<(unsigned)grid, NT, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
+  int xper = 0;
+  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, k_exact3d<T>, 128, 0));
+  k_exact3d<T><<<(unsigned)(sms * std::max(xper, 1)), 128, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }

@@ -32,7 +32,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, win, wx, wy, wt, total;
+  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, win, wx, wy, wt, wz, total;
   u64 hcap;
   i64 wcap;
 };
@@ -73,6 +73,8 @@ static Layout layout(i64 capacity, int esz = 8) {
   L.wy = off;
   off = align_up(off + (size_t)L.wcap * 4, 256);
   L.wt = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.wz = off;
   off = align_up(off + (size_t)L.wcap * 4, 256);
   L.total = off;
   return L;
@@ -177,6 +179,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.wx = reinterpret_cast<int*>(ws + L.wx);
   EP.wy = reinterpret_cast<int*>(ws + L.wy);
   EP.wt = reinterpret_cast<int*>(ws + L.wt);
+  EP.wz = reinterpret_cast<int*>(ws + L.wz);
   EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
@@ -229,7 +232,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     cudaEventElapsedTime(&g_ms[1], ev.e[2], ev.e[3]);
     g_ms[2] = 0.f;
     cudaEventElapsedTime(&g_ms[3], ev.e[0], ev.e[3]);
-    if (desc->ndim == 2 && cudaEventQuery(ev.e[4]) == cudaSuccess) {
+    if (cudaEventQuery(ev.e[4]) == cudaSuccess) {
       cudaEventElapsedTime(&g_kms[0], ev.e[1], ev.e[4]);
       cudaEventElapsedTime(&g_kms[1], ev.e[4], ev.e[2]);
     } else {
