@@ -66,6 +66,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count = 1) {
 #ifndef FTK_K1_MBSLEEP
 #define FTK_K1_MBSLEEP 32     // scan warps waiting for a plane
 #endif
+#ifndef FTK_K1_SCANSLEEP
+#define FTK_K1_SCANSLEEP 0    // scan warps wait for a plane with the suspend-time hint too
+#endif
 #ifndef FTK_K1_PRODSLEEP
 #define FTK_K1_PRODSLEEP 256  // the producer waiting for a free stage
 #endif
@@ -1159,7 +1162,8 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
     while (true) {
       const int s = gk % NSTAGE;
       pf.lap(PF_OTHER);
-      mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
+      if (FTK_K1_SCANSLEEP) mbar_wait_sleep(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk);
+      else mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
       pf.lap(PF_WFULL);
       const StageMeta m = sm.meta[s];
       if (m.done) break;

@@ -82,6 +82,22 @@ static Layout layout(i64 capacity, int esz = 8) {
 
 static int esz_of(const ftk_desc* d) { return d->dtype == FTK_F32 ? 4 : 8; }
 
+// Face types an edge can look up: the upper face of a cell, seen from the neighbour cube that owns
+// it, is the chain (0, p2, p2|p3[, p2|p3|p4]) -- its last mask misses exactly one axis.  The other
+// types are only ever reached through in-cube pairs.
+template <int D>
+static constexpr unsigned long long upper_types(const KuhnTables<D>& K) {
+  unsigned long long m = 0;
+  for (int t = 0; t < KuhnTables<D>::NT; ++t) {
+    int pc = 0;
+    for (int b = 0; b < D; ++b) pc += (K.masks[t][D - 2] >> b) & 1;
+    if (pc == D - 1) m |= 1ull << t;
+  }
+  return m;
+}
+static_assert(__builtin_popcountll(upper_types<3>(kKuhn3)) == 6, "6 upper face types in 2D+t");
+static_assert(__builtin_popcountll(upper_types<4>(kKuhn4)) == 24, "24 upper face types in 3D+t");
+
 static int validate(const ftk_desc* d) {
   if (!d) return FTK_ERR_INVALID_ARG;
   if (d->ndim != 2 && d->ndim != 3) return FTK_ERR_INVALID_ARG;
@@ -198,6 +214,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
     TP.inserted = k1_insert;
     TP.prelinked = desc->ndim == 2;
+    TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
     TP.fid = reinterpret_cast<i64*>(ws + L.fid);
     TP.parent = reinterpret_cast<int*>(ws + L.parent);
     TP.T = desc->ndim == 2 ? 12 : 60;

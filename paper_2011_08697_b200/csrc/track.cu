@@ -51,6 +51,8 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const long long key = P.fid[i];
     if (!P.prelinked) P.parent[i] = (int)i;
+    // only faces that some cell of a neighbour cube looks up (the "upper" types) need a slot
+    if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
     u64 h = mix((u64)key) & hm;
     // face ids are unique among the records: claim the first empty slot of the probe sequence
     while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) h = (h + 1) & hm;

@@ -19,6 +19,8 @@ struct TrackParams {
   const long long* edges;        // [capacity][2] edges from K1
   bool verify;                   // also re-derive every face's parent cells in closed form
   bool inserted;                 // K1 already filled the table (experiment, FTK_K1B_INSERT)
+  unsigned long long lookup_types;  // face types (bit per type) inserted into the table: the types
+                                 // an edge or the verifier can look up
   bool prelinked;                // K1 initialised parent[] with its in-cube unions and emitted only
                                  // the edges to faces of neighbour cubes (2D)
   // time slabs (multi-GPU stitch)

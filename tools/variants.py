@@ -5,8 +5,9 @@ from paper_2011_08697_b200 import build as b
 VARIANTS = {
     "base": [],
     "prof": ["FTK_K1_PROF=1"],
-    "x4": ["FTK_X_MINB=4"],
-    "x2": ["FTK_X_MINB=2"],
+    "ssleep": ["FTK_K1_SCANSLEEP=1"],
+    "mb128": ["FTK_K1_MBSLEEP=128"],
+    "rw4": ["FTK_K1_RW=4"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
