@@ -214,6 +214,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
     TP.inserted = k1_insert;
     TP.prelinked = desc->ndim == 2;
+    TP.diag = getenv("FTK_PASS2_DIAG") ? atoi(getenv("FTK_PASS2_DIAG")) : 0;
     TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
     TP.fid = reinterpret_cast<i64*>(ws + L.fid);
     TP.parent = reinterpret_cast<int*>(ws + L.parent);

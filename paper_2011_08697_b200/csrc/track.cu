@@ -100,7 +100,13 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   const i64 ne0 = (i64)P.counters[CNT_EDGES];
   const i64 ne = ne0 < P.capacity ? ne0 : P.capacity;
   const u64 hm = table_mask(P);
-  for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (i64)gridDim.x * blockDim.x) {
+  const i64 nthreads = (i64)gridDim.x * blockDim.x;
+  const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (i64 j = tid; j < ne; j += nthreads) {
+    // consecutive edges come from one K1b batch and mostly join the same few trajectories; spread
+    // them over the threads (and time) so concurrent finds do not pile onto the same trees.
+    // j -> j p mod ne is a bijection for the prime p = 2654435761 > capacity (gcd(p, ne) = 1).
+    const i64 e = (P.diag == 2 || ne >= 2654435761ll) ? j : (i64)(((unsigned long long)j * 2654435761ull) % (unsigned long long)ne);
     const long long a = P.edges[2 * e];
     long long b = P.edges[2 * e + 1];
     if (b < 0) {
@@ -120,6 +126,7 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
       atomicAdd(&P.counters[CNT_INVARIANT], 1ull);  // a cell's partner face was never emitted
       continue;
     }
+    if (P.diag == 1) continue;  // diagnostics: lookups only
     uf_unite(P.parent, P.fid, (int)a, (int)b);
   }
 }
