@@ -40,148 +40,12 @@
 #include "common.cuh"
 #include "extract2d.cuh"
 #include "kuhn.cuh"
+#include "sm100.cuh"
 
 namespace ftk {
 namespace k2d {
 
-// ---------------------------------------------------------------------------------------------
-// PTX helpers: mbarrier + TMA + packed fp32
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count = 1) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-#ifndef FTK_K1_HINT
-#define FTK_K1_HINT 0
-#endif
-#ifndef FTK_K1_MBSLEEP
-#define FTK_K1_MBSLEEP 32     // scan warps waiting for a plane
-#endif
-#ifndef FTK_K1_SCANSLEEP
-#define FTK_K1_SCANSLEEP 0    // scan warps wait for a plane with the suspend-time hint too
-#endif
-#ifndef FTK_K1_PRODSLEEP
-#define FTK_K1_PRODSLEEP 256  // the producer waiting for a free stage
-#endif
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  if (FTK_K1_HINT) {  // suspend-time hint (ns)
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)FTK_K1_HINT)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-  return done != 0;
-}
-__device__ __forceinline__ unsigned long long gtimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// never hang the GPU: a wait that exceeds 2 s reports where it is stuck and traps
-__device__ __noinline__ void wait_timeout(int what, int a, int b) {
-  if ((threadIdx.x & 31) == 0)
-    printf("ftk k_extract2d: wait timeout what=%d a=%d b=%d block=%d warp=%d\n", what, a, b, blockIdx.x,
-           threadIdx.x >> 5);
-  __trap();
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int what, int a, int sleep_ns) {
-  if (mbar_try(bar, parity)) return;
-  // back off: a spinning warp takes issue slots from the scan warps on its SMSP
-  const unsigned long long t0 = gtimer_ns();
-  int spins = 0;
-  while (!mbar_try(bar, parity)) {
-    __nanosleep(sleep_ns);
-    if ((++spins & 15) == 0) {
-      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
-    }
-  }
-}
-// the producer's wait for a free stage: try_wait with a suspend-time hint, so the warp sleeps in
-// hardware until the phase completes (no issue slots spent) -- bounded by the same 2 s trap
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, int what, int a) {
-  const unsigned long long t0 = gtimer_ns();
-  int spins = 0;
-  while (true) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-        : "memory");
-    if (done) return;
-    if ((++spins & 15) == 0) {
-      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
-    }
-  }
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-// optional cycle accounting (build with -DFTK_K1_PROF=1): per role, cycles spent per activity
-#ifndef FTK_K1_PROF
-#define FTK_K1_PROF 0
-#endif
-enum ProfSlot { PF_SCAN = 0, PF_WFULL, PF_ENQ, PF_WRING, PF_EXWAIT, PF_EXLOAD, PF_EXFACE, PF_EXREC, PF_PRODWAIT, PF_OTHER, PF_N };
-struct Prof {
-  unsigned long long acc[PF_N];
-  unsigned long long t;
-  __device__ void start() {
-    if (FTK_K1_PROF) t = clock64();
-  }
-  __device__ void lap(int slot) {
-    if (FTK_K1_PROF) {
-      const unsigned long long n = clock64();
-      acc[slot] += n - t;
-      t = n;
-    }
-  }
-};
-
-struct f2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ f2 pack2(float a, float b) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  f2 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-  return r;
-}
-__device__ __forceinline__ uint32_t lo32(f2 a) { return (uint32_t)a.v; }
-__device__ __forceinline__ uint32_t hi32(f2 a) { return (uint32_t)(a.v >> 32); }
-// push the sign bit of `bits` into the low end of W
-__device__ __forceinline__ uint32_t push_sign(uint32_t W, uint32_t bits) { return __funnelshift_l(bits, W, 1); }
+using namespace sm100;
 
 // ---------------------------------------------------------------------------------------------
 // Geometry and roles
@@ -886,14 +750,6 @@ __device__ __forceinline__ uint32_t code_f32(const float4 u, const float4 v, con
   return gather_code(c);
 }
 
-__device__ __forceinline__ uint32_t max_abs_bits(uint32_t m, float a, float b, float c, float d) {
-  float r = __uint_as_float(m), t1, t2;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t1) : "f"(fabsf(a)), "f"(fabsf(b)));
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t2) : "f"(fabsf(c)), "f"(fabsf(d)));
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(t1) : "f"(t1), "f"(t2));
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(r), "f"(t1));
-  return __float_as_uint(r);
-}
 
 // Scan one plane (fp32): all RW+3 rows are loaded first (independent shared loads and shuffles),
 // then the RW+1 code rows, then the squares Sq[r] (OR over the 4 corners of each square, per
@@ -929,7 +785,7 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
 #pragma unroll
   for (int k = 0; k <= RW; ++k) {
     load(k + 2, v2, l2, r2);
-    if (k >= 1 && k <= RW) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);  // owned rows 1..RW
+    if (k < RW) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);  // centre rows k = 0..RW-1 are owned
     uint32_t C;
     if (EDGE) {
       const long long gy = c.gy0 + k;
@@ -1352,23 +1208,7 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
 // ---------------------------------------------------------------------------------------------
 // Host launcher
 // ---------------------------------------------------------------------------------------------
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
+using sm100::get_encode;
 
 template <typename T, bool TMA>
 static int launch_t(const ExtractParams& P, cudaStream_t stream) {

@@ -1,20 +1,20 @@
 // extract3d.cu -- K1 for 3D+t (4D spacetime, faces = tetrahedra, cells = pentachora).
 //
 // Pass 1 of Alg. 1 (generalised at P:439) plus the per-hypercube cell evaluation of
-// pass 2.  A CTA owns a 32 x 4 x 2 block of anchors (x, y, z) and marches t over a chunk; each plane
-// tile with its halo (x-1..x+33, y-1..y+5, z-1..z+3) is staged in shared memory (double buffered), so
-// every vertex is read from HBM once per CTA and its neighbours come from shared memory.
+// pass 2, split like the 2D path:
 //
-//   prefilter: per vertex a 6-bit code, bit = 1 when a strict sign condition does NOT hold:
-//     (dx >= thr), (dx <= -thr), (dy >= thr), (dy <= -thr), (dz >= thr), (dz <= -thr) on raw values,
-//     thr = 2^(1-s), which implies the exact integer gradient component is strictly positive/negative
-//     (DESIGN.md "prefilter").  ORed over the 16 corners of the spacetime hypercube; a code with all
-//     six bits set survives (no gradient component is one-signed on every corner).
-//   exact stage (survivors, one per thread): int64 gradients, the 60 face types with exact 3x3
-//     determinants (int128) and the SoS epsilon-expansion of det(M + E) evaluated term by term in
-//     decreasing magnitude (R4/R5), Eq. 2 location and the Descartes-rule
-//     Hessian type in fixed-order FP64, and the 24 cells (pentachora) of the hypercube: 0 or 2
-//     punctured sides each, emitted as trajectory edges.
+//   K1a k_scan3d (namespace s3): TMA 4D halo boxes of 124 x 8 x 8 anchor tiles per timestep, one warp
+//     per z-slice; per vertex a 6-bit "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) on raw
+//     values, thr = 2^(1-s), which implies the exact integer gradient component is strictly
+//     positive/negative; ANDed over the 16 corners of the spacetime hypercube
+//     (y/x pairs in registers, z pairs through shared memory, t pairs across planes); a zero code is a
+//     survivor and its anchor goes to the survivor list.
+//   K1b k_exact3d: one surviving hypercube per thread, straight from the field: int64 gradients, the
+//     60 face types with exact 3x3 determinants (int128) and the SoS epsilon-expansion of det(M + E)
+//     evaluated term by term in decreasing magnitude (R4/R5), Eq. 2
+//     location and the Descartes-rule Hessian type in fixed-order FP64, and the 24 cells
+//     (pentachora) of the hypercube: 0 or 2 punctured sides each, emitted as
+//     trajectory edges.
 #include <cstdio>
 #include <cstring>
 #include <utility>
@@ -22,15 +22,12 @@
 #include "common.cuh"
 #include "extract2d.cuh"
 #include "kuhn.cuh"
+#include "sm100.cuh"
 
 namespace ftk {
 namespace k3d {
+using namespace sm100;
 
-constexpr int TX = 32, TY = 4, TZ = 2;          // anchors per CTA
-constexpr int NT = TX * TY * TZ;                // threads (one anchor each)
-constexpr int SX = TX + 3, SY = TY + 3, SZ = TZ + 3;  // tile with halo: x-1 .. x+TX+1
-constexpr int SV = SX * SY * SZ;
-constexpr int CX = TX + 1, CY = TY + 1, CZ = TZ + 1;  // vertex codes: x .. x+TX
 constexpr int TCH = 16;                         // anchor timesteps per work item
 constexpr int CHUNK3 = 32;                      // survivor-list entries a warp reserves at a time
 
@@ -119,13 +116,6 @@ struct Geo3 {
   double scale;
 };
 
-template <typename T>
-struct Tile {  // staged plane tile, value at global (x, y, z)
-  const T* S;
-  __device__ __forceinline__ T at(const Geo3& G, i64 x, i64 y, i64 z) const {
-    return S[((int)(z - G.z0 + 1) * SY + (int)(y - G.y0 + 1)) * SX + (int)(x - G.x0 + 1)];
-  }
-};
 
 template <typename T>
 struct GTile {  // a plane of the field in global memory, value at global (x, y, z) (in the grid)
@@ -403,160 +393,413 @@ __device__ void process_hypercube(const Acc& A, const Acc& B, bool hasB, const G
   }
 }
 
-// ------------------------------------------------------------------------------ the kernel
+// ------------------------------------------------------------------------------ K1a (3D): the scan
+// Persistent, one CTA per SM.  A work item is a 124 x 8 x 8 tile of anchors (x, y, z) times a chunk
+// of TCH anchor timesteps.  Per timestep the producer warp stages the 136 x 11 x 11 halo box
+// (x0-4.., y0-1.., z0-1..) with one 4D TMA load into an NSTAGE3-deep ring.  Scan warp w < 8 owns
+// z-slice z0 + w (8 rows, rolled through a 3-row register window as in 2D, plus the slices z +- 1 of
+// the centre row for dz); warp 8 computes the squares of slice z0 + 8 only.  Per vertex a 6-bit
+// "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) in the top of a byte; ANDed over the
+// y-pair and x-pair in registers, over the z-pair through a double-buffered shared exchange (one
+// named barrier per plane), over the t-pair with the previous plane's cube codes in registers; a
+// zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte are zero).
+namespace s3 {
+constexpr int LX = 128, TX = 124, RW = 8, XOFF = 4, PITCH = LX + 8;
+constexpr int ROWS = RW + 3;  // y0-1 .. y0+RW+1
 template <typename T>
-__device__ __forceinline__ uint32_t sbit(T v) {
-  if constexpr (sizeof(T) == 4) return __float_as_uint(v) >> 31;
-  else return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63);
+constexpr int nzw() { return sizeof(T) == 4 ? 8 : 4; }  // z-slice warps (owned slices per tile)
+template <typename T>
+constexpr int slices() { return nzw<T>() + 3; }         // z0-1 .. z0+NZW+1
+template <typename T>
+constexpr int nstage() { return sizeof(T) == 4 ? 3 : 2; }
+template <typename T>
+constexpr int nthreads() { return (nzw<T>() + 2) * 32; }  // NZW slice warps + top warp + producer
+template <typename T>
+constexpr int stage_elems() { return (PITCH * ROWS * slices<T>() * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T); }
+constexpr uint32_t NEUTRAL = 0xFCFCFCFCu;
+constexpr int CHUNK = 32;
+
+struct Meta {
+  int x0, y0, z0, p, k, nplanes, tb, done;
+};
+
+template <typename T>
+struct alignas(128) Smem {
+  static constexpr int NSTAGE = nstage<T>(), NZW = nzw<T>();
+  T plane[NSTAGE][stage_elems<T>()];
+  uint32_t xch[2][NZW + 1][RW][32];  // per plane parity: squares of every slice
+  Meta meta[NSTAGE];
+  uint64_t full[NSTAGE];
+  uint64_t empty[NSTAGE];
+  unsigned long long surv;
+  unsigned int maxbits32;
+  unsigned long long maxbits64;
+};
+
+// 6 conditions x 4 positions -> byte i bits 7..2 = [dx>thr, dx<-thr, dy>thr, dy<-thr, dz>thr, dz<-thr]
+__device__ __forceinline__ uint32_t gather6(const f2 (&c)[12]) {
+  uint32_t w[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
+    const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
+    w[j] = __byte_perm(p01, p23, 0x5410);
+  }
+  return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
+         ((w[3] >> 3) & 0x10101010u) | ((w[4] >> 4) & 0x08080808u) | ((w[5] >> 5) & 0x04040404u);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(NT, 2) k_extract3d(const __grid_constant__ ExtractParams P) {
-  __shared__ T tile[2][SV];
-  __shared__ uint8_t code[CZ * CY * CX];
-  __shared__ unsigned long long s_surv;
-  __shared__ unsigned int s_max32;
-  __shared__ unsigned long long s_max64;
-  const int tid = threadIdx.x;
-  Geo3 G;
-  G.nx = P.nx;
-  G.ny = P.ny;
-  G.nz = P.nz;
-  G.ntg = P.nt_global;
-  G.scale = P.scale;
-  G.scale_f = (float)P.scale;
-  const T thr = (T)P.thr;
-  const T* field = reinterpret_cast<const T*>(P.field);
-  const i64 ntx = (G.nx + TX - 1) / TX, nty = (G.ny + TY - 1) / TY, ntz = (G.nz + TZ - 1) / TZ;
-  const i64 nchunk = (P.tb - P.ta + TCH - 1) / TCH;
-  const i64 nitems = ntx * nty * ntz * nchunk;
-  if (tid == 0) {
-    s_surv = 0;
-    s_max32 = 0;
-    s_max64 = 0;
-  }
-  unsigned long long my_surv = 0;
-  uint32_t my_max32 = 0;
-  double my_maxd = 0.0;
-  const int lx = tid % TX, ly = (tid / TX) % TY, lz = tid / (TX * TY);
-  const int lane = tid & 31;
-  // survivor list (K1b input): per-warp chunks of CHUNK3 entries, one global atomic per chunk
-  long long cur = 0, end = 0;
-  auto enqueue = [&](bool surv, i64 x, i64 y, i64 z, int tflag) {
-    const uint32_t ball = __ballot_sync(0xffffffffu, surv);
-    if (!ball) return;
-    const int n = __popc(ball);
-    int rank = __popc(ball & ((1u << lane) - 1u));
-    int done = 0;
-    while (done < n) {
-      if (cur == end) {
-        long long c = 0;
-        if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK3);
-        cur = __shfl_sync(0xffffffffu, c, 0);
-        end = cur + CHUNK3;
-      }
-      const int k = (int)min((long long)(n - done), end - cur);
-      if (surv && rank >= done && rank < done + k) {
-        const long long e = cur + (rank - done);
-        if (e < P.wcap) {
-          P.wx[e] = (int)x;
-          P.wy[e] = (int)y;
-          P.wz[e] = (int)z;
-          P.wt[e] = tflag;
-        }
-      }
-      cur += k;
-      done += k;
-    }
-    my_surv += surv ? 1 : 0;
-  };
+__device__ __forceinline__ uint32_t code6_f32(const float4 u, const float4 v, const float4 d, const float4 zm,
+                                              const float4 zp, float l, float r, f2 thr2, f2 nthr2) {
+  const f2 dx01 = pack2(__fsub_rn(v.y, l), __fsub_rn(v.z, v.x));
+  const f2 dx23 = pack2(__fsub_rn(v.w, v.y), __fsub_rn(r, v.z));
+  const f2 dy01 = sub2(pack2(d.x, d.y), pack2(u.x, u.y));
+  const f2 dy23 = sub2(pack2(d.z, d.w), pack2(u.z, u.w));
+  const f2 dz01 = sub2(pack2(zp.x, zp.y), pack2(zm.x, zm.y));
+  const f2 dz23 = sub2(pack2(zp.z, zp.w), pack2(zm.z, zm.w));
+  f2 c[12];
+  c[0] = sub2(thr2, dx01);  c[1] = sub2(thr2, dx23);
+  c[2] = sub2(dx01, nthr2); c[3] = sub2(dx23, nthr2);
+  c[4] = sub2(thr2, dy01);  c[5] = sub2(thr2, dy23);
+  c[6] = sub2(dy01, nthr2); c[7] = sub2(dy23, nthr2);
+  c[8] = sub2(thr2, dz01);  c[9] = sub2(thr2, dz23);
+  c[10] = sub2(dz01, nthr2); c[11] = sub2(dz23, nthr2);
+  return gather6(c);
+}
 
-  for (i64 item = blockIdx.x; item < nitems; item += gridDim.x) {
-    i64 r = item;
-    const i64 tx = r % ntx; r /= ntx;
-    const i64 ty = r % nty; r /= nty;
-    const i64 tz = r % ntz; r /= ntz;
-    const i64 ta = P.ta + r * TCH;
-    const i64 tb = min(ta + TCH, P.tb);
-    const i64 plast = min(tb, G.ntg - 1);
-    G.x0 = tx * TX;
-    G.y0 = ty * TY;
-    G.z0 = tz * TZ;
-    const i64 ax = G.x0 + lx, ay = G.y0 + ly, az = G.z0 + lz;
-    uint32_t prev = 0x3Fu;
-    for (i64 p = ta; p <= plast; ++p) {
-      const int cur = (int)((p - ta) & 1);
-      T* S = tile[cur];
-      const T* src = field + (p - P.t0) * G.nx * G.ny * G.nz;
-      __syncthreads();  // previous users of this buffer / of `code` are done
-      for (int i = tid; i < SV; i += NT) {
-        const int xx = i % SX, yy = (i / SX) % SY, zz = i / (SX * SY);
-        const i64 gx = G.x0 - 1 + xx, gy = G.y0 - 1 + yy, gz = G.z0 - 1 + zz;
-        T v = (T)0;
-        if (gx >= 0 && gx < G.nx && gy >= 0 && gy < G.ny && gz >= 0 && gz < G.nz) {
-          v = src[(gz * G.ny + gy) * G.nx + gx];
-          // each vertex is owned by exactly one tile position for the range statistic
-          if (xx >= 1 && xx <= TX && yy >= 1 && yy <= TY && zz >= 1 && zz <= TZ) {
-            if constexpr (sizeof(T) == 4) {
-              const uint32_t b = __float_as_uint(v) & 0x7fffffffu;
-              my_max32 = max(my_max32, b);
-            } else {
-              const double a = fabs(v);
-              my_maxd = (a != a || my_maxd != my_maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(my_maxd, a);
-            }
-          }
-        }
-        S[i] = v;
+__device__ __forceinline__ uint32_t sgn64(double v) { return (uint32_t)((unsigned long long)__double_as_longlong(v) >> 63); }
+
+struct Ctx {
+  int lane;
+  int rpos;        // position (0..3) of x = nx - 1 in this lane, else -1
+  bool lpat;       // x = 0 is this lane's position 0
+  uint32_t oob;    // NEUTRAL bits of this lane's out-of-grid positions
+  long long gy0, ny;
+  long long gz, nz;
+};
+
+// squares (AND over y-pair and x-pair) of the slice whose centre rows start at S (row 0 = y0-1),
+// with the z -+ 1 slices at S -/+ slice_stride
+template <typename T, bool EDGE>
+__device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx& c, f2 thr2, f2 nthr2, T thr,
+                                              uint32_t (&Sq)[RW], uint32_t& maxb, double& maxd, bool count) {
+  const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
+  const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
+  const bool zlo = EDGE && c.gz == 0, zhi = EDGE && c.gz == c.nz - 1, zout = EDGE && c.gz >= c.nz;
+  const T* Zm = zlo ? S : S - zstride;
+  const T* Zp = zhi ? S : S + zstride;
+  if constexpr (sizeof(T) == 4) {
+    auto load = [&](int i, float4& v, float& l, float& r) {
+      v = *reinterpret_cast<const float4*>(S + i * PITCH + XOFF + 4 * c.lane);
+      const float h = S[i * PITCH + hcol];
+      const float up = __shfl_up_sync(0xffffffffu, v.w, 1);
+      const float dn = __shfl_down_sync(0xffffffffu, v.x, 1);
+      l = lane0 ? h : up;
+      r = lane31 ? h : dn;
+      if (EDGE) {
+        if (c.lpat) l = v.x;
+        if (c.rpos == 0) v.y = v.x;
+        if (c.rpos == 1) v.z = v.y;
+        if (c.rpos == 2) v.w = v.z;
+        if (c.rpos == 3) r = v.w;
       }
-      __syncthreads();
-      // vertex codes for x0..x0+TX, y0..y0+TY, z0..z0+TZ (0 = neutral outside the grid)
-      const Tile<T> Pt{S};
-      for (int i = tid; i < CX * CY * CZ; i += NT) {
-        const int xx = i % CX, yy = (i / CX) % CY, zz = i / (CX * CY);
-        const i64 vx = G.x0 + xx, vy = G.y0 + yy, vz = G.z0 + zz;
-        uint32_t cval = 0x3Fu;
-        if (vx < G.nx && vy < G.ny && vz < G.nz) {
-          cval = 0;
-          const i64 c[3] = {vx, vy, vz};
-          const i64 N[3] = {G.nx, G.ny, G.nz};
+    };
+    float4 v0, v1, v2;
+    float l0, r0, l1, r1, l2, r2;
+    load(0, v0, l0, r0);
+    load(1, v1, l1, r1);
+    uint32_t Cprev = 0;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            i64 lo[3] = {vx, vy, vz}, hi[3] = {vx, vy, vz};
-            if (c[a] > 0) lo[a] -= 1;
-            if (c[a] < N[a] - 1) hi[a] += 1;
-            const T d = Pt.at(G, hi[0], hi[1], hi[2]) - Pt.at(G, lo[0], lo[1], lo[2]);
-            cval |= (sbit<T>(thr - d) << (2 * a)) | (sbit<T>(d + thr) << (2 * a + 1));
-          }
-        }
-        code[i] = (uint8_t)cval;
+    for (int k = 0; k <= RW; ++k) {
+      load(k + 2, v2, l2, r2);
+      if (count && k < RW) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);
+      const float4 zm = *reinterpret_cast<const float4*>(Zm + (k + 1) * PITCH + XOFF + 4 * c.lane);
+      const float4 zp = *reinterpret_cast<const float4*>(Zp + (k + 1) * PITCH + XOFF + 4 * c.lane);
+      uint32_t C;
+      if (EDGE) {
+        const long long gy = c.gy0 + k;
+        const float4 u = gy == 0 ? v1 : v0;
+        const float4 d = gy == c.ny - 1 ? v1 : v2;
+        C = (gy >= c.ny || zout) ? NEUTRAL : (code6_f32(u, v1, d, zm, zp, l1, r1, thr2, nthr2) | c.oob);
+      } else {
+        C = code6_f32(v0, v1, v2, zm, zp, l1, r1, thr2, nthr2);
       }
-      __syncthreads();
-      uint32_t cube = 0x3Fu;
+      if (k >= 1) {
+        const uint32_t Y = Cprev & C;
+        const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+        Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
+      }
+      Cprev = C;
+      v0 = v1; l0 = l1; r0 = r1;
+      v1 = v2; l1 = l2; r1 = r2;
+    }
+  } else {
+    // fp64: scalar arithmetic, same layout
+    auto load = [&](int i, double (&f)[6]) {
+      const double* p = S + i * PITCH;
+      const double2 a = *reinterpret_cast<const double2*>(p + XOFF + 4 * c.lane);
+      const double2 b = *reinterpret_cast<const double2*>(p + XOFF + 4 * c.lane + 2);
+      const double h = p[hcol];
+      f[1] = a.x; f[2] = a.y; f[3] = b.x; f[4] = b.y;
+      const double up = __shfl_up_sync(0xffffffffu, b.y, 1);
+      const double dn = __shfl_down_sync(0xffffffffu, a.x, 1);
+      f[0] = lane0 ? h : up;
+      f[5] = lane31 ? h : dn;
+      if (EDGE) {
+        if (c.lpat) f[0] = f[1];
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        cube &= code[((lz + ((c >> 2) & 1)) * CY + ly + ((c >> 1) & 1)) * CX + lx + (c & 1)];
-      const bool inside = ax < G.nx && ay < G.ny && az < G.nz;
-      // anchors at p - 1 (hypercube over planes p - 1 and p), then anchors on the last timestep (no
-      // t+1 corners)
-      const bool s0 = p > ta && inside && ((prev & cube) & 0x3Fu) == 0;
-      const bool s1 = p == G.ntg - 1 && p < tb && inside && (cube & 0x3Fu) == 0;
-      enqueue(s0, ax, ay, az, (int)((uint32_t)(p - 1) | 0x80000000u));
-      enqueue(s1, ax, ay, az, (int)p);
-      prev = cube;
+        for (int q = 0; q < 4; ++q)
+          if (c.rpos == q) f[q + 2] = f[q + 1];
+      }
+    };
+    double f0[6], f1[6], f2_[6];
+    load(0, f0);
+    load(1, f1);
+    uint32_t Cprev = 0;
+#pragma unroll
+    for (int k = 0; k <= RW; ++k) {
+      load(k + 2, f2_);
+      if (count && k < RW)
+#pragma unroll
+        for (int q = 1; q <= 4; ++q) {
+          const double a = fabs(f1[q]);
+          maxd = (a != a || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, a);
+        }
+      const long long gy = c.gy0 + k;
+      const double* fu = (EDGE && gy == 0) ? f1 : f0;
+      const double* fd = (EDGE && gy == c.ny - 1) ? f1 : f2_;
+      uint32_t W = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double zmv = Zm[(k + 1) * PITCH + XOFF + 4 * c.lane + q], zpv = Zp[(k + 1) * PITCH + XOFF + 4 * c.lane + q];
+        const double dx = f1[q + 2] - f1[q], dy = fd[q + 1] - fu[q + 1], dz = zpv - zmv;
+        const uint32_t b6 = (sgn64(thr - dx) << 5) | (sgn64(dx + thr) << 4) | (sgn64(thr - dy) << 3) |
+                            (sgn64(dy + thr) << 2) | (sgn64(thr - dz) << 1) | sgn64(dz + thr);
+        W |= b6 << (8 * q + 2);
+      }
+      const uint32_t C = (EDGE && (gy >= c.ny || zout)) ? NEUTRAL : (EDGE ? (W | c.oob) : W);
+      if (k >= 1) {
+        const uint32_t Y = Cprev & C;
+        const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+        Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
+      }
+      Cprev = C;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        f0[q] = f1[q];
+        f1[q] = f2_[q];
+      }
     }
   }
-  // the unused rest of the warp's chunk holds no cube
-  for (long long e = cur + lane; e < end; e += 32)
-    if (e < P.wcap) P.wt[e] = -1;
-  atomicAdd(&s_surv, my_surv);
-  atomicMax(&s_max32, my_max32);
-  atomicMax(&s_max64, (unsigned long long)__double_as_longlong(my_maxd));
+}
+
+template <typename T, bool TMA>
+__global__ void __launch_bounds__(nthreads<T>(), 1)
+    k_scan3d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
+  constexpr int NZW = nzw<T>(), SL = slices<T>(), NSTAGE = nstage<T>();
+  constexpr int PRODUCER = NZW + 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const uint32_t mis = smem_u32(smem_raw) & 127u;
+  Smem<T>& sm = *reinterpret_cast<Smem<T>*>(smem_raw + (mis ? 128 - mis : 0));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const i64 nx = P.nx, ny = P.ny, nz = P.nz;
+  constexpr uint32_t STAGE_BYTES = PITCH * ROWS * SL * sizeof(T);
+  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
+  const int ntc = (int)((P.tb - P.ta + TCH - 1) / TCH);
+  const long long nitems = (long long)ntx * nty * ntz * ntc;
+  if (tid == 0) {
+    sm.surv = 0;
+    sm.maxbits32 = 0;
+    sm.maxbits64 = 0;
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], NZW + 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == PRODUCER) {
+    const T* field = reinterpret_cast<const T*>(P.field);
+    int gk = 0;
+    while (true) {
+      long long item = 0;
+      if (lane == 0) item = (long long)atomicAdd(&P.counters[CNT_WORK], 1ull);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= nitems) break;
+      long long r = item;
+      const int tx = (int)(r % ntx); r /= ntx;
+      const int ty_ = (int)(r % nty); r /= nty;
+      const int tz = (int)(r % ntz); r /= ntz;
+      const i64 x0 = (i64)tx * TX, y0 = (i64)ty_ * RW, z0 = (i64)tz * NZW;
+      const i64 ta = P.ta + r * TCH;
+      const i64 tb = min(ta + TCH, P.tb);
+      const i64 plast = min(tb, P.nt_global - 1);
+      const int np = (int)(plast - ta + 1);
+      for (int k = 0; k < np; ++k, ++gk) {
+        const int s = gk % NSTAGE;
+        if (gk >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
+        if (lane == 0) {
+          Meta& m = sm.meta[s];
+          m.x0 = (int)x0; m.y0 = (int)y0; m.z0 = (int)z0;
+          m.p = (int)(ta + k); m.k = k; m.nplanes = np; m.tb = (int)tb; m.done = 0;
+        }
+        if (TMA) {
+          if (lane == 0) {
+            mbar_expect_tx(&sm.full[s], STAGE_BYTES);
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+                    smem_u32(sm.plane[s])),
+                "l"(&tmap), "r"(smem_u32(&sm.full[s])), "r"((int)(x0 - XOFF)), "r"((int)(y0 - 1)), "r"((int)(z0 - 1)),
+                "r"((int)(ta + k - P.t0))
+                : "memory");
+          }
+        } else {
+          const T* src = field + (ta + k - P.t0) * nx * ny * nz;
+          T* dst = sm.plane[s];
+          for (int idx = lane; idx < PITCH * ROWS * SL; idx += 32) {
+            const int xx = idx % PITCH, yy = (idx / PITCH) % ROWS, zz = idx / (PITCH * ROWS);
+            const i64 gx = x0 - XOFF + xx, gy = y0 - 1 + yy, gz = z0 - 1 + zz;
+            dst[idx] = (gx >= 0 && gx < nx && gy >= 0 && gy < ny && gz >= 0 && gz < nz) ? src[(gz * ny + gy) * nx + gx] : (T)0;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.full[s]);
+        }
+      }
+    }
+    const int s = gk % NSTAGE;
+    if (gk >= NSTAGE) mbar_wait_sleep(&sm.empty[s], (uint32_t)((gk / NSTAGE - 1) & 1), 1, gk);
+    if (lane == 0) {
+      sm.meta[s].done = 1;
+      mbar_arrive(&sm.full[s]);
+    }
+  } else {
+    // scan warps: warp w owns slice z0 + w (w = NZW: the top slice, squares only)
+    const T thr = (T)P.thr;
+    const f2 thr2 = pack2((float)P.thr, (float)P.thr);
+    const f2 nthr2 = pack2(-(float)P.thr, -(float)P.thr);
+    uint32_t maxb32 = 0;
+    double maxd = 0.0;
+    unsigned long long mysurv = 0;
+    uint32_t prevK[RW];
+    long long cur = 0, end = 0;
+    const bool top = warp == NZW;
+    auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0, int z) {
+      while (__any_sync(0xffffffffu, mask != 0)) {
+        if (cur == end) {
+          long long cc = 0;
+          if (lane == 0) cc = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
+          cur = __shfl_sync(0xffffffffu, cc, 0);
+          end = cur + CHUNK;
+        }
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int n = (int)min((long long)total, end - cur);
+        int r = incl - cnt;
+        while (mask && r < n) {
+          const int bb = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const long long e = cur + r++;
+          if (e < P.wcap) {
+            P.wx[e] = x0 + 4 * lane + (bb >> 3);
+            P.wy[e] = y0 + (bb & 7);
+            P.wz[e] = z;
+            P.wt[e] = tflag;
+          }
+        }
+        cur += n;
+        mysurv += n;
+      }
+    };
+    Ctx c;
+    c.lane = lane;
+    c.ny = ny;
+    c.nz = nz;
+    int gk = 0, x0 = 0, y0 = 0, z0 = 0;
+    bool edge = false;
+    while (true) {
+      const int s = gk % NSTAGE;
+      mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
+      const Meta m = sm.meta[s];
+      if (m.done) break;
+      if (m.k == 0) {
+        x0 = m.x0;
+        y0 = m.y0;
+        z0 = m.z0;
+        const i64 gx = (i64)x0 + 4 * lane;
+        c.gy0 = y0;
+        c.gz = z0 + warp;
+        c.lpat = gx == 0;
+        c.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
+        c.oob = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (gx + i >= nx) c.oob |= 0xFCu << (8 * i);
+        edge = x0 < 1 || x0 + LX + 1 > nx || y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
+      }
+      const T* S = sm.plane[s] + (warp + 1) * (PITCH * ROWS);  // slice z0 + warp
+      uint32_t Sq[RW];
+      if (edge) slice_squares<T, true>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      else slice_squares<T, false>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
+      const int par = gk & 1;
+#pragma unroll
+      for (int r = 0; r < RW; ++r) sm.xch[par][warp][r][lane] = Sq[r];
+      asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * 32) : "memory");
+      if (!top) {
+        uint32_t K[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) K[r] = Sq[r] & sm.xch[par][warp + 1][r][lane];  // z-pair
+        auto survivors_of = [&](const uint32_t* Q) {
+          uint32_t mask = 0;
+#pragma unroll
+          for (int r = 0; r < RW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
+          return lane == 31 ? 0u : mask;
+        };
+        const bool inz = z0 + warp < nz;
+        const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
+        if (inz) {
+          if (m.k > 0) {
+            uint32_t Q[RW];
+#pragma unroll
+            for (int r = 0; r < RW; ++r) Q[r] = prevK[r] & K[r];
+            enqueue(survivors_of(Q), (int)((uint32_t)(m.p - 1) | 0x80000000u), x0, y0, z0 + warp);
+          }
+          if (lastg) enqueue(survivors_of(K), m.p, x0, y0, z0 + warp);
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r) prevK[r] = K[r];
+      }
+      ++gk;
+    }
+    for (long long e = cur + lane; e < end; e += 32)
+      if (e < P.wcap) P.wt[e] = -1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      maxb32 = max(maxb32, __shfl_xor_sync(0xffffffffu, maxb32, o));
+      const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
+      maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
+    }
+    if (lane == 0) {
+      atomicAdd(&sm.surv, mysurv);
+      atomicMax(&sm.maxbits32, maxb32);
+      atomicMax(&sm.maxbits64, (unsigned long long)__double_as_longlong(maxd));
+    }
+  }
   __syncthreads();
   if (tid == 0) {
-    atomicAdd(&P.counters[CNT_SURVIVORS], s_surv);
-    atomicMax(&P.counters[CNT_MAXBITS], sizeof(T) == 4 ? (unsigned long long)s_max32 : s_max64);
+    atomicAdd(&P.counters[CNT_SURVIVORS], sm.surv);
+    atomicMax(&P.counters[CNT_MAXBITS], sizeof(T) == 4 ? (unsigned long long)sm.maxbits32 : sm.maxbits64);
   }
 }
+}  // namespace s3
 
 // K1b (3D): one thread per surviving hypercube of the list; gradients and Hessians straight from the
 // field (L2/HBM).
@@ -587,18 +830,36 @@ __global__ void __launch_bounds__(128) k_exact3d(const __grid_constant__ Extract
 
 }  // namespace k3d
 
-template <typename T>
+template <typename T, bool TMA>
 static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   using namespace k3d;
+  using namespace k3d::s3;
+  CUtensorMap map;
+  memset(&map, 0, sizeof map);
+  if (TMA) {
+    auto enc = sm100::get_encode();
+    const cuuint64_t dims[4] = {(cuuint64_t)P.nx, (cuuint64_t)P.ny, (cuuint64_t)P.nz, (cuuint64_t)P.nt_buf};
+    const cuuint64_t strides[3] = {(cuuint64_t)P.nx * sizeof(T), (cuuint64_t)P.nx * P.ny * sizeof(T),
+                                   (cuuint64_t)P.nx * P.ny * P.nz * sizeof(T)};
+    const cuuint32_t box[4] = {PITCH, ROWS, (cuuint32_t)slices<T>(), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&map, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                     const_cast<void*>(P.field), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return launch3_t<T, false>(P, stream);
+  }
+  const size_t smem = sizeof(Smem<T>) + 128;
+  auto kern = k_scan3d<T, TMA>;
+  FTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148, per_sm = 0;
   FTK_CUDA_TRY(cudaGetDevice(&dev));
   FTK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract3d<T>, NT, 0));
-  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY) * ((P.nz + TZ - 1) / TZ) *
+  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads<T>(), smem));
+  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
                           ((P.tb - P.ta + TCH - 1) / TCH);
   if (items <= 0) return FTK_OK;
-  const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1) * 4);
-  k_extract3d<T><<<(unsigned)grid, NT, 0, stream>>>(P);
+  const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, nthreads<T>(), smem, stream>>>(map, P);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
   int xper = 0;
@@ -609,8 +870,13 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
 }
 
 int launch_extract3d(const ExtractParams& P, cudaStream_t stream) {
-  if (P.dtype == FTK_F32) return launch3_t<float>(P, stream);
-  return launch3_t<double>(P, stream);
+  const size_t esz = P.dtype == FTK_F32 ? 4 : 8;
+  const bool aligned = (reinterpret_cast<uintptr_t>(P.field) % 16 == 0) && ((P.nx * esz) % 16 == 0);
+  const bool tma = aligned && sm100::get_encode() != nullptr && !P.force_generic;
+  if (P.nx >= (1ll << 31) - 256 || P.ny >= (1ll << 31) - 64 || P.nz >= (1ll << 31) - 64 || P.nt_global >= (1ll << 30))
+    return FTK_ERR_INVALID_ARG;
+  if (P.dtype == FTK_F32) return tma ? launch3_t<float, true>(P, stream) : launch3_t<float, false>(P, stream);
+  return tma ? launch3_t<double, true>(P, stream) : launch3_t<double, false>(P, stream);
 }
 
 }  // namespace ftk

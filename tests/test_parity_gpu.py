@@ -236,3 +236,22 @@ def test_c3_closed_form_full_size(ftk, oracle_lib):
     sub = f[ta: tb + 1].cpu()
     ref, _ = oracle_lib.extract(sub.numpy(), cfg.scale_log2, t0=ta, nt_global=nt, ta=ta, tb=tb)
     compare(rec[(t_of >= ta) & (t_of < tb)], ref, labels=False)
+
+
+@pytest.mark.parametrize("where", [(0, 0, 0), (1, 0, 7), (2, 5, 0), (1, 39, 66), (0, 17, 66)])
+def test_range_error_anywhere_2d(ftk, where):
+    """the range check covers every vertex, grid boundary rows and columns included"""
+    f = fi.Woven(67, 40, 3, sigma=0.0).generate()
+    f[where] = float("nan")
+    with pytest.raises(ftk.FtkError) as e:
+        ftk.track(f.cuda(), 26)
+    assert e.value.status == ftk.ERR_RANGE
+
+
+@pytest.mark.parametrize("where", [(0, 0, 0, 0), (1, 12, 0, 7), (2, 0, 9, 0), (1, 12, 9, 66), (0, 5, 0, 66)])
+def test_range_error_anywhere_3d(ftk, where):
+    f = fi.Woven(67, 10, 3, L=15.0, sigma=0.0, nz=13).generate()
+    f[where] = float("nan")
+    with pytest.raises(ftk.FtkError) as e:
+        ftk.track(f.cuda(), 26)
+    assert e.value.status == ftk.ERR_RANGE
