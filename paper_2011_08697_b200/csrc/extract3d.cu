@@ -251,148 +251,6 @@ constexpr Cells4 make_cells4() {
 }
 __constant__ Cells4 cCells4 = make_cells4();
 
-// ------------------------------------------------------------------------------ exact stage
-template <typename T, typename Acc>
-__device__ void process_hypercube(const Acc& A, const Acc& B, bool hasB, const Geo3& G,
-                                  const ExtractParams& P, i64 x, i64 y, i64 z, i64 t) {
-  i64 g[16][3];
-  uint32_t exists = 0;
-#pragma unroll 1
-  for (int c = 0; c < 16; ++c) {
-    const i64 cx = x + (c & 1), cy = y + ((c >> 1) & 1), cz = z + ((c >> 2) & 1);
-    const bool ex = cx < G.nx && cy < G.ny && cz < G.nz && ((c & 8) == 0 || hasB);
-    if (ex) {
-      grad3<T>((c & 8) ? B : A, G, cx, cy, cz, g[c]);
-      exists |= 1u << c;
-    } else {
-      g[c][0] = g[c][1] = g[c][2] = 0;
-    }
-  }
-  // own faces (60 types)
-  unsigned long long pmask = 0;
-#pragma unroll 1
-  for (int ty = 0; ty < 60; ++ty) {
-    const int m1 = cK4.masks[ty][0], m2 = cK4.masks[ty][1], m3 = cK4.masks[ty][2];
-    if (!((exists >> m3) & 1)) continue;
-    const i64 gv[4][3] = {{g[0][0], g[0][1], g[0][2]}, {g[m1][0], g[m1][1], g[m1][2]},
-                          {g[m2][0], g[m2][1], g[m2][2]}, {g[m3][0], g[m3][1], g[m3][2]}};
-    bool rej = false;  // exact sign reject: one component of one strict sign on all vertices
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      rej |= (gv[0][j] > 0 && gv[1][j] > 0 && gv[2][j] > 0 && gv[3][j] > 0) ||
-             (gv[0][j] < 0 && gv[1][j] < 0 && gv[2][j] < 0 && gv[3][j] < 0);
-    if (!rej && punctured4(gv)) pmask |= 1ull << ty;
-  }
-  // cells: only full hypercubes have cells anchored here
-  const bool full = x + 1 < G.nx && y + 1 < G.ny && z + 1 < G.nz && hasB;
-  const int npunct = __popcll(pmask);
-  unsigned long long rbase = 0;
-  if (npunct) rbase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)npunct);
-  if (full) {
-#pragma unroll 1
-    for (int ci = 0; ci < 24; ++ci) {
-      const Cell4& cd = cCells4.c[ci];
-      int k = 0;
-      long long ends[2] = {-1, -1};
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((pmask >> cd.own[q]) & 1ull) {
-          if (k < 2) ends[k] = (long long)(rbase + __popcll(pmask & ((1ull << cd.own[q]) - 1ull)));
-          ++k;
-        }
-      // upper face (w1, w2, w3, 15): vertices are hypercube corners
-      const i64 gu[4][3] = {{g[cd.w[1]][0], g[cd.w[1]][1], g[cd.w[1]][2]}, {g[cd.w[2]][0], g[cd.w[2]][1], g[cd.w[2]][2]},
-                            {g[cd.w[3]][0], g[cd.w[3]][1], g[cd.w[3]][2]}, {g[15][0], g[15][1], g[15][2]}};
-      if (punctured4(gu)) {
-        if (k < 2) {
-          const int a1 = cd.w[1];
-          const i64 fx = x + (a1 & 1), fy = y + ((a1 >> 1) & 1), fz = z + ((a1 >> 2) & 1), ft = t + ((a1 >> 3) & 1);
-          ends[k] = -1 - ((((ft * G.nz + fz) * G.ny + fy) * G.nx + fx) * 60 + cd.up_type);
-        }
-        ++k;
-      }
-      if (k == 2) {
-        const unsigned long long e = atomicAdd(&P.counters[CNT_EDGES], 1ull);
-        if (e < (unsigned long long)P.capacity) {
-          P.edges[2 * e] = ends[0] >= 0 ? ends[0] : ends[1];
-          P.edges[2 * e + 1] = ends[0] >= 0 ? ends[1] : ends[0];
-        }
-      } else if (k != 0) {
-        atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
-      }
-    }
-  }
-  // records
-  unsigned long long pm = pmask;
-  while (pm) {
-    const int ty = __ffsll((long long)pm) - 1;
-    pm &= pm - 1;
-    const unsigned long long slot = rbase + __popcll(pmask & ((1ull << ty) - 1ull));
-    const int m[4] = {0, cK4.masks[ty][0], cK4.masks[ty][1], cK4.masks[ty][2]};
-    i64 gv[4][3];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) gv[k][j] = g[m[k]][j];
-    // D_k = (-1)^(k+3) det(rows != k)  (Eq. 2)
-    const i128 D0 = -det3(gv[1], gv[2], gv[3]);
-    const i128 D1 = det3(gv[0], gv[2], gv[3]);
-    const i128 D2 = -det3(gv[0], gv[1], gv[3]);
-    const i128 D3 = det3(gv[0], gv[1], gv[2]);
-    const i128 S = D0 + D1 + D2 + D3;
-    double mu[4];
-    uint32_t flags = 0;
-    if (S == 0) {
-      mu[0] = mu[1] = mu[2] = mu[3] = 0.25;
-      flags |= FTK_CP_DEGENERATE_LOC;
-    } else {
-      const double s = i128_to_double_rn(S);
-      mu[0] = __ddiv_rn(i128_to_double_rn(D0), s);
-      mu[1] = __ddiv_rn(i128_to_double_rn(D1), s);
-      mu[2] = __ddiv_rn(i128_to_double_rn(D2), s);
-      mu[3] = __ddiv_rn(i128_to_double_rn(D3), s);
-    }
-    double pv[4][4];  // x, y, z, t of each vertex
-    double Hd[6][4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const i64 vx = x + (m[k] & 1), vy = y + ((m[k] >> 1) & 1), vz = z + ((m[k] >> 2) & 1), vt = t + ((m[k] >> 3) & 1);
-      pv[0][k] = (double)vx;
-      pv[1][k] = (double)vy;
-      pv[2][k] = (double)vz;
-      pv[3][k] = (double)vt;
-      i64 H[6];
-      hess3<T>(P, G, vx, vy, vz, vt, H);
-#pragma unroll
-      for (int e = 0; e < 6; ++e) Hd[e][k] = __ll2double_rn(H[e]);
-    }
-    double Hb[6];
-#pragma unroll
-    for (int e = 0; e < 6; ++e) Hb[e] = dot4_nofma(mu, Hd[e]);
-    const int type = classify3(Hb);
-    const int span = m[3];
-    if (!(span & 8)) flags |= FTK_CP_ORDINAL;
-    if (span != 15) {
-      const int c = 15 & ~span;
-      const i64 vc = c == 1 ? x : c == 2 ? y : c == 4 ? z : t;
-      const i64 Nc = c == 1 ? G.nx : c == 2 ? G.ny : c == 4 ? G.nz : G.ntg;
-      if (vc == 0 || vc == Nc - 1) flags |= FTK_CP_BOUNDARY;
-    }
-    if (slot < (unsigned long long)P.capacity) {
-      ftk_cp* r = P.out + slot;
-      r->face_id = (((t * G.nz + z) * G.ny + y) * G.nx + x) * 60 + ty;
-      P.fid[slot] = r->face_id;
-      r->label = -1;
-      r->x = dot4_nofma(mu, pv[0]);
-      r->y = dot4_nofma(mu, pv[1]);
-      r->z = dot4_nofma(mu, pv[2]);
-      r->t = dot4_nofma(mu, pv[3]);
-      r->type = type;
-      r->flags = flags;
-    }
-  }
-}
-
 // ------------------------------------------------------------------------------ K1a (3D): the scan
 // Persistent, one CTA per SM.  A work item is a 124 x 8 x 8 tile of anchors (x, y, z) times a chunk
 // of TCH anchor timesteps.  Per timestep the producer warp stages the 136 x 11 x 11 halo box
@@ -801,10 +659,19 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
 }
 }  // namespace s3
 
-// K1b (3D): one thread per surviving hypercube of the list; gradients and Hessians straight from the
-// field (L2/HBM).
+// ------------------------------------------------------------------------------ K1b (3D)
+// One warp per surviving hypercube of the list: lanes 0..15 take the 16 corner gradients (exact
+// int64, straight from the field), the 60 face types are spread over the lanes (two each) for the
+// SoS point-in-simplex test, lanes 0..23 take the 24 cells (pentachora) -- 0 or 2
+// punctured sides each, pairs become trajectory edges -- and the punctured faces are
+// spread over the lanes for the Eq. 2 location and the Descartes-rule Hessian type in fixed-order
+// FP64.  A hypercube's 60 faces with their SoS chains are far too much serial work for one thread.
+constexpr int XW3 = 4;  // warps per block
+
 template <typename T>
-__global__ void __launch_bounds__(128) k_exact3d(const __grid_constant__ ExtractParams P) {
+__global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ ExtractParams P) {
+  __shared__ i64 sg[XW3][16][3];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Geo3 G;
   G.nx = P.nx;
   G.ny = P.ny;
@@ -816,15 +683,170 @@ __global__ void __launch_bounds__(128) k_exact3d(const __grid_constant__ Extract
   const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
   const T* field = reinterpret_cast<const T*>(P.field);
   const i64 plane = G.nx * G.ny * G.nz;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nwin;
-       e += (long long)gridDim.x * blockDim.x) {
+  i64(&g)[16][3] = sg[w];
+  for (long long e = (long long)blockIdx.x * XW3 + w; e < nwin; e += (long long)gridDim.x * XW3) {
     const int et = P.wt[e];
     if (et == -1) continue;
     const bool hasB = et < 0;
     const i64 t = et & 0x3fffffff;
+    const i64 x = P.wx[e], y = P.wy[e], z = P.wz[e];
     const GTile<T> A{field + (t - P.t0) * plane};
     const GTile<T> B{hasB ? A.S + plane : A.S};
-    process_hypercube<T>(A, B, hasB, G, P, P.wx[e], P.wy[e], P.wz[e], t);
+    // corner gradients
+    uint32_t ex = 0;
+    {
+      const int c = lane & 15;
+      const i64 cx = x + (c & 1), cy = y + ((c >> 1) & 1), cz = z + ((c >> 2) & 1);
+      const bool e1 = cx < G.nx && cy < G.ny && cz < G.nz && ((c & 8) == 0 || hasB);
+      if (lane < 16) {
+        i64 gc[3] = {0, 0, 0};
+        if (e1) grad3<T>((c & 8) ? B : A, G, cx, cy, cz, gc);
+        g[c][0] = gc[0];
+        g[c][1] = gc[1];
+        g[c][2] = gc[2];
+      }
+      ex = __ballot_sync(0xffffffffu, lane < 16 && e1);
+    }
+    __syncwarp();
+    // the 60 face types, two per lane
+    unsigned long long pmask = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ty = lane + 32 * h;
+      bool pu = false;
+      if (ty < 60) {
+        const int m1 = cK4.masks[ty][0], m2 = cK4.masks[ty][1], m3 = cK4.masks[ty][2];
+        if ((ex >> m3) & 1) {
+          const i64 gv[4][3] = {{g[0][0], g[0][1], g[0][2]}, {g[m1][0], g[m1][1], g[m1][2]},
+                                {g[m2][0], g[m2][1], g[m2][2]}, {g[m3][0], g[m3][1], g[m3][2]}};
+          bool rej = false;  // exact sign reject: one component of one strict sign on all vertices
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            rej |= (gv[0][j] > 0 && gv[1][j] > 0 && gv[2][j] > 0 && gv[3][j] > 0) ||
+                   (gv[0][j] < 0 && gv[1][j] < 0 && gv[2][j] < 0 && gv[3][j] < 0);
+          pu = !rej && punctured4(gv);
+        }
+      }
+      pmask |= (unsigned long long)__ballot_sync(0xffffffffu, pu) << (32 * h);
+    }
+    const int npunct = __popcll(pmask);
+    unsigned long long rbase = 0;
+    if (lane == 0 && npunct) rbase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)npunct);
+    rbase = __shfl_sync(0xffffffffu, rbase, 0);
+    // cells: only full hypercubes have cells anchored here
+    const bool full = x + 1 < G.nx && y + 1 < G.ny && z + 1 < G.nz && hasB;
+    if (full) {
+      int k = 0;
+      long long ends[2] = {-1, -1};
+      if (lane < 24) {
+        const Cell4& cd = cCells4.c[lane];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((pmask >> cd.own[q]) & 1ull) {
+            if (k < 2) ends[k] = (long long)(rbase + __popcll(pmask & ((1ull << cd.own[q]) - 1ull)));
+            ++k;
+          }
+        // upper face (w1, w2, w3, 15): vertices are hypercube corners
+        const i64 gu[4][3] = {{g[cd.w[1]][0], g[cd.w[1]][1], g[cd.w[1]][2]},
+                              {g[cd.w[2]][0], g[cd.w[2]][1], g[cd.w[2]][2]},
+                              {g[cd.w[3]][0], g[cd.w[3]][1], g[cd.w[3]][2]},
+                              {g[15][0], g[15][1], g[15][2]}};
+        if (punctured4(gu)) {
+          if (k < 2) {
+            const int a1 = cd.w[1];
+            const i64 fx = x + (a1 & 1), fy = y + ((a1 >> 1) & 1), fz = z + ((a1 >> 2) & 1), ft = t + ((a1 >> 3) & 1);
+            ends[k] = -1 - ((((ft * G.nz + fz) * G.ny + fy) * G.nx + fx) * 60 + cd.up_type);
+          }
+          ++k;
+        }
+      }
+      const uint32_t pairs = __ballot_sync(0xffffffffu, k == 2);
+      const uint32_t bad = __ballot_sync(0xffffffffu, k != 0 && k != 2);
+      if (lane == 0 && bad) atomicAdd(&P.counters[CNT_INVARIANT], (unsigned long long)__popc(bad));
+      if (pairs) {
+        unsigned long long eb = 0;
+        if (lane == 0) eb = atomicAdd(&P.counters[CNT_EDGES], (unsigned long long)__popc(pairs));
+        eb = __shfl_sync(0xffffffffu, eb, 0);
+        if (k == 2) {
+          const unsigned long long es = eb + __popc(pairs & ((1u << lane) - 1u));
+          if (es < (unsigned long long)P.capacity) {
+            P.edges[2 * es] = ends[0] >= 0 ? ends[0] : ends[1];
+            P.edges[2 * es + 1] = ends[0] >= 0 ? ends[1] : ends[0];
+          }
+        }
+      }
+    }
+    // records: the punctured faces spread over the lanes
+    for (int i = lane; i < npunct; i += 32) {
+      unsigned long long pm = pmask;
+      for (int j = 0; j < i; ++j) pm &= pm - 1;
+      const int ty = __ffsll((long long)pm) - 1;
+      const unsigned long long slot = rbase + i;
+      const int m[4] = {0, cK4.masks[ty][0], cK4.masks[ty][1], cK4.masks[ty][2]};
+      i64 gv[4][3];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gv[kk][j] = g[m[kk]][j];
+      // D_k = (-1)^(k+3) det(rows != k)  (Eq. 2)
+      const i128 D0 = -det3(gv[1], gv[2], gv[3]);
+      const i128 D1 = det3(gv[0], gv[2], gv[3]);
+      const i128 D2 = -det3(gv[0], gv[1], gv[3]);
+      const i128 D3 = det3(gv[0], gv[1], gv[2]);
+      const i128 S = D0 + D1 + D2 + D3;
+      double mu[4];
+      uint32_t flags = 0;
+      if (S == 0) {
+        mu[0] = mu[1] = mu[2] = mu[3] = 0.25;
+        flags |= FTK_CP_DEGENERATE_LOC;
+      } else {
+        const double sd = i128_to_double_rn(S);
+        mu[0] = __ddiv_rn(i128_to_double_rn(D0), sd);
+        mu[1] = __ddiv_rn(i128_to_double_rn(D1), sd);
+        mu[2] = __ddiv_rn(i128_to_double_rn(D2), sd);
+        mu[3] = __ddiv_rn(i128_to_double_rn(D3), sd);
+      }
+      double pv[4][4];  // x, y, z, t of each vertex
+      double Hd[6][4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const i64 vx = x + (m[kk] & 1), vy = y + ((m[kk] >> 1) & 1), vz = z + ((m[kk] >> 2) & 1),
+                  vt = t + ((m[kk] >> 3) & 1);
+        pv[0][kk] = (double)vx;
+        pv[1][kk] = (double)vy;
+        pv[2][kk] = (double)vz;
+        pv[3][kk] = (double)vt;
+        i64 H[6];
+        hess3<T>(P, G, vx, vy, vz, vt, H);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) Hd[q][kk] = __ll2double_rn(H[q]);
+      }
+      double Hb[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) Hb[q] = dot4_nofma(mu, Hd[q]);
+      const int type = classify3(Hb);
+      const int span = m[3];
+      if (!(span & 8)) flags |= FTK_CP_ORDINAL;
+      if (span != 15) {
+        const int c = 15 & ~span;
+        const i64 vc = c == 1 ? x : c == 2 ? y : c == 4 ? z : t;
+        const i64 Nc = c == 1 ? G.nx : c == 2 ? G.ny : c == 4 ? G.nz : G.ntg;
+        if (vc == 0 || vc == Nc - 1) flags |= FTK_CP_BOUNDARY;
+      }
+      if (slot < (unsigned long long)P.capacity) {
+        ftk_cp* r = P.out + slot;
+        r->face_id = (((t * G.nz + z) * G.ny + y) * G.nx + x) * 60 + ty;
+        P.fid[slot] = r->face_id;
+        r->label = -1;
+        r->x = dot4_nofma(mu, pv[0]);
+        r->y = dot4_nofma(mu, pv[1]);
+        r->z = dot4_nofma(mu, pv[2]);
+        r->t = dot4_nofma(mu, pv[3]);
+        r->type = type;
+        r->flags = flags;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -863,8 +885,8 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
   int xper = 0;
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, k_exact3d<T>, 128, 0));
-  k_exact3d<T><<<(unsigned)(sms * std::max(xper, 1)), 128, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, k_exact3d<T>, XW3 * 32, 0));
+  k_exact3d<T><<<(unsigned)(sms * std::max(xper, 1)), XW3 * 32, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }
