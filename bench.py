@@ -119,17 +119,24 @@ def cpu_baseline(cfg, seconds_budget: float = 20.0):
     import ftk_inputs as fi
     import paper_2011_08697_b200 as ftk
 
-    nx, ny = cfg.shape[0], cfg.shape[1]
+    spatial = cfg.shape[:-1]
     nt_s = 3
     w = cfg.make()
+    if len(spatial) == 3:
+        # 3D: a 64^3 block of the same field kind as its own domain keeps the oracle within ~20 s
+        w = fi.Woven(64, 64, nt_s, nz=64, scale_log2=cfg.scale_log2) if cfg.kind == "woven3d" else \
+            fi.MovingExtremum((64, 64, 64), nt_s, c0=(30.0, 31.0, 32.0), v=(0.25, 0.125, -0.0625),
+                              scale_log2=cfg.scale_log2)
+        spatial = (64, 64, 64)
     f = w.generate(nt=nt_s).numpy()
     cores = os.cpu_count() or 1
     t = time.perf_counter()
     rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
     dt = time.perf_counter() - t
     return {"value": nf / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"oracle track (plain C, OpenMP {cores} threads) on {nx}x{ny}x{nt_s} timesteps of {cfg.name} "
-                      f"as its own domain: {nf} faces in {dt:.2f} s"}
+            "sample": f"oracle track (plain C, OpenMP {cores} threads) on {'x'.join(map(str, spatial))}x{nt_s} "
+                      f"timesteps of a {cfg.name}-kind field as its own domain: {nf} faces in {dt:.2f} s "
+                      f"({dt * cores:.0f} core-seconds)"}
 
 
 def run_reference(args):
@@ -141,11 +148,12 @@ def run_reference(args):
     import ftk_inputs as fi
 
     cfg = fi.CONFIGS[args.config]
-    nx, ny, nt = cfg.shape
+    spatial = cfg.shape[:-1]
+    ny = spatial[-1]           # extent of the sliced axis (y in 2D, z in 3D; the field is [t][z][y][x])
     cores = os.cpu_count() or 1
     w = cfg.make()
-    # per-step sample: full rows x a band of rows x 2 timesteps, sized so the whole run ends in
-    # about two minutes
+    # per-step sample: a band of rows (2D) / slices (3D) x 2 timesteps of the workload's field, sized
+    # so the whole run ends in about two minutes
     total_budget = 120.0
     per_step = total_budget / max(1, args.steps + args.warmup)
     rows = 16
@@ -167,7 +175,8 @@ def run_reference(args):
             times.append(dt)
     ms = 1000.0 * sum(times) / len(times)
     value = nf / (ms / 1000.0)
-    sample = f"oracle track on {nx}x{rows}x2 of {cfg.name} per step ({nf} faces), {cores} threads"
+    band = "x".join(map(str, list(spatial[:-1]) + [rows]))
+    sample = f"oracle track on {band}x2 of {cfg.name} per step ({nf} faces), {cores} threads"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -196,7 +205,7 @@ def run_ours(args):
     ftk.lib()
 
     cfg = fi.CONFIGS[args.config]
-    nx, ny, nt = cfg.shape
+    spatial, nt = cfg.shape[:-1], cfg.shape[-1]
     w = cfg.make()
     if world > 1:
         nt_global = nt * world
@@ -270,10 +279,13 @@ def run_ours(args):
     kb_avg = sum(kb_ms) / len(kb_ms)
     _, st3 = ftk.last_timings()
     n_surv = st3[1]
-    alg_bytes = field.numel() * esz + 12 * n_surv
+    alg_bytes = field.numel() * esz + (16 if field.dim() == 4 else 12) * n_surv
     achieved = alg_bytes / (ka_avg / 1000.0) / 1e9
     peak, peak_src = _peaks()
-    traffic = _ncu_traffic(cfg.name, "k_scan2d")
+    d3 = field.dim() == 4
+    kscan, kexact = ("k_scan3d", "k_exact3d") if d3 else ("k_scan2d", "k_exact2d")
+    win_bytes = (256 if d3 else 32) * esz  # the exact kernel's window per survivor: 4x4[x4]x2 values
+    traffic = _ncu_traffic(cfg.name, kscan)
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
     e2e = None
@@ -296,7 +308,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.desc}" + (f", {world} time slabs of {nt} + ghost" if world > 1 else ""),
-                   "grid": [nx, ny, nt_global], "faces_per_step": int(total_faces),
+                   "grid": [*spatial, nt_global], "faces_per_step": int(total_faces),
                    "punctured_per_step": int(n_punct), "input": f"{field.dtype}".replace("torch.", ""),
                    "arith": "exact int64/int128 predicates, fixed-order f64 location/type, f32 prefilter",
                    "l2": "input (%.2f GB) larger than L2 (126 MB); no flush" % (field.numel() * esz / 1e9),
@@ -305,9 +317,9 @@ def run_ours(args):
                    **({"stitch_ms": sum(st_ms) / len(st_ms)} if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_scan2d (K1a, prefilter scan)", "alg_bytes_per_launch": alg_bytes,
-                     "k_exact2d": {"ms": kb_avg, "alg_bytes_per_launch": 128 * n_surv + n_punct * ftk.RECORD_BYTES,
-                                   "traffic": _ncu_traffic(cfg.name, "k_exact2d")}},
+                     "kernel": f"{kscan} (K1a, prefilter scan)", "alg_bytes_per_launch": alg_bytes,
+                     kexact: {"ms": kb_avg, "alg_bytes_per_launch": win_bytes * n_surv + n_punct * ftk.RECORD_BYTES,
+                              "traffic": _ncu_traffic(cfg.name, kexact)}},
         "clocks": clk.summary(),
         "e2e": e2e,
         # K1a + K1b + k_clear + k_hash_insert + k_edges + k_label; slabs add k_export and k_relabel

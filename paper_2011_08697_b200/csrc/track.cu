@@ -100,13 +100,11 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   const i64 ne0 = (i64)P.counters[CNT_EDGES];
   const i64 ne = ne0 < P.capacity ? ne0 : P.capacity;
   const u64 hm = table_mask(P);
-  const i64 nthreads = (i64)gridDim.x * blockDim.x;
-  const i64 tid = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  for (i64 j = tid; j < ne; j += nthreads) {
-    // consecutive edges come from one K1b batch and mostly join the same few trajectories; spread
-    // them over the threads (and time) so concurrent finds do not pile onto the same trees.
-    // j -> j p mod ne is a bijection for the prime p = 2654435761 > capacity (gcd(p, ne) = 1).
-    const i64 e = (P.diag == 2 || ne >= 2654435761ll) ? j : (i64)(((unsigned long long)j * 2654435761ull) % (unsigned long long)ne);
+  // Edges are visited in emission order (K1b batch order follows the scan: time-major runs of one
+  // region), coalesced across the threads.  Measured alternatives -- a scattered permutation, or
+  // one contiguous run per thread -- are within 15% on C2 but 3x slower on C4, where the union-find
+  // working set is far beyond L2 and the shallow trees of the in-order unions matter.
+  for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (i64)gridDim.x * blockDim.x) {
     const long long a = P.edges[2 * e];
     long long b = P.edges[2 * e + 1];
     if (b < 0) {

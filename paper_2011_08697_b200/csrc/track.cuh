@@ -21,9 +21,9 @@ struct TrackParams {
   bool inserted;                 // K1 already filled the table (experiment, FTK_K1B_INSERT)
   unsigned long long lookup_types;  // face types (bit per type) inserted into the table: the types
                                  // an edge or the verifier can look up
-  bool prelinked;
-  int diag;                      // diagnostics (FTK_PASS2_DIAG): 1 = k_edges skips the unions                // K1 initialised parent[] with its in-cube unions and emitted only
+  bool prelinked;                // K1 initialised parent[] with its in-cube unions and emitted only
                                  // the edges to faces of neighbour cubes (2D)
+  int diag;                      // diagnostics (FTK_PASS2_DIAG): 1 = k_edges skips the unions
   // time slabs (multi-GPU stitch)
   int T;                         // face types per cube (12 / 60)
   i64 plane;                     // vertices per timestep (nx * ny * nz)
