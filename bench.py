@@ -224,7 +224,7 @@ def run_ours(args):
     cptr = comm.ptr if comm is not None else None
 
     stream = torch.cuda.current_stream(dev)
-    ftk.set_profiling(True)
+    ftk.set_profiling(False)
     rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, comm=cptr, return_buffers=True)
     n_punct = rec.shape[0]
     # warmup
@@ -233,22 +233,28 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    k1_ms, p2_ms, st_ms, ka_ms, kb_ms = [], [], [], [], []
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index or 0) as clk:
         start.record(stream)
         for _ in range(args.steps):
             ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
-            ms4, st3 = ftk.last_timings()
-            km = ftk.last_kernel_timings()
-            ka_ms.append(km[0])
-            kb_ms.append(km[1])
-            k1_ms.append(ms4[0])
-            p2_ms.append(ms4[1])
-            st_ms.append(ms4[2])
         stop.record(stream)
         torch.cuda.synchronize(dev)
     ms_total = start.elapsed_time(stop)
+    # per-kernel split (CUDA events recorded by the library around each kernel on the launch stream),
+    # in a separate profiled pass so the events do not sit inside the headline timing
+    k1_ms, p2_ms, st_ms, ka_ms, kb_ms = [], [], [], [], []
+    ftk.set_profiling(True)
+    for _ in range(max(3, min(args.steps, 30))):
+        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
+        ms4, st3 = ftk.last_timings()
+        km = ftk.last_kernel_timings()
+        ka_ms.append(km[0])
+        kb_ms.append(km[1])
+        k1_ms.append(ms4[0])
+        p2_ms.append(ms4[1])
+        st_ms.append(ms4[2])
+    ftk.set_profiling(False)
     if clk.ok and len(clk.samples) < 5:
         # short timed regions: keep the GPU busy with the same step and sample again
         with ClockSampler(dev.index or 0) as clk2:

@@ -75,7 +75,11 @@ constexpr int ROWS = TY + 3;        // y0-1 .. y0+33
 #define FTK_K1_CHUNK 32
 #endif
 constexpr int CHUNK = FTK_K1_CHUNK; // window-buffer entries a scan warp reserves at a time
-constexpr int TCHUNK = 32;          // anchor timesteps per work item
+#ifndef FTK_K1_TCHUNK
+#define FTK_K1_TCHUNK 32
+#endif
+constexpr int TCHUNK = FTK_K1_TCHUNK;  // anchor timesteps per work item (halved by the launcher when
+                                       // there would be fewer than 16 items per CTA: tail balance)
 template <typename T>
 constexpr int nstage() { return sizeof(T) == 4 ? FTK_K1_NSTAGE : 3; }
 
@@ -876,7 +880,8 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
   const i64 nx = P.nx, ny = P.ny;
   constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
   const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
-  const int ntz = (int)((P.tb - P.ta + TCHUNK - 1) / TCHUNK);
+  const int tch = (int)P.tchunk;
+  const int ntz = (int)((P.tb - P.ta + tch - 1) / tch);
   const long long nitems = (long long)ntx * nty * ntz;
 
   if (tid == 0) {
@@ -911,8 +916,8 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
       if (item >= nitems) break;
       const int tx = (int)(item % ntx), ty_ = (int)((item / ntx) % nty), tz = (int)(item / ((long long)ntx * nty));
       const i64 x0 = (i64)tx * TX, y0 = (i64)ty_ * TY;
-      const i64 ta = P.ta + (i64)tz * TCHUNK;
-      const i64 tb = min(ta + TCHUNK, P.tb);
+      const i64 ta = P.ta + (i64)tz * tch;
+      const i64 tb = min(ta + tch, P.tb);
       const i64 plast = min(tb, P.nt_global - 1);
       const int np = (int)(plast - ta + 1);
       for (int k = 0; k < np; ++k, ++gk) {
@@ -1229,15 +1234,18 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   }
   const size_t smem = sizeof(ScanSmem<T>) + 128;
   auto kern = k_scan2d<T, TMA>;
-  FTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148, per_sm = 0;
-  FTK_CUDA_TRY(cudaGetDevice(&dev));
-  FTK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem));
-  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY) * ((P.tb - P.ta + TCHUNK - 1) / TCHUNK);
+  const sm100::LaunchGeom lg = sm100::launch_geom(kern, NTHREADS, smem);
+  if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan2d launch geometry");
+  const int sms = lg.sms, per_sm = lg.per_sm;
+  const long long tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
+  const long long slots = (long long)sms * std::max(per_sm, 1);
+  ExtractParams Q = P;
+  Q.tchunk = TCHUNK;
+  if (tiles * ((P.tb - P.ta + TCHUNK - 1) / TCHUNK) < 16 * slots) Q.tchunk = TCHUNK / 2;
+  const long long items = tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk);
   if (items <= 0) return FTK_OK;
-  const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
-  kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, P);
+  const long long grid = std::min<long long>(items, slots);
+  kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, Q);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
   if (P.table) {
@@ -1247,9 +1255,9 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   // K1b: persistent grid over the survivor list
   const size_t xsmem = sizeof(ExSmem<T>);
   auto xk = k_exact2d<T>;
-  FTK_CUDA_TRY(cudaFuncSetAttribute(xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
-  int xper = 0;
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, xk, EXW * 32, xsmem));
+  const sm100::LaunchGeom xg = sm100::launch_geom(xk, EXW * 32, xsmem);
+  if (xg.err != cudaSuccess) return set_cuda_error(xg.err, "k_exact2d launch geometry");
+  const int xper = xg.per_sm;
   xk<<<(unsigned)(sms * std::max(xper, 1)), EXW * 32, xsmem, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;

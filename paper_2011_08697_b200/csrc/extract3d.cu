@@ -872,11 +872,9 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   }
   const size_t smem = sizeof(Smem<T>) + 128;
   auto kern = k_scan3d<T, TMA>;
-  FTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148, per_sm = 0;
-  FTK_CUDA_TRY(cudaGetDevice(&dev));
-  FTK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads<T>(), smem));
+  const sm100::LaunchGeom lg = sm100::launch_geom(kern, nthreads<T>(), smem);
+  if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan3d launch geometry");
+  const int sms = lg.sms, per_sm = lg.per_sm;
   const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
                           ((P.tb - P.ta + TCH - 1) / TCH);
   if (items <= 0) return FTK_OK;
@@ -884,8 +882,9 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   kern<<<(unsigned)grid, nthreads<T>(), smem, stream>>>(map, P);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
-  int xper = 0;
-  FTK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, k_exact3d<T>, XW3 * 32, 0));
+  const sm100::LaunchGeom xg = sm100::launch_geom(k_exact3d<T>, XW3 * 32, 0);
+  if (xg.err != cudaSuccess) return set_cuda_error(xg.err, "k_exact3d launch geometry");
+  const int xper = xg.per_sm;
   k_exact3d<T><<<(unsigned)(sms * std::max(xper, 1)), XW3 * 32, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;

@@ -136,18 +136,17 @@ static int range_status(const ftk_desc* d, unsigned long long maxbits) {
 
 static thread_local float g_kms[4] = {0, 0, 0, 0};  // K1a, K1b, pass 2, stitch
 
-struct Events {
-  cudaEvent_t e[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // 4: between K1a and K1b
+struct Events {  // profiling events, created once per host thread and reused
+  cudaEvent_t* e = nullptr;  // 4: between K1a and K1b
   bool on = false;
   Events() {
+    thread_local cudaEvent_t pool[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (g_profiling) {
+      if (!pool[0])
+        for (auto& x : pool) cudaEventCreate(&x);
+      e = pool;
       on = true;
-      for (auto& x : e) cudaEventCreate(&x);
     }
-  }
-  ~Events() {
-    for (auto& x : e)
-      if (x) cudaEventDestroy(x);
   }
   void rec(int i, cudaStream_t s) {
     if (on) cudaEventRecord(e[i], s);
@@ -199,6 +198,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
+  if (ev.on) cudaEventRecord(ev.e[4], stream);  // a recorded default for paths that skip K1a
   ev.rec(1, stream);
   st = desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream);
   if (st) return st;

@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <unordered_map>
 
 namespace ftk {
 namespace sm100 {
@@ -178,6 +179,33 @@ inline EncodeTiledFn get_encode() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   }
   return fn;
+}
+
+// Per-thread cache of the launch geometry of a kernel on the current device: SM count and resident
+// blocks per SM (the dynamic-smem attribute is set on the first call).  Keeps the per-call host
+// overhead of the persistent launches to a lookup.
+struct LaunchGeom {
+  int sms = 0, per_sm = 0;
+  cudaError_t err = cudaSuccess;
+};
+template <typename K>
+inline LaunchGeom launch_geom(K kern, int threads, size_t smem) {
+  thread_local std::unordered_map<unsigned long long, LaunchGeom> cache;
+  int dev = 0;
+  LaunchGeom g;
+  if ((g.err = cudaGetDevice(&dev)) != cudaSuccess) return g;
+  const unsigned long long key = reinterpret_cast<unsigned long long>(reinterpret_cast<const void*>(kern)) ^
+                                 ((unsigned long long)dev << 56) ^ ((unsigned long long)smem << 40) ^ (unsigned)threads;
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024 &&
+      (g.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return g;
+  if ((g.err = cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return g;
+  if ((g.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g.per_sm, kern, threads, smem)) != cudaSuccess) return g;
+  if (g.per_sm < 1) g.per_sm = 1;
+  cache[key] = g;
+  return g;
 }
 
 }  // namespace sm100

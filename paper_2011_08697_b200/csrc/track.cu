@@ -21,6 +21,17 @@
 #include "track.cuh"
 
 namespace ftk {
+
+static int num_sms() {  // cached per host thread and device
+  thread_local int cached_dev = -1, cached = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != cached_dev) {
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    cached_dev = dev;
+  }
+  return cached;
+}
+
 namespace trk {
 
 constexpr int EMPTY = -1;
@@ -310,9 +321,7 @@ __global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) 
 
 int launch_export(const TrackParams& P, cudaStream_t stream) {
   using namespace trk;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = num_sms();
   k_export<<<sms * 4, 256, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
@@ -322,9 +331,7 @@ int launch_relabel(ftk_cp* rec, i64 n, const long long* old_labels, const long l
                    cudaStream_t stream) {
   using namespace trk;
   if (n <= 0 || nmap <= 0) return FTK_OK;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = num_sms();
   k_relabel<<<sms * 4, 256, 0, stream>>>(rec, n, old_labels, new_labels, nmap);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
@@ -332,9 +339,7 @@ int launch_relabel(ftk_cp* rec, i64 n, const long long* old_labels, const long l
 
 int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t stream) {
   using namespace trk;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = num_sms();
   const int threads = 256, blocks = sms * 8;
   if (!P.inserted) {  // 3D: K1 does not fill the table
     k_clear<<<blocks, threads, 0, stream>>>(P);
