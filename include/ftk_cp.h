@@ -168,6 +168,20 @@ FTK_API int ftk_stitch_resolve(const int64_t* A, int64_t nA, const int64_t* B, i
 FTK_API int ftk_relabel(ftk_cp* d_out, int64_t n, const int64_t* h_map_old, const int64_t* h_map_new, int64_t nmap,
                         void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream);
 
+/* Device seam path (used by ftk_cp_track with a communicator; exposed for tests and custom
+ * transports).  A packed seam block holds one slab's lists:
+ *   [0] nA, [1] nB, [2, 2 + 2 cap) A pairs, [2 + 2 cap, 2 + 4 cap) B pairs   (int64, 2 + 4 cap total).
+ * ftk_seam_pack writes this slab's block (from the workspace of its last track call) to d_block
+ * (device).  ftk_seam_resolve takes the world blocks concatenated in slab order (device, e.g. an
+ * allgather), unions every A pair's label with the B label of the same face on the device and
+ * relabels d_out[0, n) with the component minima -- labels not on any seam are unchanged.  Returns
+ * FTK_ERR_CAPACITY (nothing relabelled) when a count exceeds cap, FTK_ERR_INVARIANT when an A face
+ * has no B entry in any block.  Synchronises `stream` once (flag check). */
+FTK_API int ftk_seam_pack(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t capacity, int64_t* d_block,
+                          int64_t cap, ftk_stream stream);
+FTK_API int ftk_seam_resolve(const int64_t* d_all, int world, int64_t cap, ftk_cp* d_out, int64_t n,
+                             ftk_stream stream);
+
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);

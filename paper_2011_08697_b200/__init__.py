@@ -38,7 +38,7 @@ EXPORTS = [
     "ftk_cp_extract", "ftk_cp_track", "ftk_cp_track_host", "ftk_set_profiling", "ftk_last_timings",
     "ftk_last_kernel_timings",
     "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
-    "ftk_relabel",
+    "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
 ]
 
 
@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
         L.ftk_set_profiling.argtypes = [ctypes.c_int]
         L.ftk_last_timings.argtypes = [P, P]
         L.ftk_last_kernel_timings.argtypes = [P, ctypes.c_int]
+        L.ftk_seam_pack.argtypes = [P, P, ctypes.c_size_t, ctypes.c_int64, P, ctypes.c_int64, P]
+        L.ftk_seam_resolve.argtypes = [P, ctypes.c_int, ctypes.c_int64, P, ctypes.c_int64, P]
         L.ftk_comm_get_unique_id.argtypes = [P]
         L.ftk_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         L.ftk_comm_destroy.argtypes = [P]
@@ -283,6 +285,26 @@ def relabel(rec: torch.Tensor, old: np.ndarray, new: np.ndarray, buffers: Buffer
     _check(lib().ftk_relabel(ctypes.c_void_p(rec.data_ptr()), rec.shape[0], _np_ptr(old), _np_ptr(new), len(old),
                              ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
                              buffers.capacity, ctypes.c_void_p(_stream_ptr(rec.device))), "ftk_relabel")
+
+
+def seam_block_size(cap: int) -> int:
+    """int64 elements of one packed seam block (include/ftk_cp.h)"""
+    return 2 + 4 * cap
+
+
+def seam_pack(field: torch.Tensor, scale_log2: int, t0: int, nt_global: int, ghost: bool, buffers: Buffers,
+              block: torch.Tensor, cap: int):
+    """After track() on a slab with these buffers: write its packed seam block into `block` (device int64)."""
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost)
+    _check(lib().ftk_seam_pack(ctypes.byref(desc), ctypes.c_void_p(buffers.workspace.data_ptr()),
+                               buffers.workspace.numel(), buffers.capacity, ctypes.c_void_p(block.data_ptr()), cap,
+                               ctypes.c_void_p(_stream_ptr(block.device))), "ftk_seam_pack")
+
+
+def seam_resolve(all_blocks: torch.Tensor, world: int, cap: int, rec: torch.Tensor):
+    """Device resolve of the concatenated blocks of all slabs; relabels rec (int64 [n, 7] device view)."""
+    _check(lib().ftk_seam_resolve(ctypes.c_void_p(all_blocks.data_ptr()), world, cap, ctypes.c_void_p(rec.data_ptr()),
+                                  rec.shape[0], ctypes.c_void_p(_stream_ptr(rec.device))), "ftk_seam_resolve")
 
 
 class Comm:

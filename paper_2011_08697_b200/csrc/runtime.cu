@@ -406,6 +406,9 @@ struct ftk_comm {
   long long* d_send = nullptr;  // library-owned exchange buffers, grown on demand
   long long* d_recv = nullptr;
   size_t cap_pairs = 0;
+  long long seam_cap = 0;       // pairs per list of a packed seam block (0: not sized yet)
+  long long* d_gather = nullptr;  // world packed seam blocks (in-place allgather)
+  size_t gather_elems = 0;
 };
 
 namespace ftk {
@@ -416,9 +419,90 @@ static int nccl_check(ncclResult_t r, const char* what) {
   return FTK_ERR_NCCL;
 }
 
+// ------------------------------------------------------------------ device seam path
+// library-owned scratch of the device resolve, per host thread, grown on demand
+static int seam_scratch(int world, long long cap, SeamScratch& S) {
+  thread_local char* base = nullptr;
+  thread_local size_t bytes = 0;
+  const u64 hb = hash_slots(2 * (long long)world * cap, 1ull << 40);
+  const u64 hl = hash_slots(4 * (long long)world * cap, 1ull << 40);
+  const size_t need = hb * 16 + hl * 12 + 64;
+  if (need > bytes) {
+    if (base) cudaFree(base);
+    base = nullptr;
+    bytes = 0;
+    FTK_CUDA_TRY(cudaMalloc(&base, need));
+    bytes = need;
+  }
+  S.hb_key = reinterpret_cast<long long*>(base);
+  S.hb_val = S.hb_key + hb;
+  S.hb_mask = hb - 1;
+  S.hl_key = S.hb_val + hb;
+  S.hl_mask = hl - 1;
+  S.flags = reinterpret_cast<unsigned long long*>(S.hl_key + hl);
+  S.hl_parent = reinterpret_cast<int*>(S.flags + 2);
+  return FTK_OK;
+}
+
+static int seam_pack(void* d_ws, int64_t capacity, long long* block, long long cap, cudaStream_t s) {
+  const Layout L = layout(capacity);
+  char* ws = static_cast<char*>(d_ws);
+  TrackParams TP;
+  memset(&TP, 0, sizeof TP);
+  TP.counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  TP.exportA = reinterpret_cast<long long*>(ws + L.exportA);
+  TP.exportB = reinterpret_cast<long long*>(ws + L.exportB);
+  TP.capacity = capacity;
+  return launch_seam_pack(TP, block, cap, s);
+}
+
+// resolve all packed blocks on the device and relabel d_out; FTK_ERR_CAPACITY when a list did not fit
+// its block (nothing relabelled), FTK_ERR_INVARIANT for an A face no slab exported
+static int seam_resolve(const long long* all, int world, long long cap, ftk_cp* d_out, i64 n, cudaStream_t s) {
+  SeamScratch S;
+  int st = seam_scratch(world, cap, S);
+  if (st) return st;
+  st = launch_seam_resolve(all, world, cap, S, d_out, n, s);
+  if (st) return st;
+  unsigned long long fl[2];
+  FTK_CUDA_TRY(cudaMemcpyAsync(fl, S.flags, sizeof fl, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  if (fl[0]) return FTK_ERR_CAPACITY;
+  if (fl[1]) {
+    g_last_error = "seam faces without a partner slab: " + std::to_string(fl[1]);
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
+// Fast path: pack this slab's lists into its block of the gather buffer, one in-place NCCL allgather
+// of the fixed-size blocks, resolve and relabel on the device -- no host round trip except the final
+// flag check.  The block size is learnt from the first (host-path) call.
+static int stitch_device(ftk_comm* c, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity, cudaStream_t s) {
+  const long long stride = seam_stride(c->seam_cap);
+  const size_t need = (size_t)stride * c->world;
+  if (need > c->gather_elems) {
+    cudaFree(c->d_gather);
+    c->d_gather = nullptr;
+    c->gather_elems = 0;
+    FTK_CUDA_TRY(cudaMalloc(&c->d_gather, need * sizeof(long long)));
+    c->gather_elems = need;
+  }
+  long long* mine = c->d_gather + (size_t)c->rank * stride;
+  int st = seam_pack(d_ws, capacity, mine, c->seam_cap, s);
+  if (st) return st;
+  st = nccl_check(g_nccl.allGather(mine, c->d_gather, (size_t)stride, ncclInt64, c->comm, s), "ncclAllGather(seams)");
+  if (st) return st;
+  return seam_resolve(c->d_gather, c->world, c->seam_cap, d_out, n, s);
+}
+
 // exchange this slab's A and B lists with every slab (two allgathers over NVLink), resolve, relabel
 static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity,
                        cudaStream_t s) {
+  if (c->seam_cap > 0 && !getenv("FTK_STITCH_HOST")) {
+    const int st = stitch_device(c, d_out, n, d_ws, capacity, s);
+    if (st != FTK_ERR_CAPACITY) return st;  // else: a list outgrew the blocks; host path, resized
+  }
   std::vector<long long> A, B;
   int st = read_exports(desc, d_ws, capacity, A, B, s);
   if (st) return st;
@@ -441,6 +525,8 @@ static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, 
     maxA = std::max(maxA, counts[2 * r]);
     maxB = std::max(maxB, counts[2 * r + 1]);
   }
+  // every rank sees the same counts: size the device path's blocks for the next calls
+  c->seam_cap = ((std::max(maxA, maxB) * 3 / 2 + 1024) + 4095) / 4096 * 4096;
   const size_t per = (size_t)(maxA + maxB);  // pairs per rank, padded
   if (per > c->cap_pairs) {
     cudaFree(c->d_send);
@@ -644,6 +730,20 @@ int ftk_comm_get_unique_id(uint8_t id[128]) {
   return FTK_OK;
 }
 
+int ftk_seam_pack(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t capacity, int64_t* d_block,
+                  int64_t cap, ftk_stream stream) {
+  int st = validate(desc);
+  if (st) return st;
+  if (!d_ws || !d_block || cap < 1 || ws_bytes < layout(capacity, esz_of(desc)).total) return FTK_ERR_INVALID_ARG;
+  return seam_pack(d_ws, capacity, reinterpret_cast<long long*>(d_block), cap, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ftk_seam_resolve(const int64_t* d_all, int world, int64_t cap, ftk_cp* d_out, int64_t n, ftk_stream stream) {
+  if (!d_all || world < 1 || cap < 1 || n < 0 || (n > 0 && !d_out)) return FTK_ERR_INVALID_ARG;
+  return seam_resolve(reinterpret_cast<const long long*>(d_all), world, cap, d_out, n,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ftk_comm_init(ftk_comm** comm, int rank, int world, const uint8_t id[128]) {
   if (!comm || !id || world < 1 || rank < 0 || rank >= world) return FTK_ERR_INVALID_ARG;
   if (!g_nccl.load()) return FTK_ERR_NCCL;
@@ -666,6 +766,7 @@ int ftk_comm_destroy(ftk_comm* comm) {
   if (comm->comm && g_nccl.commDestroy) g_nccl.commDestroy(comm->comm);
   cudaFree(comm->d_send);
   cudaFree(comm->d_recv);
+  cudaFree(comm->d_gather);
   delete comm;
   return FTK_OK;
 }

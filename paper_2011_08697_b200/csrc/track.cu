@@ -187,6 +187,145 @@ __global__ void k_relabel(ftk_cp* rec, i64 n, const long long* old_l, const long
   }
 }
 
+// ------------------------------------------------------------------------- device seam resolve
+__global__ void k_seam_pack(const __grid_constant__ TrackParams P, long long* block, long long cap) {
+  const i64 nA = (i64)P.counters[CNT_CROSS], nB = (i64)P.counters[CNT_EXPORT_B];
+  const i64 stride = (i64)gridDim.x * blockDim.x, i0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i0 == 0) {
+    block[0] = nA;
+    block[1] = nB;
+  }
+  const i64 mA = min(nA, (i64)cap), mB = min(nB, (i64)cap);
+  for (i64 i = i0; i < mA; i += stride) {
+    block[2 + 2 * i] = P.exportA[2 * i];
+    block[3 + 2 * i] = P.exportA[2 * i + 1];
+  }
+  for (i64 i = i0; i < mB; i += stride) {
+    block[2 + 2 * cap + 2 * i] = P.exportB[2 * i];
+    block[3 + 2 * cap + 2 * i] = P.exportB[2 * i + 1];
+  }
+}
+
+struct SeamArgs {
+  const long long* all;
+  int world;
+  long long cap;
+  SeamScratch S;
+  ftk_cp* rec;
+  long long n;
+};
+
+__global__ void k_seam_clear(const __grid_constant__ SeamArgs A) {
+  const u64 stride = (u64)gridDim.x * blockDim.x, i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (u64 i = i0; i <= A.S.hb_mask; i += stride) A.S.hb_key[i] = -1;
+  for (u64 i = i0; i <= A.S.hl_mask; i += stride) {
+    A.S.hl_key[i] = -1;
+    A.S.hl_parent[i] = (int)i;
+  }
+  if (i0 < 2) A.S.flags[i0] = 0;
+}
+
+__device__ __forceinline__ int hl_insert(const SeamScratch& S, long long label) {
+  u64 h = hash_mix((u64)label) & S.hl_mask;
+  while (true) {
+    const long long prev = (long long)atomicCAS(reinterpret_cast<unsigned long long*>(&S.hl_key[h]), ~0ull,
+                                                (unsigned long long)label);
+    if (prev == -1 || prev == label) return (int)h;
+    h = (h + 1) & S.hl_mask;
+  }
+}
+__device__ __forceinline__ int hl_find(const SeamScratch& S, long long label) {
+  u64 h = hash_mix((u64)label) & S.hl_mask;
+  while (true) {
+    const long long k = S.hl_key[h];
+    if (k == label) return (int)h;
+    if (k == -1) return -1;
+    h = (h + 1) & S.hl_mask;
+  }
+}
+
+// B faces into the face table, every label of A and B into the label table
+__global__ void k_seam_insert(const __grid_constant__ SeamArgs A) {
+  const i64 stride = (i64)gridDim.x * blockDim.x, i0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long bs = seam_stride(A.cap);
+  for (int r = 0; r < A.world; ++r) {
+    const long long* blk = A.all + r * bs;
+    const i64 nA = blk[0], nB = blk[1];
+    if ((nA > A.cap || nB > A.cap) && i0 == 0) A.S.flags[0] = 1;
+    const i64 mA = min(nA, (i64)A.cap), mB = min(nB, (i64)A.cap);
+    for (i64 i = i0; i < mB; i += stride) {
+      const long long f = blk[2 + 2 * A.cap + 2 * i], l = blk[3 + 2 * A.cap + 2 * i];
+      u64 h = hash_mix((u64)f) & A.S.hb_mask;
+      while (atomicCAS(reinterpret_cast<unsigned long long*>(&A.S.hb_key[h]), ~0ull, (unsigned long long)f) != ~0ull)
+        h = (h + 1) & A.S.hb_mask;  // face ids are unique among the B lists
+      A.S.hb_val[h] = l;
+      hl_insert(A.S, l);
+    }
+    for (i64 i = i0; i < mA; i += stride) hl_insert(A.S, blk[3 + 2 * i]);
+  }
+}
+
+__device__ __forceinline__ int seam_find(int* parent, int i) {
+  while (true) {
+    const int p = parent[i];
+    if (p == i) return i;
+    const int gp = parent[p];
+    if (gp != p) parent[i] = gp;
+    i = p;
+  }
+}
+
+// every A pair joins its label with the B label of the same face (hook the larger label's root
+// under the smaller: roots end up as component minima)
+__global__ void k_seam_union(const __grid_constant__ SeamArgs A) {
+  const i64 stride = (i64)gridDim.x * blockDim.x, i0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long bs = seam_stride(A.cap);
+  for (int r = 0; r < A.world; ++r) {
+    const long long* blk = A.all + r * bs;
+    const i64 mA = min(blk[0], (i64)A.cap);
+    for (i64 i = i0; i < mA; i += stride) {
+      const long long f = blk[2 + 2 * i], la = blk[3 + 2 * i];
+      u64 h = hash_mix((u64)f) & A.S.hb_mask;
+      long long lb = -1;
+      while (true) {
+        const long long k = A.S.hb_key[h];
+        if (k == f) {
+          lb = A.S.hb_val[h];
+          break;
+        }
+        if (k == -1) break;
+        h = (h + 1) & A.S.hb_mask;
+      }
+      if (lb < 0) {
+        atomicAdd(&A.S.flags[1], 1ull);
+        continue;
+      }
+      int a = hl_find(A.S, la), b = hl_find(A.S, lb);
+      while (true) {
+        a = seam_find(A.S.hl_parent, a);
+        b = seam_find(A.S.hl_parent, b);
+        if (a == b) break;
+        if (A.S.hl_key[a] < A.S.hl_key[b]) {
+          const int t = a;
+          a = b;
+          b = t;
+        }
+        if (atomicCAS(&A.S.hl_parent[a], a, b) == a) break;
+      }
+    }
+  }
+}
+
+// records whose label is on a seam take the label of its component root
+__global__ void k_seam_relabel(const __grid_constant__ SeamArgs A) {
+  if (A.S.flags[0]) return;  // a list overflowed its block: the caller takes the host path
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const long long l = A.rec[i].label;
+    const int node = hl_find(A.S, l);
+    if (node >= 0) A.rec[i].label = A.S.hl_key[seam_find(A.S.hl_parent, node)];
+  }
+}
+
 // ------------------------------------------------------------------------- closed-form verifier
 template <int D>
 struct Geo {
@@ -365,6 +504,29 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
     }
     FTK_CUDA_TRY(cudaGetLastError());
   }
+  return FTK_OK;
+}
+
+int launch_seam_pack(const TrackParams& P, long long* block, long long cap, cudaStream_t stream) {
+  using namespace trk;
+  k_seam_pack<<<num_sms() * 2, 256, 0, stream>>>(P, block, cap);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+int launch_seam_resolve(const long long* all, int world, long long cap, const SeamScratch& S, ftk_cp* d_out,
+                        long long n, cudaStream_t stream) {
+  using namespace trk;
+  SeamArgs A{all, world, cap, S, d_out, n};
+  const int blocks = num_sms() * 2;
+  k_seam_clear<<<blocks, 256, 0, stream>>>(A);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_seam_insert<<<blocks, 256, 0, stream>>>(A);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_seam_union<<<blocks, 256, 0, stream>>>(A);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_seam_relabel<<<num_sms() * 4, 256, 0, stream>>>(A);
+  FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }
 

@@ -43,3 +43,30 @@ int launch_export(const TrackParams& P, cudaStream_t stream);
 int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t stream);
 
 }  // namespace ftk
+
+namespace ftk {
+
+// Device-side seam resolve for time slabs (no host round trip).  A packed seam block per slab:
+//   [0] nA, [1] nB, [2 .. 2 + 2 cap) A pairs (ghost-plane face id, local label),
+//   [2 + 2 cap .. 2 + 4 cap) B pairs (first-plane ordinal face id, local label);
+// the blocks of all slabs are concatenated (NCCL allgather), every rank resolves all of them the
+// same way and relabels its own records.
+__host__ __device__ inline long long seam_stride(long long cap) { return 2 + 4 * cap; }
+
+struct SeamScratch {            // library-owned, sized for world * cap pairs per list
+  long long* hb_key;            // face id -> B label table (open addressing, -1 empty)
+  long long* hb_val;
+  unsigned long long hb_mask;
+  long long* hl_key;            // label -> node table; the node is the slot, parent per slot
+  int* hl_parent;
+  unsigned long long hl_mask;
+  unsigned long long* flags;    // [0] overflow (a slab's list exceeded cap), [1] unmatched A pairs
+};
+
+// pack this slab's lists (from the workspace after k_export) into its seam block
+int launch_seam_pack(const TrackParams& P, long long* block, long long cap, cudaStream_t stream);
+// resolve all blocks and relabel d_out[0, n) (labels not on any seam are unchanged)
+int launch_seam_resolve(const long long* all, int world, long long cap, const SeamScratch& S, ftk_cp* d_out,
+                        long long n, cudaStream_t stream);
+
+}  // namespace ftk

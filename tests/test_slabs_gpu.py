@@ -84,3 +84,47 @@ def test_nccl_communicator_single_rank(ftk):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def run_slabs_device(ftk, field_cpu, s, G, cap=4096):
+    """the device seam path: packed blocks concatenated (standing in for the NCCL allgather), resolved
+    and relabelled on the GPU by every slab"""
+    nt = field_cpu.shape[0]
+    b = ftk.slab_bounds(nt, G)
+    stride = ftk.seam_block_size(cap)
+    blocks = torch.full((G * stride,), -7, dtype=torch.int64, device="cuda")
+    parts = []
+    for r in range(G):
+        ghost = r < G - 1
+        sub = field_cpu[b[r]: b[r + 1] + (1 if ghost else 0)].contiguous().cuda()
+        rec, buf = ftk.track(sub, s, t0=b[r], nt_global=nt, ghost=ghost, return_buffers=True)
+        ftk.seam_pack(sub, s, b[r], nt, ghost, buf, blocks[r * stride:(r + 1) * stride], cap)
+        parts.append(rec)
+    out = []
+    for rec in parts:
+        ftk.seam_resolve(blocks, G, cap, rec)
+        out.append(ftk.to_numpy(rec))
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_device_seam_resolve_matches_single_domain(ftk, oracle_lib, G):
+    w = fi.Woven(96, 80, 29, sigma=0.02)
+    f = w.generate()
+    got = _sorted(run_slabs_device(ftk, f, 26, G))
+    ref, _, _ = oracle_lib.track(f.numpy(), 26)
+    ref = _sorted(ref)
+    assert np.array_equal(got["face_id"], ref["face_id"]) and np.array_equal(got["label"], ref["label"])
+
+
+def test_device_seam_resolve_3d_and_overflow(ftk, oracle_lib):
+    w = fi.Woven(23, 21, 9, L=15.0, sigma=0.02, nz=19)
+    f = w.generate()
+    got = _sorted(run_slabs_device(ftk, f, 26, 3))
+    ref, _, _ = oracle_lib.track(f.numpy(), 26)
+    ref = _sorted(ref)
+    assert np.array_equal(got["face_id"], ref["face_id"]) and np.array_equal(got["label"], ref["label"])
+    # a block too small for a slab's list: FTK_ERR_CAPACITY and nothing relabelled
+    with pytest.raises(ftk.FtkError) as e:
+        run_slabs_device(ftk, fi.Woven(96, 80, 29, sigma=0.02).generate(), 26, 2, cap=2)
+    assert e.value.status == ftk.ERR_CAPACITY
