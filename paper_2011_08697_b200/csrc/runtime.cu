@@ -243,7 +243,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
                            "exact_records", "producer_wait", "other"};
     fprintf(stderr, "K1 cycle accounting (sum over warps, Gcycles):");
     for (int i = 0; i < 10; ++i) fprintf(stderr, " %s=%.3f", names[i], host_cnt[CNT_PROF + i] * 1e-9);
-    fprintf(stderr, " edges=%llu\n", host_cnt[CNT_EDGES]);
+    fprintf(stderr, " edges=%llu find_steps=%llu cas_retries=%llu\n", host_cnt[CNT_EDGES], host_cnt[30], host_cnt[31]);
   }
   if (ev.on) {
     cudaEventElapsedTime(&g_ms[0], ev.e[1], ev.e[2]);

@@ -106,6 +106,17 @@ __device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int
   }
 }
 
+__device__ __forceinline__ int uf_find_count(int* parent, int i, unsigned long long& steps) {
+  while (true) {
+    const int p = parent[i];
+    ++steps;
+    if (p == i) return i;
+    const int gp = parent[p];
+    if (gp != p) parent[i] = gp;
+    i = p;
+  }
+}
+
 __global__ void k_edges(const __grid_constant__ TrackParams P) {
   const i64 nrec = n_records(P);
   const i64 ne0 = (i64)P.counters[CNT_EDGES];
@@ -136,6 +147,21 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
       continue;
     }
     if (P.diag == 1) continue;  // diagnostics: lookups only
+    if (P.diag == 3) {  // diagnostics: count find steps and CAS retries (counters 30, 31)
+      unsigned long long steps = 0, retries = 0;
+      int ra = (int)a, rb = (int)b;
+      while (true) {
+        ra = uf_find_count(P.parent, ra, steps);
+        rb = uf_find_count(P.parent, rb, steps);
+        if (ra == rb) break;
+        if (P.fid[ra] < P.fid[rb]) { const int t = ra; ra = rb; rb = t; }
+        if (atomicCAS(&P.parent[ra], ra, rb) == ra) break;
+        ++retries;
+      }
+      atomicAdd(&P.counters[30], steps);
+      atomicAdd(&P.counters[31], retries);
+      continue;
+    }
     uf_unite(P.parent, P.fid, (int)a, (int)b);
   }
 }

@@ -5,9 +5,7 @@ from paper_2011_08697_b200 import build as b
 VARIANTS = {
     "base": [],
     "prof": ["FTK_K1_PROF=1"],
-    "tc16": ["FTK_K1_TCHUNK=16"],
-    "tc64": ["FTK_K1_TCHUNK=64"],
-    "tc8": ["FTK_K1_TCHUNK=8"],
+    "mixhash": ["FTK_LOCAL_HASH=0"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
