@@ -801,7 +801,8 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
     }
     if (k >= 1) {
       const uint32_t Y = Cprev & C;                             // y-pair
-      const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0 = byte 0
+      uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
+      if (c.lane == 31) nb = 0xF0u;  // beyond the tile: AND-neutral
       Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));                 // x-pair
     }
     Cprev = C;
@@ -860,7 +861,8 @@ __device__ __forceinline__ void scan_plane_f64(const double* S, const ScanCtx& c
 #pragma unroll
   for (int k = 0; k < RW; ++k) {
     const uint32_t Y = C[k] & C[k + 1];
-    const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+    uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
+    if (c.lane == 31) nb = 0xF0u;  // beyond the tile: AND-neutral
     Sq[k] = Y & ((Y >> 8) | (nb << 24));
   }
 }
@@ -879,7 +881,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
 
   const i64 nx = P.nx, ny = P.ny;
   constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
-  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
+  const int ntx = (int)x_tiles(nx), nty = (int)((ny + TY - 1) / TY);
   const int tch = (int)P.tchunk;
   const int ntz = (int)((P.tb - P.ta + tch - 1) / tch);
   const long long nitems = (long long)ntx * nty * ntz;
@@ -1011,7 +1013,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
 
     int gk = 0;
     int x0 = -1, y0 = -1;
-    bool edge = false;
+    bool edge = false, last_x = false;
     ScanCtx sc;
     sc.srow0 = srow0;
     sc.lane = lane;
@@ -1034,6 +1036,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
         const i64 gx = (i64)x0 + 4 * lane;
         sc.gy0 = (i64)y0 + sw * RW;
         edge = x0 < 1 || x0 + LX + 1 > nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
+        last_x = x0 + LX >= nx;
         sc.lpat = gx == 0;
         sc.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
         sc.xmask = 0;
@@ -1060,7 +1063,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
         uint32_t mask = 0;
 #pragma unroll
         for (int r = 0; r < RW; ++r) mask |= (((K[r] - 0x01010101u) & ~K[r] & 0x80808080u) >> (7 - r));
-        return lane == 31 ? 0u : mask;  // the halo lane owns no anchors
+        return (lane == 31 && !last_x) ? 0u : mask;  // the halo lane owns no anchors (but in the last x tile)
       };
       // pass 0: anchors at p-1 (cube = planes p-1, p); pass 1: anchors on the last timestep (no
       // t+1 corners: the AND runs over the plane only)
@@ -1237,7 +1240,7 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   const sm100::LaunchGeom lg = sm100::launch_geom(kern, NTHREADS, smem);
   if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan2d launch geometry");
   const int sms = lg.sms, per_sm = lg.per_sm;
-  const long long tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
+  const long long tiles = x_tiles(P.nx) * ((P.ny + TY - 1) / TY);
   const long long slots = (long long)sms * std::max(per_sm, 1);
   ExtractParams Q = P;
   Q.tchunk = TCHUNK;

@@ -384,7 +384,8 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       }
       if (k >= 1) {
         const uint32_t Y = Cprev & C;
-        const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+        uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
+        if (c.lane == 31) nb = 0xFCu;  // beyond the tile: AND-neutral
         Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
       }
       Cprev = C;
@@ -438,7 +439,8 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       const uint32_t C = (EDGE && (gy >= c.ny || zout)) ? NEUTRAL : (EDGE ? (W | c.oob) : W);
       if (k >= 1) {
         const uint32_t Y = Cprev & C;
-        const uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+        uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
+        if (c.lane == 31) nb = 0xFCu;  // beyond the tile: AND-neutral
         Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
       }
       Cprev = C;
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const i64 nx = P.nx, ny = P.ny, nz = P.nz;
   constexpr uint32_t STAGE_BYTES = PITCH * ROWS * SL * sizeof(T);
-  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
+  const int ntx = (int)x_tiles(nx), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
   const int ntc = (int)((P.tb - P.ta + TCH - 1) / TCH);
   const long long nitems = (long long)ntx * nty * ntz * ntc;
   if (tid == 0) {
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     c.ny = ny;
     c.nz = nz;
     int gk = 0, x0 = 0, y0 = 0, z0 = 0;
-    bool edge = false;
+    bool edge = false, last_x = false;
     while (true) {
       const int s = gk % NSTAGE;
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
@@ -600,6 +602,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
         for (int i = 0; i < 4; ++i)
           if (gx + i >= nx) c.oob |= 0xFCu << (8 * i);
         edge = x0 < 1 || x0 + LX + 1 > nx || y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
+        last_x = x0 + LX >= nx;
       }
       const T* S = sm.plane[s] + (warp + 1) * (PITCH * ROWS);  // slice z0 + warp
       uint32_t Sq[RW];
@@ -619,7 +622,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
           uint32_t mask = 0;
 #pragma unroll
           for (int r = 0; r < RW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
-          return lane == 31 ? 0u : mask;
+          return (lane == 31 && !last_x) ? 0u : mask;
         };
         const bool inz = z0 + warp < nz;
         const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
@@ -875,7 +878,7 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   const sm100::LaunchGeom lg = sm100::launch_geom(kern, nthreads<T>(), smem);
   if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan3d launch geometry");
   const int sms = lg.sms, per_sm = lg.per_sm;
-  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
+  const long long items = x_tiles(P.nx) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
                           ((P.tb - P.ta + TCH - 1) / TCH);
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));

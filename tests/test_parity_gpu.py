@@ -255,3 +255,16 @@ def test_range_error_anywhere_3d(ftk, where):
     with pytest.raises(ftk.FtkError) as e:
         ftk.track(f.cuda(), 26)
     assert e.value.status == ftk.ERR_RANGE
+
+
+@pytest.mark.parametrize("nx", [124, 125, 127, 128, 129, 248, 252, 253, 256])
+def test_x_tile_boundaries_2d(ftk, oracle_lib, nx):
+    """widths around the 124-column tiles and the full-width last tile"""
+    w = fi.Woven(nx, 70, 6, sigma=0.02)
+    run_pair(ftk, oracle_lib, w.generate(), 26)
+
+
+@pytest.mark.parametrize("nx", [124, 128, 129, 133])
+def test_x_tile_boundaries_3d(ftk, oracle_lib, nx):
+    w = fi.Woven(nx, 9, 3, L=15.0, sigma=0.02, nz=10)
+    run_pair(ftk, oracle_lib, w.generate(), 26)
