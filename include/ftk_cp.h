@@ -110,7 +110,8 @@ FTK_API const char* ftk_last_error(void);
  * classifies; used for the faces/s metric.  Host-only arithmetic. */
 FTK_API int ftk_num_faces(const ftk_desc* desc, int64_t* n_faces);
 
-/* Device workspace needed by extract/track for up to `capacity` records.  It includes (2D) a
+/* Device workspace needed by extract/track for up to `capacity` records (0 <= capacity < 2^31 - 1,
+ * else FTK_ERR_INVALID_ARG).  It includes (2D) a
  * list of max(1024, capacity) prefilter-surviving cubes, handed from the scan kernel to the exact
  * kernel. */
 FTK_API int ftk_workspace_size(const ftk_desc* desc, int64_t capacity, size_t* bytes);

@@ -138,8 +138,11 @@ def _check(status: int, what: str):
         raise FtkError(status, what, lib().ftk_last_error().decode())
 
 
+MAX_CAPACITY = (1 << 31) - 2  # int32 record slots (include/ftk_cp.h)
+
+
 def default_capacity(field: torch.Tensor) -> int:
-    return max(1 << 16, field.numel() // 64)
+    return min(MAX_CAPACITY, max(1 << 16, field.numel() // 64))
 
 
 @dataclass
@@ -179,7 +182,9 @@ def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global,
             args.append(comm)
         st = getattr(lib(), fn_name)(*args)
         if st == ERR_CAPACITY:
-            cap = int(n_out.value * 1.25) + 1024
+            if cap >= MAX_CAPACITY:
+                _check(st, fn_name)
+            cap = min(MAX_CAPACITY, int(n_out.value * 1.25) + 1024)
             buffers = None
             continue
         _check(st, fn_name)

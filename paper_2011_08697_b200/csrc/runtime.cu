@@ -80,6 +80,9 @@ static Layout layout(i64 capacity, int esz = 8) {
   return L;
 }
 
+// record slots, union-find parents and hash slots are int32: capacity stays below 2^31 - 1
+static constexpr int64_t kMaxCapacity = (1ll << 31) - 2;
+
 static int esz_of(const ftk_desc* d) { return d->dtype == FTK_F32 ? 4 : 8; }
 
 // Face types an edge can look up: the upper face of a cell, seen from the neighbour cube that owns
@@ -157,7 +160,8 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
                void* d_ws, size_t ws_bytes, cudaStream_t stream, bool track) {
   int st = validate(desc);
   if (st) return st;
-  if (!d_field || !n_out || !d_ws || capacity < 0 || (capacity > 0 && !d_out)) return FTK_ERR_INVALID_ARG;
+  if (!d_field || !n_out || !d_ws || capacity < 0 || capacity > kMaxCapacity || (capacity > 0 && !d_out))
+    return FTK_ERR_INVALID_ARG;
   const Layout L = layout(capacity, esz_of(desc));
   if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
   char* ws = static_cast<char*>(d_ws);
@@ -615,7 +619,7 @@ int ftk_num_faces(const ftk_desc* d, int64_t* n_faces) {
 int ftk_workspace_size(const ftk_desc* d, int64_t capacity, size_t* bytes) {
   int st = validate(d);
   if (st) return st;
-  if (!bytes || capacity < 0) return FTK_ERR_INVALID_ARG;
+  if (!bytes || capacity < 0 || capacity > kMaxCapacity) return FTK_ERR_INVALID_ARG;
   *bytes = layout(capacity, esz_of(d)).total;
   return FTK_OK;
 }

@@ -6,6 +6,7 @@ import os
 import re
 
 import numpy as np
+import torch
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -109,3 +110,14 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "ftk_oracle" not in src, f
+
+
+def test_capacity_bounds(ftk):
+    """record slots are int32: capacities at or beyond 2^31 - 1 are rejected on the host"""
+    L = ftk.lib()
+    desc = ftk.make_desc((4, 8, 8), np.float32, 0)
+    b = ctypes.c_size_t(0)
+    assert L.ftk_workspace_size(ctypes.byref(desc), ftk.MAX_CAPACITY, ctypes.byref(b)) == ftk.OK
+    assert L.ftk_workspace_size(ctypes.byref(desc), ftk.MAX_CAPACITY + 1, ctypes.byref(b)) == ftk.ERR_INVALID_ARG
+    assert L.ftk_workspace_size(ctypes.byref(desc), -1, ctypes.byref(b)) == ftk.ERR_INVALID_ARG
+    assert ftk.default_capacity(torch.empty(0)) == 1 << 16
