@@ -26,8 +26,9 @@ enum Counter : int {
   CNT_EDGES = 6,      // trajectory-graph edges emitted by K1 (one per cell holding two punctured faces)
   CNT_CROSS = 7,      // slab stitch: edges whose partner face lies on the ghost plane
   CNT_EXPORT_B = 8,   // slab stitch: own ordinal faces on the first owned plane
-  CNT_WIN = 9,        // 2D K1a: survivor-list entries reserved (chunks of FTK_K1_CHUNK; may exceed wcap)
+  CNT_WIN = 9,        // K1a: survivor-list entries reserved (2D: group entries; chunks of FTK_K1_CHUNK; may exceed wcap)
   CNT_HMASK = 10,     // pass 2: hash-table slot mask in use (set before the first insert)
+  CNT_CUBES = 11,     // 2D: surviving cubes expanded from K1a's group entries (may exceed wcap)
   CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
   CNT_N = 32
 };

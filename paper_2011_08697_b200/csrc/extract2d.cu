@@ -51,8 +51,9 @@ using namespace sm100;
 // Geometry and roles
 // ---------------------------------------------------------------------------------------------
 constexpr int LX = 128;             // x positions scanned per warp row (32 lanes x 4)
-constexpr int TX = 124;             // anchors owned per tile in x: lane 31 is a halo lane whose codes
-                                    // only complete lane 30's cubes (a cube needs its x+1 corners)
+constexpr int TX = LX;              // anchors owned per tile in x: all 128 columns; lane 31's cubes take
+                                    // their x + 1 corners from the codes of column x0 + 128, computed once
+                                    // per plane (one row per lane)
 #ifndef FTK_K1_RW
 #define FTK_K1_RW 8
 #endif
@@ -715,6 +716,8 @@ struct ScanCtx {
   int lane;
   int rpos;        // position (0..3) of x = nx - 1 in this lane, else -1
   bool lpat;       // x = 0 is this lane's position 0
+  bool xe_out;     // column x0 + 128 is outside the grid
+  bool xe_last;    // column x0 + 128 is x = nx - 1
   uint32_t xmask;  // top-nibble mask of the lane's in-grid positions (0xF0 per in-grid byte)
   long long gy0;   // global y of the warp's first anchor row
   long long ny;
@@ -781,6 +784,31 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
       if (c.rpos == 3) r = v.w;
     }
   };
+  // codes of column x0 + 128 (the next tile's first column; they complete lane 31's cubes): lane k
+  // computes code row k (centre smem row srow0 + k), Ye = the y-pair of code rows k, k + 1
+  uint32_t Ye;
+  {
+    const int k = min(c.lane, RW);
+    const float* p = S + (c.srow0 + k) * PITCH + XOFF + LX;
+    const float ctr = p[0], l = p[-1];
+    float r = p[1], u = p[-PITCH], d = p[PITCH];
+    bool out = false;
+    if (EDGE) {
+      const long long gy = c.gy0 + k;
+      if (c.xe_last) r = ctr;
+      if (gy == 0) u = ctr;
+      if (gy == c.ny - 1) d = ctr;
+      out = c.xe_out || gy >= c.ny;
+    }
+    const float thr = __uint_as_float(lo32(thr2));
+    const float dx = __fsub_rn(r, l), dy = __fsub_rn(d, u);
+    const uint32_t ce = out ? 0xF0u
+                            : ((__float_as_uint(__fsub_rn(thr, dx)) >> 31) << 7) |
+                                  ((__float_as_uint(__fadd_rn(dx, thr)) >> 31) << 6) |
+                                  ((__float_as_uint(__fsub_rn(thr, dy)) >> 31) << 5) |
+                                  ((__float_as_uint(__fadd_rn(dy, thr)) >> 31) << 4);
+    Ye = ce & __shfl_down_sync(0xffffffffu, ce, 1);
+  }
   float4 v0, v1, v2;
   float l0, r0, l1, r1, l2, r2;
   load(0, v0, l0, r0);
@@ -802,7 +830,8 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
     if (k >= 1) {
       const uint32_t Y = Cprev & C;                             // y-pair
       uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
-      if (c.lane == 31) nb = 0xF0u;  // beyond the tile: AND-neutral
+      const uint32_t ne = __shfl_sync(0xffffffffu, Ye, k - 1);  // column x0 + 128
+      if (c.lane == 31) nb = ne;
       Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));                 // x-pair
     }
     Cprev = C;
@@ -844,6 +873,25 @@ __device__ __forceinline__ void scan_plane_f64(const double* S, const ScanCtx& c
       const double a = fabs(f[i][q]);
       maxd = (a != a || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, a);
     }
+  // codes of column x0 + 128 (as in scan_plane_f32)
+  uint32_t Ye;
+  {
+    const int k = min(c.lane, RW);
+    const double* p = S + (c.srow0 + k) * PITCH + XOFF + LX;
+    const double ctr = p[0], l = p[-1];
+    double r = p[1], u = p[-PITCH], d = p[PITCH];
+    bool out = false;
+    if (EDGE) {
+      const long long gy = c.gy0 + k;
+      if (c.xe_last) r = ctr;
+      if (gy == 0) u = ctr;
+      if (gy == c.ny - 1) d = ctr;
+      out = c.xe_out || gy >= c.ny;
+    }
+    const double dx = r - l, dy = d - u;
+    const uint32_t ce = out ? 0xF0u : (sbit(thr - dx) << 7) | (sbit(dx + thr) << 6) | (sbit(thr - dy) << 5) | (sbit(dy + thr) << 4);
+    Ye = ce & __shfl_down_sync(0xffffffffu, ce, 1);
+  }
   uint32_t C[RW + 1];
 #pragma unroll
   for (int k = 0; k <= RW; ++k) {
@@ -862,7 +910,8 @@ __device__ __forceinline__ void scan_plane_f64(const double* S, const ScanCtx& c
   for (int k = 0; k < RW; ++k) {
     const uint32_t Y = C[k] & C[k + 1];
     uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
-    if (c.lane == 31) nb = 0xF0u;  // beyond the tile: AND-neutral
+    const uint32_t ne = __shfl_sync(0xffffffffu, Ye, k);  // column x0 + 128
+    if (c.lane == 31) nb = ne;
     Sq[k] = Y & ((Y >> 8) | (nb << 24));
   }
 }
@@ -881,7 +930,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
 
   const i64 nx = P.nx, ny = P.ny;
   constexpr uint32_t STAGE_BYTES = ROWS * PITCH * sizeof(T);
-  const int ntx = (int)x_tiles(nx), nty = (int)((ny + TY - 1) / TY);
+  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + TY - 1) / TY);
   const int tch = (int)P.tchunk;
   const int ntz = (int)((P.tb - P.ta + tch - 1) / tch);
   const long long nitems = (long long)ntx * nty * ntz;
@@ -975,51 +1024,49 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
     // the warp's current chunk of the window buffer: entries [cur, end)
     long long cur = 0, end = 0;
 
-    // Hand the survivors (bit 8i + r <-> position i, anchor row r) to K1b: their anchors go into the
-    // window buffer (K1b fetches the windows from the field), in chunks of CHUNK entries reserved
-    // with one global atomic per warp and chunk.
+    // Hand the survivors to K1b as group entries: one per lane with surviving cubes, holding the
+    // lane's first anchor (x0 + 4 lane, first anchor row of the warp), the plane flag and the lane's
+    // 32-bit survivor mask (bit 8i + r <-> position i, anchor row r); K1b expands the masks and
+    // fetches the cube windows from the field.  Entries are reserved in chunks of CHUNK with one
+    // global atomic per warp and chunk.
+    const uint32_t lt_mask = (1u << lane) - 1u;
     auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0) {
-      while (__any_sync(0xffffffffu, mask != 0)) {
-        if (cur == end) {
-          long long c = 0;
-          if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
-          cur = __shfl_sync(0xffffffffu, c, 0);
-          end = cur + CHUNK;
-        }
-        const int cnt = __popc(mask);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int n = (int)min((long long)total, end - cur);
-        int r = incl - cnt;
-        while (mask && r < n) {
-          const int bb = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const long long e = cur + r++;
-          if (e < P.wcap) {
-            P.wx[e] = x0 + 4 * lane + (bb >> 3);
-            P.wy[e] = y0 + sw * RW + (bb & 7);
-            P.wt[e] = tflag;
-          }
-        }
+      const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
+      if (bal == 0u) return;
+      const int n = __popc(bal), rank = __popc(bal & lt_mask);
+      const int avail = (int)(end - cur);
+      long long e = cur + rank;
+      if (n > avail) {  // the chunk runs out: the rest goes to a fresh chunk (n <= 32 = CHUNK)
+        long long c = 0;
+        if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (rank >= avail) e = c + (rank - avail);
+        cur = c + (n - avail);
+        end = c + CHUNK;
+      } else {
         cur += n;
-        mysurv += n;
       }
+      if (mask != 0u && e < P.wcap) {
+        P.wx[e] = x0 + 4 * lane;
+        P.wy[e] = y0 + sw * RW;
+        P.wt[e] = tflag;
+        P.wz[e] = (int)mask;
+      }
+      mysurv += __popc(mask);
     };
+    static_assert(CHUNK >= 32, "one fresh chunk must hold a whole warp's group entries");
 
     int gk = 0;
     int x0 = -1, y0 = -1;
-    bool edge = false, last_x = false;
+    bool edge = false;
     ScanCtx sc;
     sc.srow0 = srow0;
     sc.lane = lane;
     sc.ny = ny;
     sc.rpos = -1;
     sc.lpat = false;
+    sc.xe_out = false;
+    sc.xe_last = false;
     sc.xmask = 0xF0F0F0F0u;
     sc.gy0 = 0;
     while (true) {
@@ -1035,8 +1082,9 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
         y0 = m.y0;
         const i64 gx = (i64)x0 + 4 * lane;
         sc.gy0 = (i64)y0 + sw * RW;
-        edge = x0 < 1 || x0 + LX + 1 > nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
-        last_x = x0 + LX >= nx;
+        edge = x0 < 1 || x0 + LX + 2 > nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
+        sc.xe_out = x0 + LX >= nx;
+        sc.xe_last = x0 + LX == nx - 1;
         sc.lpat = gx == 0;
         sc.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
         sc.xmask = 0;
@@ -1063,7 +1111,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
         uint32_t mask = 0;
 #pragma unroll
         for (int r = 0; r < RW; ++r) mask |= (((K[r] - 0x01010101u) & ~K[r] & 0x80808080u) >> (7 - r));
-        return (lane == 31 && !last_x) ? 0u : mask;  // the halo lane owns no anchors (but in the last x tile)
+        return mask;
       };
       // pass 0: anchors at p-1 (cube = planes p-1, p); pass 1: anchors on the last timestep (no
       // t+1 corners: the AND runs over the plane only)
@@ -1082,11 +1130,12 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
     }
     // the unused rest of the warp's chunk holds no cube
     for (long long e = cur + lane; e < end; e += 32)
-      if (e < P.wcap) P.wt[e] = -1;
+      if (e < P.wcap) P.wz[e] = 0;
 
     // statistics
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
+      mysurv += __shfl_xor_sync(0xffffffffu, mysurv, o);  // survivors were counted per lane
       maxb32 = max(maxb32, __shfl_xor_sync(0xffffffffu, maxb32, o));
       const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
       maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
@@ -1112,12 +1161,67 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
 // Between K1a and K1b: size the pass-2 hash table for at most min(12 survivors, capacity) records
 // (a cube has 12 faces) and clear that many slots; K1b inserts every record it stores.
 __global__ void k_table_prep(const __grid_constant__ ExtractParams P) {
-  const long long nwin = min((long long)P.counters[CNT_WIN], (long long)P.wcap);
-  const long long bound = min(12 * nwin, (long long)P.capacity);
+  const long long bound = min(12 * (long long)P.counters[CNT_SURVIVORS], (long long)P.capacity);
   const u64 hm = hash_slots(bound, P.table_cap) - 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_HMASK] = hm;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
     P.table[i] = -1;
+}
+
+// Between K1a and K1b: expand the group entries (one per scan lane with surviving cubes: first
+// anchor, plane flag, 32-bit survivor mask) into the dense cube list K1b takes in batches of 32.
+// A block takes EXPI x 256 consecutive entries (EXPI per thread), block-wide exclusive scan of the
+// survivor counts, one global atomic per block.
+constexpr int EXPI = 4;
+__global__ void __launch_bounds__(256) k_expand2d(const __grid_constant__ ExtractParams P) {
+  __shared__ int wsum[8];
+  __shared__ unsigned long long bbase;
+  const long long ng = min((long long)P.counters[CNT_WIN], (long long)P.wcap);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (long long t0 = (long long)blockIdx.x * 256 * EXPI; t0 < ng; t0 += (long long)gridDim.x * 256 * EXPI) {
+    const long long e0 = t0 + (long long)threadIdx.x * EXPI;
+    uint32_t m[EXPI];
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < EXPI; ++i) {
+      m[i] = e0 + i < ng ? (uint32_t)P.wz[e0 + i] : 0u;
+      cnt += __popc(m[i]);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int wex = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int v = wsum[k];
+      wex += k < wid ? v : 0;
+      tot += v;
+    }
+    if (threadIdx.x == 0) bbase = tot ? atomicAdd(&P.counters[CNT_CUBES], (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    long long o = (long long)bbase + wex + incl - cnt;
+#pragma unroll
+    for (int i = 0; i < EXPI; ++i) {
+      uint32_t mm = m[i];
+      if (!mm) continue;
+      const long long e = e0 + i;
+      const int x = P.wx[e], y = P.wy[e], t = P.wt[e];
+      for (; mm; mm &= mm - 1, ++o) {
+        const int bit = __ffs(mm) - 1;
+        if (o < P.wcap) {
+          P.cx[o] = x + (bit >> 3);
+          P.cy[o] = y + (bit & 7);
+          P.ct[o] = t;
+        }
+      }
+    }
+    __syncthreads();  // wsum / bbase are rewritten by the next tile
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1139,7 +1243,7 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
   G.hm = P.counters[CNT_HMASK];
   const float qmaxf = (float)G.qmax;
   BatchBuf bb{sm.ring + w * 32 * ws_words<T>(), sm.qx + w * 32, sm.qy + w * 32, sm.qt + w * 32, sm.items[w]};
-  const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
+  const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_CUBES], (long long)P.wcap);
   const long long nbat = (nwin + 31) / 32;
   const T* field = reinterpret_cast<const T*>(P.field);
   Prof pf;
@@ -1148,11 +1252,11 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
   pf.start();
   for (long long b = (long long)blockIdx.x * EXW + w; b < nbat; b += (long long)gridDim.x * EXW) {
     const long long e = b * 32 + lane;
-    const int et = e < nwin ? P.wt[e] : -1;
+    const int et = e < nwin ? P.ct[e] : -1;
     uint32_t* ent = bb.ring + lane * ws_words<T>();
     bool fast = false;
     if (et != -1) {
-      const int x = P.wx[e], y = P.wy[e];
+      const int x = P.cx[e], y = P.cy[e];
       const bool hasB = et < 0;
       // the cube's 4x4x2 window (planes t and t+1; t again when t+1 is not in the domain), zero
       // outside the grid
@@ -1240,7 +1344,7 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   const sm100::LaunchGeom lg = sm100::launch_geom(kern, NTHREADS, smem);
   if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan2d launch geometry");
   const int sms = lg.sms, per_sm = lg.per_sm;
-  const long long tiles = x_tiles(P.nx) * ((P.ny + TY - 1) / TY);
+  const long long tiles = ((P.nx + TX - 1) / TX) * ((P.ny + TY - 1) / TY);
   const long long slots = (long long)sms * std::max(per_sm, 1);
   ExtractParams Q = P;
   Q.tchunk = TCHUNK;
@@ -1255,7 +1359,9 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
     k_table_prep<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
     FTK_CUDA_TRY(cudaGetLastError());
   }
-  // K1b: persistent grid over the survivor list
+  k_expand2d<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  // K1b: persistent grid over the cube list
   const size_t xsmem = sizeof(ExSmem<T>);
   auto xk = k_exact2d<T>;
   const sm100::LaunchGeom xg = sm100::launch_geom(xk, EXW * 32, xsmem);

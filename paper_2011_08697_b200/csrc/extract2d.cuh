@@ -25,10 +25,13 @@ struct ExtractParams {
   int* table;          // [table_cap] slots, cleared by K1's table preparation
   unsigned long long table_cap;
   int* parent;         // [capacity]
-  // K1a -> K1b survivor list (cubes passing the prefilter): anchors wx, wy, [wz] and
-  // wt = t | (t+1 in the buffer) << 31 (-1: no cube); [wcap] each
+  // K1a -> K1b survivor list.  3D: one entry per surviving hypercube, anchors wx, wy, wz and
+  // wt = t | (t+1 in the buffer) << 31 (-1: no cube).  2D: group entries (first anchor wx, wy of a scan
+  // lane's 4 x 8 anchors, wt as above, survivor mask in wz (bit 8i + r: position i, anchor row r;
+  // 0: none)), expanded by k_expand2d into the cube list cx, cy, ct.  [wcap] each
   int *wx, *wy, *wt;
-  int* wz;             // 3D: anchor z
+  int* wz;
+  int *cx, *cy, *ct;
   i64 wcap;
   bool force_generic;  // testing: disable TMA
   void* ev_mid;        // profiling: cudaEvent_t recorded between K1a and K1b (2D), or null

@@ -32,7 +32,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
-  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, win, wx, wy, wt, wz, total;
+  size_t counters, table, edges, fid, parent, cross, exportA, exportB, map, win, wx, wy, wt, wz, cx, cy, ct, total;
   u64 hcap;
   i64 wcap;
 };
@@ -75,6 +75,12 @@ static Layout layout(i64 capacity, int esz = 8) {
   L.wt = off;
   off = align_up(off + (size_t)L.wcap * 4, 256);
   L.wz = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.cx = off;  // 2D cube list
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.cy = off;
+  off = align_up(off + (size_t)L.wcap * 4, 256);
+  L.ct = off;
   off = align_up(off + (size_t)L.wcap * 4, 256);
   L.total = off;
   return L;
@@ -199,6 +205,9 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.wy = reinterpret_cast<int*>(ws + L.wy);
   EP.wt = reinterpret_cast<int*>(ws + L.wt);
   EP.wz = reinterpret_cast<int*>(ws + L.wz);
+  EP.cx = reinterpret_cast<int*>(ws + L.cx);
+  EP.cy = reinterpret_cast<int*>(ws + L.cy);
+  EP.ct = reinterpret_cast<int*>(ws + L.ct);
   EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
@@ -269,8 +278,9 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   g_stats[2] = (int64_t)host_cnt[CNT_NOUT];
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
-  if ((i64)host_cnt[CNT_WIN] > L.wcap) {  // survivors beyond the window buffer were not tested
-    *n_out = std::max<int64_t>(*n_out, (int64_t)host_cnt[CNT_WIN]);
+  if ((i64)host_cnt[CNT_WIN] > L.wcap || (i64)host_cnt[CNT_CUBES] > L.wcap) {
+    // survivors beyond the survivor / cube lists were not tested
+    *n_out = std::max<int64_t>(*n_out, (int64_t)std::max(host_cnt[CNT_WIN], host_cnt[CNT_CUBES]));
     return FTK_ERR_CAPACITY;
   }
   if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity ||

@@ -13,5 +13,6 @@ rec, buf = ftk.track(f, cfg.scale_log2, return_buffers=True)
 for i in range(reps):
     rec = ftk.track(f, cfg.scale_log2, buffers=buf)
     ms, st = ftk.last_timings()
-    print(f'{name} rep {i}: k1 {ms[0]:.3f} ms pass2 {ms[1]:.3f} ms call {ms[3]:.3f} ms faces {st[0]} survivors {st[1]} punctured {st[2]}')
+    km = ftk.last_kernel_timings()
+    print(f'{name} rep {i}: k1 {ms[0]:.3f} ms (k1a {km[0]:.3f} k1b {km[1]:.3f}) pass2 {ms[1]:.3f} ms call {ms[3]:.3f} ms faces {st[0]} survivors {st[1]} punctured {st[2]}')
 torch.cuda.synchronize()
