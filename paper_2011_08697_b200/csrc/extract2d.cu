@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 
@@ -1349,6 +1350,8 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   ExtractParams Q = P;
   Q.tchunk = TCHUNK;
   if (tiles * ((P.tb - P.ta + TCHUNK - 1) / TCHUNK) < 16 * slots) Q.tchunk = TCHUNK / 2;
+  static const int env_tchunk = getenv("FTK_TCHUNK") ? atoi(getenv("FTK_TCHUNK")) : 0;  // experiments
+  if (env_tchunk > 0) Q.tchunk = env_tchunk;
   const long long items = tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk);
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, slots);

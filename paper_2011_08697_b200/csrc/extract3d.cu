@@ -102,7 +102,28 @@ __device__ __noinline__ int sos3_chain(const i64* r0, const i64* r1, const i64* 
   return 1;  // unreachable
 }
 
-__device__ __forceinline__ int sos3(const i64* r0, const i64* r1, const i64* r2) {
+// Sign of det[a; b; c] by a floating-point filter, for entries |.| < 2^26: the 2x2 minors are exact
+// in FP64 (products < 2^52, differences < 2^53); the three products a_i m_i are rounded, and the
+// rounded sum d differs from the exact determinant by at most 3.01 u (|p0| + |p1| + |p2|), u = 2^-53,
+// which the computed bound 2^-50 (|p0| + |p1| + |p2|) exceeds -- so |d| > bound fixes the exact sign.
+// Returns 0 when the filter cannot decide (the exact int128 path then runs).
+__device__ __forceinline__ int det3_sign_fp(const i64* a, const i64* b, const i64* c) {
+  const double b0 = (double)b[0], b1 = (double)b[1], b2 = (double)b[2];
+  const double c0 = (double)c[0], c1 = (double)c[1], c2 = (double)c[2];
+  const double m0 = __dsub_rn(__dmul_rn(b1, c2), __dmul_rn(b2, c1));
+  const double m1 = __dsub_rn(__dmul_rn(b0, c2), __dmul_rn(b2, c0));
+  const double m2 = __dsub_rn(__dmul_rn(b0, c1), __dmul_rn(b1, c0));
+  const double p0 = __dmul_rn((double)a[0], m0), p1 = __dmul_rn((double)a[1], m1), p2 = __dmul_rn((double)a[2], m2);
+  const double d = __dadd_rn(__dsub_rn(p0, p1), p2);
+  const double bound = __dmul_rn(__dadd_rn(__dadd_rn(fabs(p0), fabs(p1)), fabs(p2)), 0x1p-50);
+  return d > bound ? 1 : (d < -bound ? -1 : 0);
+}
+
+__device__ __forceinline__ int sos3(const i64* r0, const i64* r1, const i64* r2, bool small) {
+  if (small) {
+    const int f = det3_sign_fp(r0, r1, r2);
+    if (f) return f;
+  }
   const i128 d = det3(r0, r1, r2);
   if (d != 0) return d > 0 ? 1 : -1;
   return sos3_chain(r0, r1, r2);
@@ -184,13 +205,14 @@ __device__ __forceinline__ double dot4_nofma(const double* mu, const double* v) 
 
 // punctured test of a face with vertex gradients g[0..3] (rows in global vertex order):
 // s_k = (-1)^(k+3) sos(rows != k), all equal
-__device__ __forceinline__ bool punctured4(const i64 (&g)[4][3]) {
-  const int s0 = -sos3(g[1], g[2], g[3]);
-  const int s1 = sos3(g[0], g[2], g[3]);
+// small: every entry |.| < 2^26 (the floating-point filter of det3_sign_fp applies)
+__device__ __forceinline__ bool punctured4(const i64 (&g)[4][3], bool small) {
+  const int s0 = -sos3(g[1], g[2], g[3], small);
+  const int s1 = sos3(g[0], g[2], g[3], small);
   if (s0 != s1) return false;
-  const int s2 = -sos3(g[0], g[1], g[3]);
+  const int s2 = -sos3(g[0], g[1], g[3], small);
   if (s0 != s2) return false;
-  const int s3 = sos3(g[0], g[1], g[2]);
+  const int s3 = sos3(g[0], g[1], g[2], small);
   return s0 == s3;
 }
 
@@ -262,7 +284,7 @@ __constant__ Cells4 cCells4 = make_cells4();
 // named barrier per plane), over the t-pair with the previous plane's cube codes in registers; a
 // zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte are zero).
 namespace s3 {
-constexpr int LX = 128, TX = 124, RW = 8, XOFF = 4, PITCH = LX + 8;
+constexpr int LX = 128, TX = LX, RW = 8, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
 constexpr int ROWS = RW + 3;  // y0-1 .. y0+RW+1
 template <typename T>
 constexpr int nzw() { return sizeof(T) == 4 ? 8 : 4; }  // z-slice warps (owned slices per tile)
@@ -332,6 +354,8 @@ struct Ctx {
   int rpos;        // position (0..3) of x = nx - 1 in this lane, else -1
   bool lpat;       // x = 0 is this lane's position 0
   uint32_t oob;    // NEUTRAL bits of this lane's out-of-grid positions
+  bool xe_out;     // column x0 + 128 is outside the grid
+  bool xe_last;    // column x0 + 128 is x = nx - 1
   long long gy0, ny;
   long long gz, nz;
 };
@@ -362,6 +386,33 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
         if (c.rpos == 3) r = v.w;
       }
     };
+    // codes of column x0 + 128 (the next tile's first column; they complete lane 31's cubes): lane k
+    // computes code row k (centre row k + 1), Ye = the y-pair of code rows k, k + 1
+    uint32_t Ye;
+    {
+      const int k = min(c.lane, RW);
+      const int o = (k + 1) * PITCH + XOFF + LX;
+      const float ctr = S[o], l = S[o - 1];
+      float r = S[o + 1], u = S[o - PITCH], d = S[o + PITCH], zm = Zm[o], zp = Zp[o];
+      bool out = false;
+      if (EDGE) {
+        const long long gy = c.gy0 + k;
+        if (c.xe_last) r = ctr;
+        if (gy == 0) u = ctr;
+        if (gy == c.ny - 1) d = ctr;
+        out = c.xe_out || gy >= c.ny || zout;
+      }
+      const float th = __uint_as_float(lo32(thr2));
+      const float dx = __fsub_rn(r, l), dy = __fsub_rn(d, u), dz = __fsub_rn(zp, zm);
+      const uint32_t ce = out ? 0xFCu
+                              : ((__float_as_uint(__fsub_rn(th, dx)) >> 31) << 7) |
+                                    ((__float_as_uint(__fadd_rn(dx, th)) >> 31) << 6) |
+                                    ((__float_as_uint(__fsub_rn(th, dy)) >> 31) << 5) |
+                                    ((__float_as_uint(__fadd_rn(dy, th)) >> 31) << 4) |
+                                    ((__float_as_uint(__fsub_rn(th, dz)) >> 31) << 3) |
+                                    ((__float_as_uint(__fadd_rn(dz, th)) >> 31) << 2);
+      Ye = ce & __shfl_down_sync(0xffffffffu, ce, 1);
+    }
     float4 v0, v1, v2;
     float l0, r0, l1, r1, l2, r2;
     load(0, v0, l0, r0);
@@ -385,7 +436,8 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       if (k >= 1) {
         const uint32_t Y = Cprev & C;
         uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
-        if (c.lane == 31) nb = 0xFCu;  // beyond the tile: AND-neutral
+        const uint32_t ne = __shfl_sync(0xffffffffu, Ye, k - 1);  // column x0 + 128
+        if (c.lane == 31) nb = ne;
         Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
       }
       Cprev = C;
@@ -411,6 +463,26 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
           if (c.rpos == q) f[q + 2] = f[q + 1];
       }
     };
+    uint32_t Ye;  // codes of column x0 + 128 (as for fp32)
+    {
+      const int k = min(c.lane, RW);
+      const int o = (k + 1) * PITCH + XOFF + LX;
+      const double ctr = S[o], l = S[o - 1];
+      double r = S[o + 1], u = S[o - PITCH], d = S[o + PITCH], zm = Zm[o], zp = Zp[o];
+      bool out = false;
+      if (EDGE) {
+        const long long gy = c.gy0 + k;
+        if (c.xe_last) r = ctr;
+        if (gy == 0) u = ctr;
+        if (gy == c.ny - 1) d = ctr;
+        out = c.xe_out || gy >= c.ny || zout;
+      }
+      const double th = (double)thr, dx = r - l, dy = d - u, dz = zp - zm;
+      const uint32_t ce = out ? 0xFCu
+                              : (sgn64(th - dx) << 7) | (sgn64(dx + th) << 6) | (sgn64(th - dy) << 5) |
+                                    (sgn64(dy + th) << 4) | (sgn64(th - dz) << 3) | (sgn64(dz + th) << 2);
+      Ye = ce & __shfl_down_sync(0xffffffffu, ce, 1);
+    }
     double f0[6], f1[6], f2_[6];
     load(0, f0);
     load(1, f1);
@@ -440,7 +512,8 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       if (k >= 1) {
         const uint32_t Y = Cprev & C;
         uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);  // next lane's position 0
-        if (c.lane == 31) nb = 0xFCu;  // beyond the tile: AND-neutral
+        const uint32_t ne = __shfl_sync(0xffffffffu, Ye, k - 1);  // column x0 + 128
+        if (c.lane == 31) nb = ne;
         Sq[k - 1] = Y & ((Y >> 8) | (nb << 24));
       }
       Cprev = C;
@@ -464,7 +537,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const i64 nx = P.nx, ny = P.ny, nz = P.nz;
   constexpr uint32_t STAGE_BYTES = PITCH * ROWS * SL * sizeof(T);
-  const int ntx = (int)x_tiles(nx), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
+  const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
   const int ntc = (int)((P.tb - P.ta + TCH - 1) / TCH);
   const long long nitems = (long long)ntx * nty * ntz * ntc;
   if (tid == 0) {
@@ -544,7 +617,38 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     uint32_t prevK[RW];
     long long cur = 0, end = 0;
     const bool top = warp == NZW;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0, int z) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
+      if (bal == 0u) return;
+      if (__all_sync(0xffffffffu, (mask & (mask - 1u)) == 0u)) {
+        // common case: at most one survivor per lane -- ranks from the ballot, no warp scan
+        const int n = __popc(bal), rank = __popc(bal & lt_mask);
+        const int avail = (int)(end - cur);
+        long long e = cur + rank;
+        if (n > avail) {  // the chunk runs out: the rest goes to a fresh chunk (n <= 32 = CHUNK)
+          long long cc = 0;
+          if (lane == 0) cc = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
+          cc = __shfl_sync(0xffffffffu, cc, 0);
+          if (rank >= avail) {
+            // entries [cur, end) of the old chunk are filled by the lanes of rank < avail
+            e = cc + (rank - avail);
+          }
+          cur = cc + (n - avail);
+          end = cc + CHUNK;
+        } else {
+          cur += n;
+        }
+        if (mask != 0u && e < P.wcap) {
+          const int bb = __ffs(mask) - 1;
+          P.wx[e] = x0 + 4 * lane + (bb >> 3);
+          P.wy[e] = y0 + (bb & 7);
+          P.wz[e] = z;
+          P.wt[e] = tflag;
+        }
+        mysurv += n;
+        return;
+      }
       while (__any_sync(0xffffffffu, mask != 0)) {
         if (cur == end) {
           long long cc = 0;
@@ -582,7 +686,9 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     c.ny = ny;
     c.nz = nz;
     int gk = 0, x0 = 0, y0 = 0, z0 = 0;
-    bool edge = false, last_x = false;
+    bool edge = false;
+    c.xe_out = false;
+    c.xe_last = false;
     while (true) {
       const int s = gk % NSTAGE;
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
@@ -601,8 +707,9 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (gx + i >= nx) c.oob |= 0xFCu << (8 * i);
-        edge = x0 < 1 || x0 + LX + 1 > nx || y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
-        last_x = x0 + LX >= nx;
+        edge = x0 < 1 || x0 + LX + 2 > nx || y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
+        c.xe_out = x0 + LX >= nx;
+        c.xe_last = x0 + LX == nx - 1;
       }
       const T* S = sm.plane[s] + (warp + 1) * (PITCH * ROWS);  // slice z0 + warp
       uint32_t Sq[RW];
@@ -622,7 +729,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
           uint32_t mask = 0;
 #pragma unroll
           for (int r = 0; r < RW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
-          return (lane == 31 && !last_x) ? 0u : mask;
+          return mask;
         };
         const bool inz = z0 + warp < nz;
         const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
@@ -674,6 +781,7 @@ constexpr int XW3 = 4;  // warps per block
 template <typename T>
 __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ ExtractParams P) {
   __shared__ i64 sg[XW3][16][3];
+  __shared__ i64 sH[XW3][16][6];  // corner Hessians (hypercubes with punctured faces)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Geo3 G;
   G.nx = P.nx;
@@ -711,6 +819,14 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
       ex = __ballot_sync(0xffffffffu, lane < 16 && e1);
     }
     __syncwarp();
+    // all 48 gradient components below 2^26 in magnitude: the FP64 determinant filter applies
+    bool small;
+    {
+      const int c = lane & 15;
+      const i64 lim = 1ll << 26;
+      small = __all_sync(0xffffffffu, g[c][0] > -lim && g[c][0] < lim && g[c][1] > -lim && g[c][1] < lim &&
+                                          g[c][2] > -lim && g[c][2] < lim);
+    }
     // the 60 face types, two per lane
     unsigned long long pmask = 0;
 #pragma unroll
@@ -727,12 +843,18 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
           for (int j = 0; j < 3; ++j)
             rej |= (gv[0][j] > 0 && gv[1][j] > 0 && gv[2][j] > 0 && gv[3][j] > 0) ||
                    (gv[0][j] < 0 && gv[1][j] < 0 && gv[2][j] < 0 && gv[3][j] < 0);
-          pu = !rej && punctured4(gv);
+          pu = !rej && punctured4(gv, small);
         }
       }
       pmask |= (unsigned long long)__ballot_sync(0xffffffffu, pu) << (32 * h);
     }
     const int npunct = __popcll(pmask);
+    if (npunct) {  // integer Hessians of the 16 corners, one per lane, for the records below
+      const int c = lane & 15;
+      if (lane < 16 && ((ex >> c) & 1))
+        hess3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+      __syncwarp();
+    }
     unsigned long long rbase = 0;
     if (lane == 0 && npunct) rbase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)npunct);
     rbase = __shfl_sync(0xffffffffu, rbase, 0);
@@ -754,7 +876,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
                               {g[cd.w[2]][0], g[cd.w[2]][1], g[cd.w[2]][2]},
                               {g[cd.w[3]][0], g[cd.w[3]][1], g[cd.w[3]][2]},
                               {g[15][0], g[15][1], g[15][2]}};
-        if (punctured4(gu)) {
+        if (punctured4(gu, small)) {
           if (k < 2) {
             const int a1 = cd.w[1];
             const i64 fx = x + (a1 & 1), fy = y + ((a1 >> 1) & 1), fz = z + ((a1 >> 2) & 1), ft = t + ((a1 >> 3) & 1);
@@ -819,10 +941,8 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
         pv[1][kk] = (double)vy;
         pv[2][kk] = (double)vz;
         pv[3][kk] = (double)vt;
-        i64 H[6];
-        hess3<T>(P, G, vx, vy, vz, vt, H);
 #pragma unroll
-        for (int q = 0; q < 6; ++q) Hd[q][kk] = __ll2double_rn(H[q]);
+        for (int q = 0; q < 6; ++q) Hd[q][kk] = __ll2double_rn(sH[w][m[kk]][q]);
       }
       double Hb[6];
 #pragma unroll
@@ -878,7 +998,7 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   const sm100::LaunchGeom lg = sm100::launch_geom(kern, nthreads<T>(), smem);
   if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan3d launch geometry");
   const int sms = lg.sms, per_sm = lg.per_sm;
-  const long long items = x_tiles(P.nx) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
+  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
                           ((P.tb - P.ta + TCH - 1) / TCH);
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));

@@ -181,13 +181,6 @@ inline EncodeTiledFn get_encode() {
   return fn;
 }
 
-// x tiles of a scan: tile k starts at 124 k and owns 124 columns (its lane 31 is a halo lane that only
-// completes lane 30's cubes) -- except the last tile, x0 + 128 >= nx, whose lane 31 owns its columns
-// too (their x + 1 neighbours are outside the grid, AND-neutral).
-__host__ __device__ __forceinline__ long long x_tiles(long long nx) {
-  return nx <= 128 ? 1 : (nx - 128 + 123) / 124 + 1;
-}
-
 // Per-thread cache of the launch geometry of a kernel on the current device: SM count and resident
 // blocks per SM (the dynamic-smem attribute is set on the first call).  Keeps the per-call host
 // overhead of the persistent launches to a lookup.

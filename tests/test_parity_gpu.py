@@ -210,6 +210,15 @@ def test_woven3d_parity(ftk, oracle_lib, shape, L, sigma):
     run_pair(ftk, oracle_lib, w.generate(), 26)
 
 
+@pytest.mark.parametrize("s", [14, 25, 27, 36])
+def test_woven3d_scale_paths(ftk, oracle_lib, s):
+    """K1b (3D) decides determinant signs with an FP64 filter when every gradient component of the
+    hypercube is below 2^26 and with exact int128 otherwise: s = 14 / 25 keep every hypercube on the
+    filter, 27 mixes both, 36 (|q| < 2^38, the 3D range limit) forces the exact path everywhere."""
+    w = fi.Woven(21, 19, 5, L=15.0, sigma=0.02, nz=17)
+    run_pair(ftk, oracle_lib, w.generate(), s)
+
+
 def test_degenerate_3d_parity(ftk, oracle_lib):
     for seed in range(2):
         f = fi.random_degenerate((3, 5, 6, 7), seed=seed)
