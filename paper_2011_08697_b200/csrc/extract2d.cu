@@ -761,10 +761,12 @@ __device__ __forceinline__ uint32_t code_f32(const float4 u, const float4 v, con
 
 // Scan one plane (fp32): all RW+3 rows are loaded first (independent shared loads and shuffles),
 // then the RW+1 code rows, then the squares Sq[r] (OR over the 4 corners of each square, per
-// position).  EDGE: one-sided differences at the grid boundary by patching neighbour values.
-template <bool EDGE>
+// position).  One-sided differences at the grid boundary by patching neighbour values; MODE 0:
+// interior tile, 1: x boundary only, 2: y boundary (and possibly x).
+template <int MODE>
 __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c, f2 thr2, f2 nthr2,
                                                uint32_t (&Sq)[RW], uint32_t& maxb) {
+  constexpr bool XE = MODE >= 1, EDGE = MODE >= 2;
   // rows srow0-1 .. srow0+RW+1, rolled through a 3-row window: code row k needs rows k (up), k+1
   // (centre, with its x neighbours l, r) and k+2 (down); square row k ANDs code rows k, k+1
   const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
@@ -777,7 +779,7 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
     const float dn = __shfl_down_sync(0xffffffffu, v.x, 1);
     l = lane0 ? h : up;
     r = lane31 ? h : dn;
-    if (EDGE) {
+    if (XE) {
       if (c.lpat) l = v.x;
       if (c.rpos == 0) v.y = v.x;
       if (c.rpos == 1) v.z = v.y;
@@ -794,12 +796,15 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
     const float ctr = p[0], l = p[-1];
     float r = p[1], u = p[-PITCH], d = p[PITCH];
     bool out = false;
+    if (XE) {
+      if (c.xe_last) r = ctr;
+      out = c.xe_out;
+    }
     if (EDGE) {
       const long long gy = c.gy0 + k;
-      if (c.xe_last) r = ctr;
       if (gy == 0) u = ctr;
       if (gy == c.ny - 1) d = ctr;
-      out = c.xe_out || gy >= c.ny;
+      out = out || gy >= c.ny;
     }
     const float thr = __uint_as_float(lo32(thr2));
     const float dx = __fsub_rn(r, l), dy = __fsub_rn(d, u);
@@ -825,6 +830,8 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
       const float4 u = gy == 0 ? v1 : v0;
       const float4 d = gy == c.ny - 1 ? v1 : v2;
       C = gy >= c.ny ? 0xF0F0F0F0u : code_f32(u, v1, d, l1, r1, thr2, nthr2) | (~c.xmask & 0xF0F0F0F0u);
+    } else if (XE) {
+      C = code_f32(v0, v1, v2, l1, r1, thr2, nthr2) | (~c.xmask & 0xF0F0F0F0u);
     } else {
       C = code_f32(v0, v1, v2, l1, r1, thr2, nthr2);
     }
@@ -1059,7 +1066,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
 
     int gk = 0;
     int x0 = -1, y0 = -1;
-    bool edge = false;
+    int mode = 0;
     ScanCtx sc;
     sc.srow0 = srow0;
     sc.lane = lane;
@@ -1083,7 +1090,8 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
         y0 = m.y0;
         const i64 gx = (i64)x0 + 4 * lane;
         sc.gy0 = (i64)y0 + sw * RW;
-        edge = x0 < 1 || x0 + LX + 2 > nx || sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
+        const bool xedge = x0 < 1 || x0 + LX + 2 > nx, yedge = sc.gy0 < 1 || sc.gy0 + RW + 2 > ny;
+        mode = yedge ? 2 : (xedge ? 1 : 0);
         sc.xe_out = x0 + LX >= nx;
         sc.xe_last = x0 + LX == nx - 1;
         sc.lpat = gx == 0;
@@ -1096,10 +1104,11 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
       const T* S = sm.plane[s];
       uint32_t Sq[RW];
       if constexpr (sizeof(T) == 4) {
-        if (edge) scan_plane_f32<true>(S, sc, thr2, nthr2, Sq, maxb32);
-        else scan_plane_f32<false>(S, sc, thr2, nthr2, Sq, maxb32);
+        if (mode == 2) scan_plane_f32<2>(S, sc, thr2, nthr2, Sq, maxb32);
+        else if (mode == 1) scan_plane_f32<1>(S, sc, thr2, nthr2, Sq, maxb32);
+        else scan_plane_f32<0>(S, sc, thr2, nthr2, Sq, maxb32);
       } else {
-        if (edge) scan_plane_f64<true>(S, sc, (double)thr, Sq, maxd);
+        if (mode) scan_plane_f64<true>(S, sc, (double)thr, Sq, maxd);
         else scan_plane_f64<false>(S, sc, (double)thr, Sq, maxd);
       }
       __syncwarp();

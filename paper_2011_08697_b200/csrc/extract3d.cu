@@ -361,10 +361,12 @@ struct Ctx {
 };
 
 // squares (AND over y-pair and x-pair) of the slice whose centre rows start at S (row 0 = y0-1),
-// with the z -+ 1 slices at S -/+ slice_stride
-template <typename T, bool EDGE>
+// with the z -+ 1 slices at S -/+ slice_stride.  MODE 0: interior; 1: x boundary only (one-sided
+// x differences, out-of-grid columns); 2: any boundary (fp64 input treats 1 as 2).
+template <typename T, int MODE>
 __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx& c, f2 thr2, f2 nthr2, T thr,
                                               uint32_t (&Sq)[RW], uint32_t& maxb, double& maxd, bool count) {
+  constexpr bool XE = MODE >= 1, EDGE = sizeof(T) == 4 ? MODE >= 2 : MODE >= 1;
   const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
   const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
   const bool zlo = EDGE && c.gz == 0, zhi = EDGE && c.gz == c.nz - 1, zout = EDGE && c.gz >= c.nz;
@@ -378,7 +380,7 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       const float dn = __shfl_down_sync(0xffffffffu, v.x, 1);
       l = lane0 ? h : up;
       r = lane31 ? h : dn;
-      if (EDGE) {
+      if (XE) {
         if (c.lpat) l = v.x;
         if (c.rpos == 0) v.y = v.x;
         if (c.rpos == 1) v.z = v.y;
@@ -395,12 +397,15 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
       const float ctr = S[o], l = S[o - 1];
       float r = S[o + 1], u = S[o - PITCH], d = S[o + PITCH], zm = Zm[o], zp = Zp[o];
       bool out = false;
+      if (XE) {
+        if (c.xe_last) r = ctr;
+        out = c.xe_out;
+      }
       if (EDGE) {
         const long long gy = c.gy0 + k;
-        if (c.xe_last) r = ctr;
         if (gy == 0) u = ctr;
         if (gy == c.ny - 1) d = ctr;
-        out = c.xe_out || gy >= c.ny || zout;
+        out = out || gy >= c.ny || zout;
       }
       const float th = __uint_as_float(lo32(thr2));
       const float dx = __fsub_rn(r, l), dy = __fsub_rn(d, u), dz = __fsub_rn(zp, zm);
@@ -430,6 +435,8 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
         const float4 u = gy == 0 ? v1 : v0;
         const float4 d = gy == c.ny - 1 ? v1 : v2;
         C = (gy >= c.ny || zout) ? NEUTRAL : (code6_f32(u, v1, d, zm, zp, l1, r1, thr2, nthr2) | c.oob);
+      } else if (XE) {
+        C = code6_f32(v0, v1, v2, zm, zp, l1, r1, thr2, nthr2) | c.oob;
       } else {
         C = code6_f32(v0, v1, v2, zm, zp, l1, r1, thr2, nthr2);
       }
@@ -686,7 +693,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     c.ny = ny;
     c.nz = nz;
     int gk = 0, x0 = 0, y0 = 0, z0 = 0;
-    bool edge = false;
+    int mode = 0;
     c.xe_out = false;
     c.xe_last = false;
     while (true) {
@@ -707,14 +714,17 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           if (gx + i >= nx) c.oob |= 0xFCu << (8 * i);
-        edge = x0 < 1 || x0 + LX + 2 > nx || y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
+        const bool xedge = x0 < 1 || x0 + LX + 2 > nx;
+        const bool yzedge = y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
+        mode = yzedge ? 2 : (xedge ? 1 : 0);
         c.xe_out = x0 + LX >= nx;
         c.xe_last = x0 + LX == nx - 1;
       }
       const T* S = sm.plane[s] + (warp + 1) * (PITCH * ROWS);  // slice z0 + warp
       uint32_t Sq[RW];
-      if (edge) slice_squares<T, true>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      else slice_squares<T, false>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      if (mode == 2) slice_squares<T, 2>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      else if (mode == 1) slice_squares<T, 1>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      else slice_squares<T, 0>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       const int par = gk & 1;
