@@ -276,9 +276,11 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = total_faces / (ms_step / 1000.0)
 
-    # roofline of the dominant kernel, the scan kernel K1a: algorithmic bytes = the
-    # field read once + the survivor list written (12 B per surviving cube); the exact kernel K1b is
-    # reported beside it (window reads of the survivors + records + edges)
+    # roofline of the extraction kernel north_star names, the scan kernel K1a:
+    # algorithmic bytes = the field read once + the survivors handed on (12 B per surviving cube);
+    # the exact kernel K1b (2D: with k_expand2d) is reported beside it -- window reads of the
+    # survivors + records -- with both kernels' shares of the step, since on C2 K1b takes the larger
+    # share (it is latency-bound)
     esz = field.element_size()
     k1_avg = sum(k1_ms) / len(k1_ms)
     ka_avg = sum(ka_ms) / len(ka_ms)
@@ -324,12 +326,16 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": f"{kscan} (K1a, prefilter scan)", "alg_bytes_per_launch": alg_bytes,
-                     kexact: {"ms": kb_avg, "alg_bytes_per_launch": win_bytes * n_surv + n_punct * ftk.RECORD_BYTES,
+                     "share_of_step": ka_avg / ms_step,
+                     kexact: {"ms": kb_avg, "share_of_step": kb_avg / ms_step,
+                              "alg_bytes_per_launch": win_bytes * n_surv + n_punct * ftk.RECORD_BYTES,
+                              "achieved_gbs": (win_bytes * n_surv + n_punct * ftk.RECORD_BYTES) / (kb_avg / 1000.0) / 1e9,
                               "traffic": _ncu_traffic(cfg.name, kexact)}},
         "clocks": clk.summary(),
         "e2e": e2e,
-        # K1a + K1b + k_clear + k_hash_insert + k_edges + k_label; slabs add k_export and k_relabel
-        "gpu_launches": (6 + (2 if world > 1 else 0)) * args.steps,
+        # K1a (+ k_expand2d in 2D) + K1b + k_clear + k_hash_insert + k_edges + k_label; time slabs add
+        # k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
+        "gpu_launches": ((6 if d3 else 7) + (6 if world > 1 else 0)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)

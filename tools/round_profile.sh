@@ -10,7 +10,7 @@ if [ $rc -eq 0 ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
     python bench.py --config $cfg --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launches_$tag.csv 2> gpurun_out/launches_$tag.err
   echo "launch list rc=$?"
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_scan2d|k_exact2d|k_extract3d" -c 2 -f \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_scan2d|k_exact2d|k_scan3d|k_exact3d" -c 2 -f \
     -o gpurun_out/full_$tag python tools/prof_run.py $cfg 1 > gpurun_out/ncu_full_$tag.log 2>&1
   echo "ncu full rc=$?"
 fi

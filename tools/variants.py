@@ -6,6 +6,8 @@ VARIANTS = {
     "base": [],
     "prof": ["FTK_K1_PROF=1"],
     "mixhash": ["FTK_LOCAL_HASH=0"],
+    "xminb2": ["FTK_X_MINB=2"],
+    "xminb4": ["FTK_X_MINB=4"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
