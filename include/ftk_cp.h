@@ -183,6 +183,34 @@ FTK_API int ftk_seam_pack(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int
 FTK_API int ftk_seam_resolve(const int64_t* d_all, int world, int64_t cap, ftk_cp* d_out, int64_t n,
                              ftk_stream stream);
 
+/* Streaming ingestion (P:709 push_field_data; the mesh is traversed one timestep after another,
+ * P:282-286).  Timesteps are pushed one at a time; the tracker stages them in a window of
+ * `window` + 1 planes inside d_ws and runs pass 1 on each full window (anchors [t0, t0 + window),
+ * plane t0 + window as the ghost plane -- the time-slab rule), keeping the last plane for the next
+ * window.  Records, trajectory edges and in-cube unions accumulate in d_out / d_ws across windows;
+ * ftk_tracker_finish runs pass 1 on the remaining planes (the last one is the final timestep),
+ * then pass 2 once over all records, and returns *n_out.  The result -- records, labels, flags --
+ * is identical to one ftk_cp_track over the whole field, but only window + 1 planes are ever
+ * resident on the device.
+ *   desc: ndim, dtype, n[], scale_log2 as for track (nt, t0, nt_global, flags are ignored);
+ *   window >= 1 timesteps per pass-1 launch (larger windows fill the GPU better: DESIGN.md 10);
+ *   d_out: device array of `capacity` records for the WHOLE stream; d_ws: device workspace of
+ *   ws_bytes >= ftk_tracker_workspace_size() bytes.  The tracker (a small host object) keeps
+ *   these pointers until finish/abort -- the one exception to "nothing is retained".
+ *   push: `plane` is one timestep (nx*ny*nz values of dtype), host or device memory (copied
+ *   asynchronously on `stream`; a host buffer must stay valid until the stream reaches the copy --
+ *   pinned memory for overlap).  Errors of a push are sticky and reported again by finish.
+ *   finish: frees the tracker (also on error).  FTK_ERR_INVALID_ARG with fewer than 2 timesteps;
+ *   FTK_ERR_CAPACITY (*n_out = required count) when records or survivors overflowed -- the stream
+ *   must then be pushed again with a larger capacity.  abort: frees the tracker, no result. */
+typedef struct ftk_tracker ftk_tracker;
+FTK_API int ftk_tracker_workspace_size(const ftk_desc* desc, int64_t capacity, int32_t window, size_t* bytes);
+FTK_API int ftk_tracker_begin(ftk_tracker** tracker, const ftk_desc* desc, int32_t window, ftk_cp* d_out,
+                              int64_t capacity, void* d_ws, size_t ws_bytes, ftk_stream stream);
+FTK_API int ftk_tracker_push(ftk_tracker* tracker, const void* plane);
+FTK_API int ftk_tracker_finish(ftk_tracker* tracker, int64_t* n_out);
+FTK_API int ftk_tracker_abort(ftk_tracker* tracker);
+
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);

@@ -10,6 +10,7 @@ is missing or no GPU is present, calls raise.
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 from dataclasses import dataclass
@@ -39,6 +40,7 @@ EXPORTS = [
     "ftk_last_kernel_timings",
     "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
+    "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
 ]
 
 
@@ -91,6 +93,11 @@ def lib() -> ctypes.CDLL:
         L.ftk_stitch_export.argtypes = [PD, P, ctypes.c_size_t, I64, P, I64, P, P, I64, P, P]
         L.ftk_stitch_resolve.argtypes = [P, I64, P, I64, P, I64, P, P, P]
         L.ftk_relabel.argtypes = [P, I64, P, P, I64, P, ctypes.c_size_t, I64, P]
+        L.ftk_tracker_workspace_size.argtypes = [PD, I64, ctypes.c_int32, P]
+        L.ftk_tracker_begin.argtypes = [P, PD, ctypes.c_int32, P, I64, P, ctypes.c_size_t, P]
+        L.ftk_tracker_push.argtypes = [P, P]
+        L.ftk_tracker_finish.argtypes = [P, P]
+        L.ftk_tracker_abort.argtypes = [P]
         _lib = L
     return _lib
 
@@ -222,6 +229,60 @@ def track_host(field_host: torch.Tensor, scale_log2: int, stage: torch.Tensor, b
         ctypes.c_void_p(_stream_ptr(stage.device)))
     _check(st, "ftk_cp_track_host")
     return n_out.value
+
+
+class Tracker:
+    """Streaming ingestion (PAPER.md:709 push_field_data; include/ftk_cp.h ftk_tracker_*): push the
+    timesteps one at a time (host or device tensors of shape [y][x] or [z][y][x]), then finish() runs
+    the rest of pass 1 and pass 2 and returns the labelled records -- identical to track() over the
+    whole field, with only window + 1 planes resident on the device.  `capacity` bounds the records
+    of the whole stream (FtkError with FTK_ERR_CAPACITY otherwise)."""
+
+    def __init__(self, spatial_shape, dtype, scale_log2: int, capacity: int, window: int = 64, device="cuda"):
+        self.device = torch.device(device)
+        self.desc = make_desc((2, *spatial_shape), dtype, scale_log2)
+        self.capacity = int(capacity)
+        b = ctypes.c_size_t(0)
+        _check(lib().ftk_tracker_workspace_size(ctypes.byref(self.desc), self.capacity, window, ctypes.byref(b)),
+               "ftk_tracker_workspace_size")
+        self.records = torch.empty(max(self.capacity, 1) * RECORD_BYTES, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.empty(b.value, dtype=torch.uint8, device=self.device)
+        self.dtype = torch.float32 if self.desc.dtype == F32 else torch.float64
+        self.spatial_shape = tuple(spatial_shape)
+        self._h = ctypes.c_void_p(0)
+        self._keep = collections.deque()  # (host plane, event after its copy): copies may be in flight
+        self._window = window
+        _check(lib().ftk_tracker_begin(ctypes.byref(self._h), ctypes.byref(self.desc), window,
+                                       ctypes.c_void_p(self.records.data_ptr()), self.capacity,
+                                       ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
+                                       ctypes.c_void_p(_stream_ptr(self.device))), "ftk_tracker_begin")
+
+    def push(self, plane: torch.Tensor):
+        if self._h is None:
+            raise FtkError(ERR_INVALID_ARG, "Tracker.push after finish")
+        if tuple(plane.shape) != self.spatial_shape or plane.dtype != self.dtype:
+            raise FtkError(ERR_INVALID_ARG, f"Tracker.push: plane must be {self.spatial_shape} {self.dtype}")
+        plane = plane.contiguous()
+        _check(lib().ftk_tracker_push(self._h, ctypes.c_void_p(plane.data_ptr())), "ftk_tracker_push")
+        if not plane.is_cuda:  # keep the host buffer alive until its asynchronous copy has run
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self._keep.append((plane, ev))
+            while len(self._keep) > 2 * self._window + 2:
+                self._keep.popleft()[1].synchronize()
+
+    def finish(self) -> torch.Tensor:
+        n_out = ctypes.c_int64(0)
+        h, self._h = self._h, None
+        st = lib().ftk_tracker_finish(h, ctypes.byref(n_out))
+        self._keep.clear()
+        _check(st, "ftk_tracker_finish")
+        return self.records[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ftk_tracker_abort(self._h)
+            self._h = None
 
 
 def to_numpy(rec: torch.Tensor) -> np.ndarray:

@@ -9,6 +9,8 @@
 #include <unordered_map>
 #include <vector>
 #include <cstring>
+#include <memory>
+#include <new>
 #include <string>
 
 #include "common.cuh"
@@ -162,20 +164,8 @@ struct Events {  // profiling events, created once per host thread and reused
   }
 };
 
-static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
-               void* d_ws, size_t ws_bytes, cudaStream_t stream, bool track) {
-  int st = validate(desc);
-  if (st) return st;
-  if (!d_field || !n_out || !d_ws || capacity < 0 || capacity > kMaxCapacity || (capacity > 0 && !d_out))
-    return FTK_ERR_INVALID_ARG;
-  const Layout L = layout(capacity, esz_of(desc));
-  if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
-  char* ws = static_cast<char*>(d_ws);
-  auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
-  Events ev;
-  ev.rec(0, stream);
-  FTK_CUDA_TRY(cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), stream));
-
+static ExtractParams extract_params(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                                    char* ws, const Layout& L, unsigned long long* counters, bool track) {
   ExtractParams EP;
   memset(&EP, 0, sizeof EP);
   EP.field = d_field;
@@ -210,6 +200,71 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.ct = reinterpret_cast<int*>(ws + L.ct);
   EP.wcap = L.wcap;
   EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
+  return EP;
+}
+
+static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t capacity, char* ws, const Layout& L,
+                                unsigned long long* counters, bool k1_insert) {
+  TrackParams TP;
+  TP.rec = d_out;
+  TP.capacity = capacity;
+  TP.counters = counters;
+  TP.table = reinterpret_cast<int*>(ws + L.table);
+  TP.table_cap = L.hcap;
+  TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
+  TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
+  TP.inserted = k1_insert;
+  TP.prelinked = desc->ndim == 2;
+  TP.diag = getenv("FTK_PASS2_DIAG") ? atoi(getenv("FTK_PASS2_DIAG")) : 0;
+  TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
+  TP.fid = reinterpret_cast<i64*>(ws + L.fid);
+  TP.parent = reinterpret_cast<int*>(ws + L.parent);
+  TP.T = desc->ndim == 2 ? 12 : 60;
+  TP.plane = desc->n[0] * desc->n[1] * desc->n[2];
+  TP.ghost_t = (desc->flags & FTK_GHOST_PLANE) ? desc->t0 + desc->nt - 1 : -1;
+  TP.first_t = desc->t0 > 0 ? desc->t0 : -1;
+  TP.cross = reinterpret_cast<long long*>(ws + L.cross);
+  TP.exportA = reinterpret_cast<long long*>(ws + L.exportA);
+  TP.exportB = reinterpret_cast<long long*>(ws + L.exportB);
+  return TP;
+}
+
+// status of a finished call from its device counters (range, capacities, the 0/2 invariant)
+static int result_status(const ftk_desc* desc, const unsigned long long* host_cnt, const Layout& L, int64_t capacity,
+                         int64_t* n_out) {
+  int st;
+  st = range_status(desc, host_cnt[CNT_MAXBITS]);
+  if (st) return st;
+  const unsigned long long wmax = std::max(std::max(host_cnt[CNT_WIN], host_cnt[CNT_CUBES]), host_cnt[CNT_WIN_MAX]);
+  if ((i64)wmax > L.wcap) {  // survivors beyond the survivor / cube lists were not tested
+    *n_out = std::max<int64_t>(*n_out, (int64_t)wmax);
+    return FTK_ERR_CAPACITY;
+  }
+  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity ||
+      (i64)host_cnt[CNT_CROSS] > capacity || (i64)host_cnt[CNT_EXPORT_B] > capacity)
+    return FTK_ERR_CAPACITY;
+  if (host_cnt[CNT_INVARIANT]) {
+    g_last_error = "cells with a punctured-face count not in {0, 2}: " + std::to_string(host_cnt[CNT_INVARIANT]);
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
+static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
+               void* d_ws, size_t ws_bytes, cudaStream_t stream, bool track) {
+  int st = validate(desc);
+  if (st) return st;
+  if (!d_field || !n_out || !d_ws || capacity < 0 || capacity > kMaxCapacity || (capacity > 0 && !d_out))
+    return FTK_ERR_INVALID_ARG;
+  const Layout L = layout(capacity, esz_of(desc));
+  if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
+  char* ws = static_cast<char*>(d_ws);
+  auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  Events ev;
+  ev.rec(0, stream);
+  FTK_CUDA_TRY(cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), stream));
+
+  ExtractParams EP = extract_params(desc, d_field, d_out, capacity, ws, L, counters, track);
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
   if (ev.on) cudaEventRecord(ev.e[4], stream);  // a recorded default for paths that skip K1a
   ev.rec(1, stream);
@@ -217,27 +272,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   if (st) return st;
   ev.rec(2, stream);
   if (track) {
-    TrackParams TP;
-    TP.rec = d_out;
-    TP.capacity = capacity;
-    TP.counters = counters;
-    TP.table = reinterpret_cast<int*>(ws + L.table);
-    TP.table_cap = L.hcap;
-    TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
-    TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
-    TP.inserted = k1_insert;
-    TP.prelinked = desc->ndim == 2;
-    TP.diag = getenv("FTK_PASS2_DIAG") ? atoi(getenv("FTK_PASS2_DIAG")) : 0;
-    TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
-    TP.fid = reinterpret_cast<i64*>(ws + L.fid);
-    TP.parent = reinterpret_cast<int*>(ws + L.parent);
-    TP.T = desc->ndim == 2 ? 12 : 60;
-    TP.plane = desc->n[0] * desc->n[1] * desc->n[2];
-    TP.ghost_t = (desc->flags & FTK_GHOST_PLANE) ? desc->t0 + desc->nt - 1 : -1;
-    TP.first_t = desc->t0 > 0 ? desc->t0 : -1;
-    TP.cross = reinterpret_cast<long long*>(ws + L.cross);
-    TP.exportA = reinterpret_cast<long long*>(ws + L.exportA);
-    TP.exportB = reinterpret_cast<long long*>(ws + L.exportB);
+    TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters, EP.table != nullptr);
     const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
     st = launch_track(TP, desc->ndim, ext, stream);
     if (st) return st;
@@ -276,21 +311,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   ftk_num_faces(desc, &g_stats[0]);
   g_stats[1] = (int64_t)host_cnt[CNT_SURVIVORS];
   g_stats[2] = (int64_t)host_cnt[CNT_NOUT];
-  st = range_status(desc, host_cnt[CNT_MAXBITS]);
-  if (st) return st;
-  if ((i64)host_cnt[CNT_WIN] > L.wcap || (i64)host_cnt[CNT_CUBES] > L.wcap) {
-    // survivors beyond the survivor / cube lists were not tested
-    *n_out = std::max<int64_t>(*n_out, (int64_t)std::max(host_cnt[CNT_WIN], host_cnt[CNT_CUBES]));
-    return FTK_ERR_CAPACITY;
-  }
-  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity ||
-      (i64)host_cnt[CNT_CROSS] > capacity || (i64)host_cnt[CNT_EXPORT_B] > capacity)
-    return FTK_ERR_CAPACITY;
-  if (host_cnt[CNT_INVARIANT]) {
-    g_last_error = "cells with a punctured-face count not in {0, 2}: " + std::to_string(host_cnt[CNT_INVARIANT]);
-    return FTK_ERR_INVARIANT;
-  }
-  return FTK_OK;
+  return result_status(desc, host_cnt, L, capacity, n_out);
 }
 
 
@@ -581,6 +602,73 @@ static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, 
 
 using namespace ftk;
 
+
+// ------------------------------------------------------------------------------ streaming ingestion
+// push_field_data (traversal of the spacetime mesh one timestep after another):
+// the caller pushes timesteps one at a time; the tracker stages them in a window of W + 1 planes and
+// runs pass 1 (K1) on every full window -- anchors [t0, t0 + W) with plane t0 + W as the ghost plane,
+// exactly the time-slab rule of DESIGN.md 7 -- then keeps the last plane as the first of the next
+// window.  Records, their compact face ids, in-cube unions and trajectory edges accumulate in the
+// caller's buffers across windows (record indices are global), so finish() runs pass 2 once over
+// everything: the labels equal those of one ftk_cp_track over the whole field, while the field
+// itself never has to be resident.
+struct ftk_tracker {
+  ftk_desc desc;        // spatial extents, dtype, scale; nt / t0 / nt_global / flags set per window
+  int window;
+  ftk_cp* out;
+  int64_t capacity;
+  char* ws;
+  Layout L;
+  char* buf;            // window + 1 planes, contiguous in time
+  size_t plane_bytes;
+  int64_t buf_t0;       // global timestep of buffer plane 0
+  int nbuf;             // planes in the buffer
+  int64_t pushed;       // timesteps pushed so far
+  cudaStream_t stream;
+  int error;            // first error of an enqueue (sticky, reported by finish)
+};
+
+static constexpr int64_t kOpenEnd = (1ll << 30) - 2;  // nt_global of a window that is not the last
+
+// per-window survivor-list counters: fold into the sticky maximum, then reset
+__global__ void k_window_reset(unsigned long long* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const unsigned long long w = c[CNT_WIN] > c[CNT_CUBES] ? c[CNT_WIN] : c[CNT_CUBES];
+    if (w > c[CNT_WIN_MAX]) c[CNT_WIN_MAX] = w;
+    c[CNT_WORK] = 0;
+    c[CNT_WIN] = 0;
+    c[CNT_CUBES] = 0;
+  }
+}
+
+static size_t tracker_ws(const ftk_desc* d, int64_t capacity, int window) {
+  const size_t plane = (size_t)d->n[0] * d->n[1] * d->n[2] * esz_of(d);
+  return align_up(layout(capacity, esz_of(d)).total, 256) + (size_t)(window + 1) * plane;
+}
+
+// pass 1 over the staged planes: a ghost window (not last) or the final window
+static int tracker_window(ftk_tracker* tr, bool last) {
+  ftk_desc c = tr->desc;
+  c.t0 = tr->buf_t0;
+  c.nt = tr->nbuf;
+  c.nt_global = last ? tr->pushed : kOpenEnd;
+  c.flags = last ? 0u : FTK_GHOST_PLANE;
+  auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
+  k_window_reset<<<1, 32, 0, tr->stream>>>(counters);
+  FTK_CUDA_TRY(cudaGetLastError());
+  ExtractParams EP = extract_params(&c, tr->buf, tr->out, tr->capacity, tr->ws, tr->L, counters, true);
+  EP.table = nullptr;
+  int st = c.ndim == 2 ? launch_extract2d(EP, tr->stream) : launch_extract3d(EP, tr->stream);
+  if (st) return st;
+  if (!last) {  // the ghost plane becomes plane 0 of the next window
+    FTK_CUDA_TRY(cudaMemcpyAsync(tr->buf, tr->buf + (size_t)(tr->nbuf - 1) * tr->plane_bytes, tr->plane_bytes,
+                                 cudaMemcpyDeviceToDevice, tr->stream));
+    tr->buf_t0 += tr->nbuf - 1;
+    tr->nbuf = 1;
+  }
+  return FTK_OK;
+}
+
 extern "C" {
 
 int ftk_abi_version(void) { return FTK_ABI_VERSION; }
@@ -711,6 +799,97 @@ int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, 
   if (st) return st;
   FTK_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, (size_t)*n_out * sizeof(ftk_cp), cudaMemcpyDeviceToHost, s));
   FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  return FTK_OK;
+}
+
+int ftk_tracker_workspace_size(const ftk_desc* desc, int64_t capacity, int32_t window, size_t* bytes) {
+  if (!desc || !bytes || window < 1 || capacity < 0 || capacity > kMaxCapacity) return FTK_ERR_INVALID_ARG;
+  ftk_desc c = *desc;
+  c.t0 = 0;
+  c.nt = 2;
+  c.nt_global = 2;
+  c.flags = 0;
+  const int st = validate(&c);
+  if (st) return st;
+  *bytes = tracker_ws(&c, capacity, window);
+  return FTK_OK;
+}
+
+int ftk_tracker_begin(ftk_tracker** out, const ftk_desc* desc, int32_t window, ftk_cp* d_out, int64_t capacity,
+                      void* d_ws, size_t ws_bytes, ftk_stream stream) {
+  size_t need = 0;
+  if (!out) return FTK_ERR_INVALID_ARG;
+  int st = ftk_tracker_workspace_size(desc, capacity, window, &need);
+  if (st) return st;
+  if (!d_ws || ws_bytes < need || (capacity > 0 && !d_out)) return FTK_ERR_INVALID_ARG;
+  auto* tr = new (std::nothrow) ftk_tracker();
+  if (!tr) return FTK_ERR_NOMEM;
+  tr->desc = *desc;
+  tr->desc.t0 = 0;
+  tr->desc.flags = 0;
+  tr->window = window;
+  tr->out = d_out;
+  tr->capacity = capacity;
+  tr->ws = static_cast<char*>(d_ws);
+  tr->L = layout(capacity, esz_of(desc));
+  tr->buf = tr->ws + align_up(tr->L.total, 256);
+  tr->plane_bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * esz_of(desc);
+  tr->stream = reinterpret_cast<cudaStream_t>(stream);
+  auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
+  const cudaError_t e = cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), tr->stream);
+  if (e != cudaSuccess) {
+    delete tr;
+    return set_cuda_error(e, "ftk_tracker_begin");
+  }
+  *out = tr;
+  return FTK_OK;
+}
+
+int ftk_tracker_push(ftk_tracker* tr, const void* plane) {
+  if (!tr || !plane) return FTK_ERR_INVALID_ARG;
+  if (tr->error) return tr->error;
+  if (tr->pushed + 1 >= kOpenEnd) return FTK_ERR_INVALID_ARG;
+  cudaError_t e = cudaMemcpyAsync(tr->buf + (size_t)tr->nbuf * tr->plane_bytes, plane, tr->plane_bytes,
+                                  cudaMemcpyDefault, tr->stream);
+  if (e != cudaSuccess) return tr->error = set_cuda_error(e, "ftk_tracker_push");
+  ++tr->nbuf;
+  ++tr->pushed;
+  if (tr->nbuf == tr->window + 1) {
+    const int st = tracker_window(tr, false);
+    if (st) return tr->error = st;
+  }
+  return FTK_OK;
+}
+
+int ftk_tracker_finish(ftk_tracker* tr, int64_t* n_out) {
+  if (!tr || !n_out) return FTK_ERR_INVALID_ARG;
+  std::unique_ptr<ftk_tracker> own(tr);
+  if (tr->error) return tr->error;
+  if (tr->pushed < 2) return FTK_ERR_INVALID_ARG;  // tracking needs two timesteps
+  int st = tracker_window(tr, true);
+  if (st) return st;
+  ftk_desc f = tr->desc;
+  f.t0 = 0;
+  f.nt = tr->pushed;
+  f.nt_global = tr->pushed;
+  f.flags = 0;
+  auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
+  TrackParams TP = track_params(&f, tr->out, tr->capacity, tr->ws, tr->L, counters, false);
+  const i64 ext[4] = {f.n[0], f.n[1], f.n[2], f.nt_global};
+  st = launch_track(TP, f.ndim, ext, tr->stream);
+  if (st) return st;
+  unsigned long long host_cnt[CNT_N];
+  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, sizeof host_cnt, cudaMemcpyDeviceToHost, tr->stream));
+  FTK_CUDA_TRY(cudaStreamSynchronize(tr->stream));
+  *n_out = (int64_t)host_cnt[CNT_NOUT];
+  ftk_num_faces(&f, &g_stats[0]);
+  g_stats[1] = (int64_t)host_cnt[CNT_SURVIVORS];
+  g_stats[2] = (int64_t)host_cnt[CNT_NOUT];
+  return result_status(&f, host_cnt, tr->L, tr->capacity, n_out);
+}
+
+int ftk_tracker_abort(ftk_tracker* tr) {
+  delete tr;
   return FTK_OK;
 }
 
