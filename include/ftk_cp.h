@@ -130,10 +130,10 @@ FTK_API int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_
 FTK_API int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
                  int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream, ftk_comm* comm);
 
-/* End-to-end variant from HOST memory: h_field is a host buffer (pinned for overlap) of the whole
- * input; the library streams it to d_stage (device buffer of the field's size) in time chunks,
- * overlapping the copies with pass 1, runs track, and copies the records to h_out (host array of
- * `capacity` records). */
+/* End-to-end variant from HOST memory: h_field is a host buffer (pinned for full PCIe speed) of the
+ * whole input; the library copies it to d_stage (device buffer of the field's size) on `stream`,
+ * runs track, and copies the records to h_out (host array of `capacity` records).  The streaming
+ * tracker below is the variant that never holds the whole field on the device. */
 FTK_API int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, ftk_cp* d_out,
                       ftk_cp* h_out, int64_t capacity, int64_t* n_out, void* d_ws, size_t ws_bytes,
                       ftk_stream stream);

@@ -238,15 +238,18 @@ class Tracker:
     whole field, with only window + 1 planes resident on the device.  `capacity` bounds the records
     of the whole stream (FtkError with FTK_ERR_CAPACITY otherwise)."""
 
-    def __init__(self, spatial_shape, dtype, scale_log2: int, capacity: int, window: int = 64, device="cuda"):
+    def __init__(self, spatial_shape, dtype, scale_log2: int, capacity: int, window: int = 64, device="cuda",
+                 records: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
         self.device = torch.device(device)
         self.desc = make_desc((2, *spatial_shape), dtype, scale_log2)
         self.capacity = int(capacity)
-        b = ctypes.c_size_t(0)
-        _check(lib().ftk_tracker_workspace_size(ctypes.byref(self.desc), self.capacity, window, ctypes.byref(b)),
-               "ftk_tracker_workspace_size")
-        self.records = torch.empty(max(self.capacity, 1) * RECORD_BYTES, dtype=torch.uint8, device=self.device)
-        self.workspace = torch.empty(b.value, dtype=torch.uint8, device=self.device)
+        need = self.workspace_bytes(spatial_shape, dtype, scale_log2, capacity, window)
+        # caller-owned buffers may be passed in (reused across streams), else allocated here
+        if records is None or records.numel() < max(self.capacity, 1) * RECORD_BYTES:
+            records = torch.empty(max(self.capacity, 1) * RECORD_BYTES, dtype=torch.uint8, device=self.device)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=self.device)
+        self.records, self.workspace = records, workspace
         self.dtype = torch.float32 if self.desc.dtype == F32 else torch.float64
         self.spatial_shape = tuple(spatial_shape)
         self._h = ctypes.c_void_p(0)
@@ -256,6 +259,14 @@ class Tracker:
                                        ctypes.c_void_p(self.records.data_ptr()), self.capacity,
                                        ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
                                        ctypes.c_void_p(_stream_ptr(self.device))), "ftk_tracker_begin")
+
+    @staticmethod
+    def workspace_bytes(spatial_shape, dtype, scale_log2: int, capacity: int, window: int) -> int:
+        desc = make_desc((2, *spatial_shape), dtype, scale_log2)
+        b = ctypes.c_size_t(0)
+        _check(lib().ftk_tracker_workspace_size(ctypes.byref(desc), int(capacity), window, ctypes.byref(b)),
+               "ftk_tracker_workspace_size")
+        return b.value
 
     def push(self, plane: torch.Tensor):
         if self._h is None:
