@@ -191,6 +191,73 @@ class MovingExtremum:
         return out
 
 
+@dataclass
+class DoubleGyre:
+    """2D time-varying vector field [t][y][x][2] (u, v interleaved) of the double gyre (PAPER.md:509-511:
+    domain [0,2] x [0,1], timesteps 0.1 apart): u = -pi A sin(pi f) cos(pi y),
+    v = pi A cos(pi f) sin(pi y) df/dx, f = a(t) x^2 + b(t) x, a = eps sin(w t), b = 1 - 2 eps sin(w t);
+    the common parameters A = 0.1, eps = 0.25, w = 2 pi / 10 (our choice; the paper gives none)."""
+    nx: int
+    ny: int
+    nt: int
+    dt: float = 0.1
+    A: float = 0.1
+    eps: float = 0.25
+    omega: float = 2.0 * math.pi / 10.0
+    scale_log2: int = 26
+
+    def plane(self, t_global: int, device="cpu") -> torch.Tensor:
+        t = t_global * self.dt
+        xs = torch.arange(self.nx, dtype=torch.float64, device=device) * (2.0 / (self.nx - 1))
+        ys = torch.arange(self.ny, dtype=torch.float64, device=device) * (1.0 / (self.ny - 1))
+        Y, X = torch.meshgrid(ys, xs, indexing="ij")
+        a = self.eps * math.sin(self.omega * t)
+        b = 1.0 - 2.0 * a
+        f = a * X * X + b * X
+        dfdx = 2.0 * a * X + b
+        u = -math.pi * self.A * torch.sin(math.pi * f) * torch.cos(math.pi * Y)
+        v = math.pi * self.A * torch.cos(math.pi * f) * torch.sin(math.pi * Y) * dfdx
+        return torch.stack([u, v], dim=-1)
+
+    def generate(self, t0: int = 0, nt: int | None = None, device="cpu", dtype=torch.float32):
+        nt = self.nt - t0 if nt is None else nt
+        out = torch.empty((nt, self.ny, self.nx, 2), dtype=dtype, device=device)
+        for k in range(nt):
+            out[k] = self.plane(t0 + k, device).to(dtype)
+        return out
+
+
+@dataclass
+class MovingLinear:
+    """2D vector field v(x, t) = A (x - c(t)), c(t) = c0 + w t, on integer grid coordinates: the PL
+    field is exactly linear, so its one zero per timestep is c(t) and its type is A's (source, sink,
+    saddle, spiral, centre).  Dyadic c and integer A with scale 2^8 keep every value exact in fp32."""
+    n: tuple
+    nt: int
+    A: tuple            # ((a, b), (c, d))
+    c0: tuple
+    w: tuple
+    scale_log2: int = 8
+
+    def center(self, t: float):
+        return tuple(c + vv * t for c, vv in zip(self.c0, self.w))
+
+    def plane(self, t_global: int, device="cpu") -> torch.Tensor:
+        cx, cy = self.center(t_global)
+        xs = torch.arange(self.n[0], dtype=torch.float64, device=device) - cx
+        ys = torch.arange(self.n[1], dtype=torch.float64, device=device) - cy
+        Y, X = torch.meshgrid(ys, xs, indexing="ij")
+        (a, b), (c, d) = self.A
+        return torch.stack([a * X + b * Y, c * X + d * Y], dim=-1)
+
+    def generate(self, t0: int = 0, nt: int | None = None, device="cpu", dtype=torch.float32):
+        nt = self.nt - t0 if nt is None else nt
+        out = torch.empty((nt, self.n[1], self.n[0], 2), dtype=dtype, device=device)
+        for k in range(nt):
+            out[k] = self.plane(t0 + k, device).to(dtype)
+        return out
+
+
 def random_degenerate(shape, values=(-1.0, 0.0, 1.0), seed=0, dtype=torch.float32):
     """Massively degenerate field: every vertex value drawn from a tiny set (ties everywhere)."""
     g = torch.Generator().manual_seed(seed)

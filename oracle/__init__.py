@@ -19,7 +19,7 @@ _SRC = os.path.join(_HERE, "ftk_oracle.c")
 _LIB = os.path.join(_HERE, "libftk_oracle.so")
 
 OK, INVALID_ARG, RANGE, CAPACITY, INVARIANT, NOMEM = 0, 1, 2, 3, 6, 7
-DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX = 0, 1, 2, 3, 4, 5
+DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX, SOURCE, SINK, CENTER = 0, 1, 2, 3, 4, 5, 6, 7, 8
 FL_ORDINAL, FL_BOUNDARY, FL_DEGEN_LOC = 1, 2, 4
 
 CP_DTYPE = np.dtype(
@@ -40,6 +40,7 @@ class _Desc(ctypes.Structure):
         ("ndim", ctypes.c_int32), ("dtype", ctypes.c_int32), ("n", ctypes.c_int64 * 3),
         ("nt", ctypes.c_int64), ("t0", ctypes.c_int64), ("nt_global", ctypes.c_int64),
         ("scale_log2", ctypes.c_int32), ("nthreads", ctypes.c_int32),
+        ("kind", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
 
@@ -116,11 +117,18 @@ def cvt(v: int) -> float:
     return lib().ftko_cvt(hi, lo)
 
 
-def _desc(field: np.ndarray, scale_log2: int, t0: int, nt_global: int | None, nthreads: int):
+def _desc(field: np.ndarray, scale_log2: int, t0: int, nt_global: int | None, nthreads: int,
+          vector: bool = False):
+    """vector=True: a 2D vector field [t][y][x][2] (components interleaved), tracked as given."""
     if field.dtype not in (np.float32, np.float64):
         raise TypeError("field must be float32 or float64")
     field = np.ascontiguousarray(field)
-    if field.ndim == 3:
+    if vector:
+        if field.ndim != 4 or field.shape[3] != 2:
+            raise ValueError("vector field must be [t][y][x][2]")
+        nt, ny, nx, _ = field.shape
+        nz, ndim = 1, 2
+    elif field.ndim == 3:
         nt, ny, nx = field.shape
         nz, ndim = 1, 2
     elif field.ndim == 4:
@@ -137,13 +145,14 @@ def _desc(field: np.ndarray, scale_log2: int, t0: int, nt_global: int | None, nt
     d.nt_global = nt_global if nt_global is not None else t0 + nt
     d.scale_log2 = scale_log2
     d.nthreads = nthreads
+    d.kind = 1 if vector else 0
     return d, field
 
 
 def extract(field: np.ndarray, scale_log2: int, t0: int = 0, nt_global: int | None = None,
-            ta: int | None = None, tb: int | None = None, nthreads: int = 0):
+            ta: int | None = None, tb: int | None = None, nthreads: int = 0, vector: bool = False):
     """Pass 1 over anchors with global t in [ta, tb). Returns (records sorted by face_id, n_faces)."""
-    d, field = _desc(field, scale_log2, t0, nt_global, nthreads)
+    d, field = _desc(field, scale_log2, t0, nt_global, nthreads, vector)
     ta = t0 if ta is None else ta
     tb = min(t0 + d.nt, d.nt_global) if tb is None else tb
     n_out = ctypes.c_int64(0)
@@ -160,9 +169,9 @@ def extract(field: np.ndarray, scale_log2: int, t0: int = 0, nt_global: int | No
     return out[: n_out.value], n_faces.value
 
 
-def track(field: np.ndarray, scale_log2: int, nthreads: int = 0, check: bool = True):
+def track(field: np.ndarray, scale_log2: int, nthreads: int = 0, check: bool = True, vector: bool = False):
     """Full two-pass tracking. Returns (records sorted by face_id with labels, n_faces, stats)."""
-    d, field = _desc(field, scale_log2, 0, None, nthreads)
+    d, field = _desc(field, scale_log2, 0, None, nthreads, vector)
     n_out = ctypes.c_int64(0)
     n_faces = ctypes.c_int64(0)
     stats = np.zeros(4, np.int64)

@@ -50,8 +50,10 @@ typedef __int128 i128;
 /* status codes (values chosen to match the C-ABI's documented meanings; defined independently) */
 enum { FTKO_OK = 0, FTKO_INVALID_ARG = 1, FTKO_RANGE = 2, FTKO_CAPACITY = 3,
        FTKO_INVARIANT = 6, FTKO_NOMEM = 7 };
-/* critical point types (maxima, minima, saddles of the gradient field) */
-enum { CP_DEGENERATE = 0, CP_MIN = 1, CP_SADDLE = 2, CP_SADDLE1 = 3, CP_SADDLE2 = 4, CP_MAX = 5 };
+/* critical point types (maxima, minima, saddles of the gradient field; sources, sinks and
+ * saddles of a vector field, with centres where the Jacobian's trace vanishes) */
+enum { CP_DEGENERATE = 0, CP_MIN = 1, CP_SADDLE = 2, CP_SADDLE1 = 3, CP_SADDLE2 = 4, CP_MAX = 5,
+       CP_SOURCE = 6, CP_SINK = 7, CP_CENTER = 8 };
 /* record flags */
 enum { FL_ORDINAL = 1, FL_BOUNDARY = 2, FL_DEGEN_LOC = 4 };
 
@@ -64,6 +66,9 @@ typedef struct {
   int64_t nt_global; /* global number of timesteps */
   int32_t scale_log2;
   int32_t nthreads;  /* 0 = OpenMP default */
+  int32_t kind;      /* 0 = scalar field (its gradient is tracked); 1 = vector field: n
+                        components per vertex, interleaved ([t][y][x][n]), tracked as given; 2D only */
+  int32_t pad_;
 } ftko_desc;
 
 typedef struct {     /* 56 bytes */
@@ -266,11 +271,13 @@ static int64_t bidx(const ctx_t* C, const int64_t* c) {
 static int in_buffer_t(const ctx_t* C, int64_t t) { return t >= C->D->t0 && t < C->D->t0 + C->D->nt; }
 
 static int64_t qat(const ctx_t* C, const int64_t* c) { return C->q[bidx(C, c)]; }
+/* vector fields: component j of the quantized vector at c */
+static int64_t qcomp(const ctx_t* C, const int64_t* c, int j) { return C->q[bidx(C, c) * C->n + j]; }
 
 /* step 1: quantize the whole buffer */
 static int quantize_all(ctx_t* C, const void* field) {
   const ftko_desc* D = C->D;
-  int64_t nv = D->n[0] * D->n[1] * D->n[2] * D->nt;
+  int64_t nv = D->n[0] * D->n[1] * D->n[2] * D->nt * (D->kind == 1 ? C->n : 1); /* values */
   double bound = ldexp(1.0, C->n == 2 ? 59 : 38);
   int bad = 0;
 #pragma omp parallel for reduction(| : bad) schedule(static)
@@ -338,6 +345,37 @@ static void hessian(const ctx_t* C, const int64_t* c, int64_t* H) {
         H[k++] = qat(C, pp) - qat(C, pm) - qat(C, mp) + qat(C, mm);
       }
     }
+}
+
+/* Vector fields: Jacobian at a vertex ("the (spatial) Jacobian"), the gradient rule of step
+ * 2 applied to every component: J[j][a] = q_j[+a] - q_j[-a] (2x the derivative), one-sided doubled
+ * at the spatial boundary.  Order J[j * n + a]: u_x, u_y, v_x, v_y. */
+static void jacobian(const ctx_t* C, const int64_t* c, int64_t* J) {
+  int n = C->n;
+  for (int j = 0; j < n; j++)
+    for (int a = 0; a < n; a++) {
+      int64_t N = C->D->n[a];
+      int64_t lo[MAXD], hi[MAXD];
+      memcpy(lo, c, sizeof lo);
+      memcpy(hi, c, sizeof hi);
+      int64_t f = 1;
+      if (c[a] == 0) { hi[a] = 1; lo[a] = 0; f = 2; }
+      else if (c[a] == N - 1) { hi[a] = N - 1; lo[a] = N - 2; f = 2; }
+      else { hi[a] = c[a] + 1; lo[a] = c[a] - 1; }
+      J[j * n + a] = f * (qcomp(C, hi, j) - qcomp(C, lo, j));
+    }
+}
+
+/* Vector-field type from the mu-interpolated Jacobian (2D; "sources, sinks, and saddles"):
+ * det < 0 saddle; det > 0: trace > 0 source, trace < 0 sink, trace == 0 centre; det == 0
+ * degenerate (reading R17).  No tolerance. */
+static int classify_vec(const double* Jb) {
+  double a = Jb[0], b = Jb[1], c = Jb[2], d = Jb[3];
+  double det = a * d - b * c;
+  double tr = a + d;
+  if (det < 0) return CP_SADDLE;
+  if (det > 0) return tr > 0 ? CP_SOURCE : (tr < 0 ? CP_SINK : CP_CENTER);
+  return CP_DEGENERATE;
 }
 
 /* step 6: type from the mu-interpolated Hessian ("based on the eigensystem"; reading R9) */
@@ -451,11 +489,13 @@ static int test_face(const ctx_t* C, const int64_t* anchor, int type, ftko_cp* r
     pos[a] = acc;
   }
   /* step 6: type */
-  int nh = n == 2 ? 3 : 6;
-  double Hb[6];
+  const int vec = C->D->kind == 1;
+  int nh = vec ? n * n : (n == 2 ? 3 : 6);
+  double Hb[9];
   for (int k = 0; k <= n; k++) {
-    int64_t H[6];
-    hessian(C, verts[k], H);
+    int64_t H[9];
+    if (vec) jacobian(C, verts[k], H);
+    else hessian(C, verts[k], H);
     for (int e = 0; e < nh; e++) {
       double term = mu[k] * (double)H[e];
       Hb[e] = k == 0 ? term : Hb[e] + term;
@@ -470,7 +510,7 @@ static int test_face(const ctx_t* C, const int64_t* anchor, int type, ftko_cp* r
   rec->y = pos[1];
   rec->z = n == 3 ? pos[2] : 0.0;
   rec->t = pos[d - 1];
-  rec->type = classify(n, Hb);
+  rec->type = vec ? classify_vec(Hb) : classify(n, Hb);
   rec->flags = flags;
   return 1;
 }
@@ -495,6 +535,8 @@ static int check_desc(const ftko_desc* D) {
   if (D->ndim == 3 ? D->n[2] < 3 : D->n[2] != 1) return 0;
   if (D->nt < 1 || D->t0 < 0 || D->t0 + D->nt > D->nt_global) return 0;
   if (D->scale_log2 < -64 || D->scale_log2 > 64) return 0;
+  if (D->kind != 0 && D->kind != 1) return 0;
+  if (D->kind == 1 && D->ndim != 2) return 0; /* vector fields: 2D for now */
   return 1;
 }
 
@@ -511,6 +553,13 @@ static int setup(ctx_t* C, const ftko_desc* D, const void* field) {
   if (D->nthreads > 0) omp_set_num_threads(D->nthreads);
 #endif
   int64_t nv = D->n[0] * D->n[1] * D->n[2] * D->nt;
+  if (D->kind == 1) {
+    /* vector field: the quantized components ARE the tracked field (no gradient step) */
+    C->q = (int64_t*)malloc((size_t)nv * C->n * sizeof(int64_t));
+    if (!C->q) return FTKO_NOMEM;
+    C->g = C->q;
+    return quantize_all(C, field);
+  }
   C->q = (int64_t*)malloc((size_t)nv * sizeof(int64_t));
   C->g = (int64_t*)malloc((size_t)nv * C->n * sizeof(int64_t));
   if (!C->q || !C->g) return FTKO_NOMEM;
@@ -520,7 +569,10 @@ static int setup(ctx_t* C, const ftko_desc* D, const void* field) {
   return FTKO_OK;
 }
 
-static void teardown(ctx_t* C) { free(C->q); free(C->g); }
+static void teardown(ctx_t* C) {
+  if (C->g != C->q) free(C->g);
+  free(C->q);
+}
 
 /* Pass 1 over anchors with global t in [ta, tb): all faces in canonical order. */
 static int pass1(const ctx_t* C, int64_t ta, int64_t tb, vec_t* out, int64_t* n_faces) {
