@@ -271,7 +271,7 @@ def random_degenerate(shape, values=(-1.0, 0.0, 1.0), seed=0, dtype=torch.float3
 @dataclass
 class Config:
     name: str
-    kind: str          # woven2d | moving3d | woven3d
+    kind: str          # woven2d | moving3d | woven3d | gyre2d (vector field)
     shape: tuple       # (nx, ny, [nz,] nt)
     scale_log2: int
     desc: str
@@ -283,6 +283,9 @@ class Config:
         if self.kind == "woven3d":
             nx, ny, nz, T = self.shape
             return Woven(nx, ny, nt or T, nz=nz, scale_log2=self.scale_log2)
+        if self.kind == "gyre2d":
+            nx, ny, T = self.shape
+            return DoubleGyre(nx, ny, nt or T, scale_log2=self.scale_log2)
         if self.kind == "moving3d":
             nx, ny, nz, T = self.shape
             return MovingExtremum((nx, ny, nz), nt or T, c0=(60.0, 62.0, 64.0), v=(0.25, 0.125, -0.0625),
@@ -296,5 +299,7 @@ CONFIGS = {
     "C3": Config("C3", "moving3d", (128, 128, 128, 32), 8, "3D moving extremum 128^3x32"),
     "C4": Config("C4", "woven2d", (4096, 4096, 512), 26, "2D woven 4096^2x512, time-slab strong scaling"),
     "C5": Config("C5", "woven3d", (256, 256, 256, 64), 26, "3D woven 256^3x64 per GPU, weak scaling"),
+    # SURVEY.md 8(f) NEXT row 2 (vector-field input); not a BASELINE.json config
+    "V2": Config("V2", "gyre2d", (2048, 1024, 256), 26, "2D double-gyre vector field 2048x1024x256 (vector path)"),
 }
 

@@ -23,8 +23,8 @@ LIB_PATH = os.environ.get("FTK_LIB") or os.path.join(_HERE, "libftk_cp.so")
 
 OK, ERR_INVALID_ARG, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_INVARIANT, ERR_NOMEM = range(8)
 F32, F64 = 0, 1
-DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX = range(6)
-GHOST_PLANE, SORTED = 1, 2
+DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX, SOURCE, SINK, CENTER = range(9)
+GHOST_PLANE, SORTED, VECTOR_FIELD = 1, 2, 4
 CP_ORDINAL, CP_BOUNDARY, CP_DEGENERATE_LOC = 1, 2, 4
 
 RECORD_DTYPE = np.dtype(
@@ -103,10 +103,16 @@ def lib() -> ctypes.CDLL:
 
 
 def make_desc(shape, dtype, scale_log2: int, t0: int = 0, nt_global: int | None = None,
-              ghost: bool = False, sorted_output: bool = False) -> Desc:
-    """shape: [t][y][x] (2D) or [t][z][y][x] (3D)."""
+              ghost: bool = False, sorted_output: bool = False, vector: bool = False) -> Desc:
+    """shape: [t][y][x] (2D scalar), [t][z][y][x] (3D scalar) or, with vector=True, [t][y][x][2] (2D
+    vector field, components interleaved; FTK_VECTOR_FIELD)."""
     d = Desc()
-    if len(shape) == 3:
+    if vector:
+        if len(shape) != 4 or shape[3] != 2:
+            raise ValueError("vector field must be [t][y][x][2]")
+        nt, ny, nx, _ = shape
+        nz, d.ndim = 1, 2
+    elif len(shape) == 3:
         nt, ny, nx = shape
         nz, d.ndim = 1, 2
     elif len(shape) == 4:
@@ -124,7 +130,7 @@ def make_desc(shape, dtype, scale_log2: int, t0: int = 0, nt_global: int | None 
     d.nt, d.t0 = nt, t0
     d.nt_global = t0 + nt if nt_global is None else nt_global
     d.scale_log2 = scale_log2
-    d.flags = (GHOST_PLANE if ghost else 0) | (SORTED if sorted_output else 0)
+    d.flags = (GHOST_PLANE if ghost else 0) | (SORTED if sorted_output else 0) | (VECTOR_FIELD if vector else 0)
     return d
 
 
@@ -171,12 +177,12 @@ def _stream_ptr(device) -> int:
 
 
 def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global, capacity, ghost,
-         buffers: Buffers | None, comm=None, sorted_output=False):
+         buffers: Buffers | None, comm=None, sorted_output=False, vector=False):
     if not field.is_cuda:
         raise FtkError(ERR_INVALID_ARG, f"{fn_name}: field must be a CUDA tensor (no CPU fallback)")
     if not field.is_contiguous():
         field = field.contiguous()
-    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost, sorted_output)
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost, sorted_output, vector)
     cap = capacity if capacity is not None else (buffers.capacity if buffers else default_capacity(field))
     while True:
         if buffers is None or buffers.capacity < cap:
@@ -201,18 +207,19 @@ def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global,
 
 def extract(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
             capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
-            return_buffers: bool = False):
+            return_buffers: bool = False, vector: bool = False):
     """Pass 1: punctured faces of the buffer's owned timesteps (label = -1).
     Returns an int64 [n, 7] device tensor of 56-byte records (see RECORD_DTYPE)."""
-    rec, buf = _run("ftk_cp_extract", field, scale_log2, t0, nt_global, capacity, ghost, buffers)
+    rec, buf = _run("ftk_cp_extract", field, scale_log2, t0, nt_global, capacity, ghost, buffers, vector=vector)
     return (rec, buf) if return_buffers else rec
 
 
 def track(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
           capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
-          comm=None, return_buffers: bool = False):
-    """Pass 1 + pass 2: punctured faces labelled with their trajectory (min face_id)."""
-    rec, buf = _run("ftk_cp_track", field, scale_log2, t0, nt_global, capacity, ghost, buffers, comm)
+          comm=None, return_buffers: bool = False, vector: bool = False):
+    """Pass 1 + pass 2: punctured faces labelled with their trajectory (min face_id).  vector=True:
+    field is a 2D vector field [t][y][x][2] whose own zeros are tracked."""
+    rec, buf = _run("ftk_cp_track", field, scale_log2, t0, nt_global, capacity, ghost, buffers, comm, vector=vector)
     return (rec, buf) if return_buffers else rec
 
 
@@ -239,11 +246,11 @@ class Tracker:
     of the whole stream (FtkError with FTK_ERR_CAPACITY otherwise)."""
 
     def __init__(self, spatial_shape, dtype, scale_log2: int, capacity: int, window: int = 64, device="cuda",
-                 records: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+                 records: torch.Tensor | None = None, workspace: torch.Tensor | None = None, vector: bool = False):
         self.device = torch.device(device)
-        self.desc = make_desc((2, *spatial_shape), dtype, scale_log2)
+        self.desc = make_desc((2, *spatial_shape), dtype, scale_log2, vector=vector)
         self.capacity = int(capacity)
-        need = self.workspace_bytes(spatial_shape, dtype, scale_log2, capacity, window)
+        need = self.workspace_bytes(spatial_shape, dtype, scale_log2, capacity, window, vector)
         # caller-owned buffers may be passed in (reused across streams), else allocated here
         if records is None or records.numel() < max(self.capacity, 1) * RECORD_BYTES:
             records = torch.empty(max(self.capacity, 1) * RECORD_BYTES, dtype=torch.uint8, device=self.device)
@@ -261,8 +268,9 @@ class Tracker:
                                        ctypes.c_void_p(_stream_ptr(self.device))), "ftk_tracker_begin")
 
     @staticmethod
-    def workspace_bytes(spatial_shape, dtype, scale_log2: int, capacity: int, window: int) -> int:
-        desc = make_desc((2, *spatial_shape), dtype, scale_log2)
+    def workspace_bytes(spatial_shape, dtype, scale_log2: int, capacity: int, window: int,
+                        vector: bool = False) -> int:
+        desc = make_desc((2, *spatial_shape), dtype, scale_log2, vector=vector)
         b = ctypes.c_size_t(0)
         _check(lib().ftk_tracker_workspace_size(ctypes.byref(desc), int(capacity), window, ctypes.byref(b)),
                "ftk_tracker_workspace_size")

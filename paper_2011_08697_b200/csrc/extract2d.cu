@@ -1371,8 +1371,10 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
     k_table_prep<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
     FTK_CUDA_TRY(cudaGetLastError());
   }
-  k_expand2d<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
-  FTK_CUDA_TRY(cudaGetLastError());
+  {
+    const int st = launch_expand2d(P, stream, sms);
+    if (st) return st;
+  }
   // K1b: persistent grid over the cube list
   const size_t xsmem = sizeof(ExSmem<T>);
   auto xk = k_exact2d<T>;
@@ -1380,6 +1382,12 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   if (xg.err != cudaSuccess) return set_cuda_error(xg.err, "k_exact2d launch geometry");
   const int xper = xg.per_sm;
   xk<<<(unsigned)(sms * std::max(xper, 1)), EXW * 32, xsmem, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+int launch_expand2d(const ExtractParams& P, cudaStream_t stream, int sms) {
+  k2d::k_expand2d<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }

@@ -38,6 +38,8 @@ struct ExtractParams {
 };
 
 int launch_extract2d(const ExtractParams& P, cudaStream_t stream);
+int launch_extract_vec2d(const ExtractParams& P, cudaStream_t stream);  // 2D vector fields
+int launch_expand2d(const ExtractParams& P, cudaStream_t stream, int sms);  // group entries -> cube list
 int launch_extract3d(const ExtractParams& P, cudaStream_t stream);
 
 }  // namespace ftk

@@ -92,6 +92,9 @@ static Layout layout(i64 capacity, int esz = 8) {
 static constexpr int64_t kMaxCapacity = (1ll << 31) - 2;
 
 static int esz_of(const ftk_desc* d) { return d->dtype == FTK_F32 ? 4 : 8; }
+static bool is_vector(const ftk_desc* d) { return (d->flags & FTK_VECTOR_FIELD) != 0; }
+// bytes of one vertex's values (2 interleaved components for a vector field)
+static size_t vertex_bytes(const ftk_desc* d) { return (size_t)esz_of(d) * (is_vector(d) ? 2 : 1); }
 
 // Face types an edge can look up: the upper face of a cell, seen from the neighbour cube that owns
 // it, is the chain (0, p2, p2|p3[, p2|p3|p4]) -- its last mask misses exactly one axis.  The other
@@ -118,7 +121,8 @@ static int validate(const ftk_desc* d) {
   if (d->nt < 1 || d->t0 < 0 || d->t0 + d->nt > d->nt_global) return FTK_ERR_INVALID_ARG;
   if (d->scale_log2 < -64 || d->scale_log2 > 64) return FTK_ERR_INVALID_ARG;
   if ((d->flags & FTK_GHOST_PLANE) && d->nt < 2) return FTK_ERR_INVALID_ARG;
-  if (d->flags & ~(FTK_GHOST_PLANE | FTK_SORTED)) return FTK_ERR_INVALID_ARG;
+  if (d->flags & ~(FTK_GHOST_PLANE | FTK_SORTED | FTK_VECTOR_FIELD)) return FTK_ERR_INVALID_ARG;
+  if ((d->flags & FTK_VECTOR_FIELD) && d->ndim != 2) return FTK_ERR_INVALID_ARG;  // 2D vector fields
   if (d->n[0] * d->n[1] * d->n[2] > (1ll << 40)) return FTK_ERR_INVALID_ARG;
   return FTK_OK;
 }
@@ -179,7 +183,9 @@ static ExtractParams extract_params(const ftk_desc* desc, const void* d_field, f
   owned_range(desc, EP.ta, EP.tb);
   EP.tchunk = 32;
   EP.scale = std::ldexp(1.0, desc->scale_log2);
-  EP.thr = std::ldexp(1.0, 1 - desc->scale_log2);
+  // prefilter threshold on raw values: 2^(1-s) for the differences of the gradient stencil, 2^-s for
+  // vector components (u > 2^-s => u 2^s > 1 => rint(u 2^s) >= 1)
+  EP.thr = std::ldexp(1.0, (is_vector(desc) ? 0 : 1) - desc->scale_log2);
   EP.out = d_out;
   EP.capacity = capacity;
   EP.counters = counters;
@@ -214,7 +220,7 @@ static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t cap
   TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
   TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
   TP.inserted = k1_insert;
-  TP.prelinked = desc->ndim == 2;
+  TP.prelinked = desc->ndim == 2 && !is_vector(desc);  // the vector kernel emits all pairs as edges
   TP.diag = getenv("FTK_PASS2_DIAG") ? atoi(getenv("FTK_PASS2_DIAG")) : 0;
   TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
   TP.fid = reinterpret_cast<i64*>(ws + L.fid);
@@ -268,7 +274,8 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
   if (ev.on) cudaEventRecord(ev.e[4], stream);  // a recorded default for paths that skip K1a
   ev.rec(1, stream);
-  st = desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream);
+  st = is_vector(desc) ? launch_extract_vec2d(EP, stream)
+                       : (desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream));
   if (st) return st;
   ev.rec(2, stream);
   if (track) {
@@ -642,7 +649,7 @@ __global__ void k_window_reset(unsigned long long* c) {
 }
 
 static size_t tracker_ws(const ftk_desc* d, int64_t capacity, int window) {
-  const size_t plane = (size_t)d->n[0] * d->n[1] * d->n[2] * esz_of(d);
+  const size_t plane = (size_t)d->n[0] * d->n[1] * d->n[2] * vertex_bytes(d);
   return align_up(layout(capacity, esz_of(d)).total, 256) + (size_t)(window + 1) * plane;
 }
 
@@ -652,13 +659,14 @@ static int tracker_window(ftk_tracker* tr, bool last) {
   c.t0 = tr->buf_t0;
   c.nt = tr->nbuf;
   c.nt_global = last ? tr->pushed : kOpenEnd;
-  c.flags = last ? 0u : FTK_GHOST_PLANE;
+  c.flags = (tr->desc.flags & FTK_VECTOR_FIELD) | (last ? 0u : FTK_GHOST_PLANE);
   auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
   k_window_reset<<<1, 32, 0, tr->stream>>>(counters);
   FTK_CUDA_TRY(cudaGetLastError());
   ExtractParams EP = extract_params(&c, tr->buf, tr->out, tr->capacity, tr->ws, tr->L, counters, true);
   EP.table = nullptr;
-  int st = c.ndim == 2 ? launch_extract2d(EP, tr->stream) : launch_extract3d(EP, tr->stream);
+  int st = is_vector(&c) ? launch_extract_vec2d(EP, tr->stream)
+                         : (c.ndim == 2 ? launch_extract2d(EP, tr->stream) : launch_extract3d(EP, tr->stream));
   if (st) return st;
   if (!last) {  // the ghost plane becomes plane 0 of the next window
     FTK_CUDA_TRY(cudaMemcpyAsync(tr->buf, tr->buf + (size_t)(tr->nbuf - 1) * tr->plane_bytes, tr->plane_bytes,
@@ -793,7 +801,7 @@ int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, 
   if (!h_field || !d_stage || !h_out || !n_out) return FTK_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t esz = desc->dtype == FTK_F32 ? 4 : 8;
-  const size_t bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * desc->nt * esz;
+  const size_t bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * desc->nt * esz * (is_vector(desc) ? 2 : 1);
   FTK_CUDA_TRY(cudaMemcpyAsync(d_stage, h_field, bytes, cudaMemcpyHostToDevice, s));
   st = run(desc, d_stage, d_out, capacity, n_out, d_ws, ws_bytes, s, true);
   if (st) return st;
@@ -808,7 +816,7 @@ int ftk_tracker_workspace_size(const ftk_desc* desc, int64_t capacity, int32_t w
   c.t0 = 0;
   c.nt = 2;
   c.nt_global = 2;
-  c.flags = 0;
+  c.flags &= FTK_VECTOR_FIELD;
   const int st = validate(&c);
   if (st) return st;
   *bytes = tracker_ws(&c, capacity, window);
@@ -826,14 +834,14 @@ int ftk_tracker_begin(ftk_tracker** out, const ftk_desc* desc, int32_t window, f
   if (!tr) return FTK_ERR_NOMEM;
   tr->desc = *desc;
   tr->desc.t0 = 0;
-  tr->desc.flags = 0;
+  tr->desc.flags &= FTK_VECTOR_FIELD;
   tr->window = window;
   tr->out = d_out;
   tr->capacity = capacity;
   tr->ws = static_cast<char*>(d_ws);
   tr->L = layout(capacity, esz_of(desc));
   tr->buf = tr->ws + align_up(tr->L.total, 256);
-  tr->plane_bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * esz_of(desc);
+  tr->plane_bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * vertex_bytes(desc);
   tr->stream = reinterpret_cast<cudaStream_t>(stream);
   auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
   const cudaError_t e = cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), tr->stream);
@@ -872,7 +880,7 @@ int ftk_tracker_finish(ftk_tracker* tr, int64_t* n_out) {
   f.t0 = 0;
   f.nt = tr->pushed;
   f.nt_global = tr->pushed;
-  f.flags = 0;
+  f.flags = tr->desc.flags & FTK_VECTOR_FIELD;
   auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
   TrackParams TP = track_params(&f, tr->out, tr->capacity, tr->ws, tr->L, counters, false);
   const i64 ext[4] = {f.n[0], f.n[1], f.n[2], f.nt_global};
