@@ -131,7 +131,7 @@ def cpu_baseline(cfg, seconds_budget: float = 20.0):
     f = w.generate(nt=nt_s).numpy()
     cores = os.cpu_count() or 1
     t = time.perf_counter()
-    rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+    rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
     dt = time.perf_counter() - t
     return {"value": nf / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"oracle track (plain C, OpenMP {cores} threads) on {'x'.join(map(str, spatial))}x{nt_s} "
@@ -161,7 +161,7 @@ def run_reference(args):
     while True:
         f = f_full[:, :rows, :].copy()
         t = time.perf_counter()
-        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
         dt = time.perf_counter() - t
         if dt > per_step * 0.5 or rows >= ny:
             break
@@ -169,7 +169,7 @@ def run_reference(args):
     times = []
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
-        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores)
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
         dt = time.perf_counter() - t
         if i >= args.warmup:
             times.append(dt)
@@ -206,6 +206,7 @@ def run_ours(args):
 
     cfg = fi.CONFIGS[args.config]
     spatial, nt = cfg.shape[:-1], cfg.shape[-1]
+    vec = cfg.kind == "gyre2d"  # 2D vector field (FTK_VECTOR_FIELD), SURVEY.md 8(f) NEXT row 2
     w = cfg.make()
     if world > 1:
         nt_global = nt * world
@@ -216,7 +217,8 @@ def run_ours(args):
     else:
         nt_global, t0, ghost, nbuf = nt, 0, False, nt
     field = w.generate(t0=t0, nt=nbuf, device=dev)
-    desc = ftk.make_desc(tuple(field.shape), field.dtype, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost)
+    desc = ftk.make_desc(tuple(field.shape), field.dtype, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost,
+                         vector=vec)
     faces = ftk.num_faces(desc)
     # multi-GPU: trajectories crossing slab seams are stitched inside ftk_cp_track (NCCL allgather of
     # the seam pairs, host union, device relabel)
@@ -225,11 +227,12 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(dev)
     ftk.set_profiling(False)
-    rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, comm=cptr, return_buffers=True)
+    rec, buf = ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, comm=cptr, return_buffers=True,
+                         vector=vec)
     n_punct = rec.shape[0]
     # warmup
     for _ in range(args.warmup):
-        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
+        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr, vector=vec)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -237,7 +240,7 @@ def run_ours(args):
     with ClockSampler(dev.index or 0) as clk:
         start.record(stream)
         for _ in range(args.steps):
-            ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
+            ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr, vector=vec)
         stop.record(stream)
         torch.cuda.synchronize(dev)
     ms_total = start.elapsed_time(stop)
@@ -246,7 +249,7 @@ def run_ours(args):
     k1_ms, p2_ms, st_ms, ka_ms, kb_ms = [], [], [], [], []
     ftk.set_profiling(True)
     for _ in range(max(3, min(args.steps, 30))):
-        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
+        ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr, vector=vec)
         ms4, st3 = ftk.last_timings()
         km = ftk.last_kernel_timings()
         ka_ms.append(km[0])
@@ -260,7 +263,7 @@ def run_ours(args):
         with ClockSampler(dev.index or 0) as clk2:
             t_end = time.perf_counter() + 0.3
             while time.perf_counter() < t_end:
-                ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr)
+                ftk.track(field, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr, vector=vec)
             torch.cuda.synchronize(dev)
         clk.samples += clk2.samples
         clk.reasons |= clk2.reasons
@@ -287,12 +290,13 @@ def run_ours(args):
     kb_avg = sum(kb_ms) / len(kb_ms)
     _, st3 = ftk.last_timings()
     n_surv = st3[1]
-    alg_bytes = field.numel() * esz + (16 if field.dim() == 4 else 12) * n_surv
+    alg_bytes = field.numel() * esz + (16 if (field.dim() == 4 and not vec) else 12) * n_surv
     achieved = alg_bytes / (ka_avg / 1000.0) / 1e9
     peak, peak_src = _peaks()
-    d3 = field.dim() == 4
-    kscan, kexact = ("k_scan3d", "k_exact3d") if d3 else ("k_scan2d", "k_exact2d")
-    win_bytes = (256 if d3 else 32) * esz  # the exact kernel's window per survivor: 4x4[x4]x2 values
+    d3 = field.dim() == 4 and not vec
+    kscan, kexact = ("k_scan3d", "k_exact3d") if d3 else (("k_scanvec2d", "k_exactvec2d") if vec else ("k_scan2d", "k_exact2d"))
+    # the exact kernel's window per survivor: 4x4[x4]x2 values (scalar), the 8 corner vectors (vector)
+    win_bytes = (256 if d3 else (16 if vec else 32)) * esz
     traffic = _ncu_traffic(cfg.name, kscan)
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
@@ -301,12 +305,12 @@ def run_ours(args):
         host = field.cpu().pin_memory()
         out_host = torch.empty(buf.capacity * ftk.RECORD_BYTES, dtype=torch.uint8).pin_memory()
         stage = torch.empty_like(field)
-        n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host)  # warm
+        n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host, vector=vec)  # warm
         e_steps = max(3, min(args.steps, 20))
         torch.cuda.synchronize(dev)
         t = time.perf_counter()
         for _ in range(e_steps):
-            n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host)
+            n = ftk.track_host(host, cfg.scale_log2, stage, buf, out_host, vector=vec)
         e_ms = (time.perf_counter() - t) * 1000.0 / e_steps
         e2e = {"value": faces / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": field.numel() * esz, "d2h_bytes_per_step": n * ftk.RECORD_BYTES + 64}
@@ -320,12 +324,12 @@ def run_ours(args):
         host = field.cpu().pin_memory()
         planes = [host[t] for t in range(host.shape[0])]
         sp = tuple(field.shape[1:])
-        ws = torch.empty(ftk.Tracker.workspace_bytes(sp, field.dtype, cfg.scale_log2, buf.capacity, window),
+        ws = torch.empty(ftk.Tracker.workspace_bytes(sp, field.dtype, cfg.scale_log2, buf.capacity, window, vec),
                          dtype=torch.uint8, device=dev)
 
         def one_stream():
             tr = ftk.Tracker(sp, field.dtype, cfg.scale_log2, buf.capacity, window=window,
-                             records=buf.records, workspace=ws)
+                             records=buf.records, workspace=ws, vector=vec)
             for p in planes:
                 tr.push(p)
             return tr.finish().shape[0]

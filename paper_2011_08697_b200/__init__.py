@@ -224,10 +224,10 @@ def track(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | No
 
 
 def track_host(field_host: torch.Tensor, scale_log2: int, stage: torch.Tensor, buffers: Buffers,
-               out_host: torch.Tensor):
+               out_host: torch.Tensor, vector: bool = False):
     """End-to-end from host memory (pinned for speed): H2D inside the call, records copied back to
     out_host (uint8 [capacity * 56], pinned).  Returns the record count."""
-    desc = make_desc(tuple(field_host.shape), field_host.dtype, scale_log2)
+    desc = make_desc(tuple(field_host.shape), field_host.dtype, scale_log2, vector=vector)
     n_out = ctypes.c_int64(0)
     st = lib().ftk_cp_track_host(
         ctypes.byref(desc), ctypes.c_void_p(field_host.data_ptr()), ctypes.c_void_p(stage.data_ptr()),

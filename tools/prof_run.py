@@ -8,10 +8,11 @@ name = sys.argv[1] if len(sys.argv) > 1 else 'C2'
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cfg = fi.CONFIGS[name]
 f = cfg.make().generate(device='cuda')
+vec = cfg.kind == 'gyre2d'
 ftk.set_profiling(True)
-rec, buf = ftk.track(f, cfg.scale_log2, return_buffers=True)
+rec, buf = ftk.track(f, cfg.scale_log2, return_buffers=True, vector=vec)
 for i in range(reps):
-    rec = ftk.track(f, cfg.scale_log2, buffers=buf)
+    rec = ftk.track(f, cfg.scale_log2, buffers=buf, vector=vec)
     ms, st = ftk.last_timings()
     km = ftk.last_kernel_timings()
     print(f'{name} rep {i}: k1 {ms[0]:.3f} ms (k1a {km[0]:.3f} k1b {km[1]:.3f}) pass2 {ms[1]:.3f} ms call {ms[3]:.3f} ms faces {st[0]} survivors {st[1]} punctured {st[2]}')

@@ -8,6 +8,10 @@ VARIANTS = {
     "mixhash": ["FTK_LOCAL_HASH=0"],
     "xminb2": ["FTK_X_MINB=2"],
     "xminb4": ["FTK_X_MINB=4"],
+    "vminb3": ["FTK_V_MINB=3"],
+    "vminb4": ["FTK_V_MINB=4"],
+    "vminb6": ["FTK_V_MINB=6"],
+    "vminb8": ["FTK_V_MINB=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
