@@ -219,6 +219,40 @@ FTK_API int ftk_tracker_push(ftk_tracker* tracker, const void* plane);
 FTK_API int ftk_tracker_finish(ftk_tracker* tracker, int64_t* n_out);
 FTK_API int ftk_tracker_abort(ftk_tracker* tracker);
 
+/* Trajectory post-processing (P:419 slicing; P:470-479 filtering and type smoothing) over the labelled
+ * records d_rec[0, n) of ONE ftk_cp_track call on the whole domain described by desc, with the
+ * workspace of that call (d_ws, ws_bytes, capacity; n <= capacity; its hash table, face-id and scratch
+ * regions are reused, so the workspace must not be in use by another call).  All arrays are device
+ * memory; every call is synchronous with respect to stream (one device->host read).
+ *   adjacency: d_nbr[2 i], d_nbr[2 i + 1] = record index of the partner of record i in each of its (at
+ *     most two) parent cells (closed-form side_of), -1 where the parent cell lies outside the domain.
+ *     A trajectory is thereby a path (two ends with one -1) or a loop.  FTK_ERR_INVARIANT if a parent
+ *     cell does not hold exactly one partner.  Must precede filter on the same workspace.
+ *   slice: the trajectories at time t0: every record with t == t0 (copied), and for every adjacent pair
+ *     whose t values strictly straddle t0 the point on their straight segment (the zero set inside the
+ *     cell) at t0 -- x = x_lo + s (x_hi - x_lo), s = (t0 - t_lo) / (t_hi - t_lo), FP64, no FMA --
+ *     carrying the face id, label and type of the end nearer in t (the earlier one on a tie), flags 0.
+ *     Where several faces share one location (a trajectory through a grid vertex, the SoS case) the
+ *     point is reported once per such face.
+ *   filter: copies the records of the trajectories whose time extent (max t - min t over its records)
+ *     is >= min_duration and, with drop_loops, that are not loops.
+ *   smooth_types: for every record, up to half_window records are visited along the trajectory on each
+ *     side; if both sides are non-empty and all visited records share one type T different from the
+ *     record's own, its type becomes T (decided on the unmodified types, then applied; in place).
+ *   slice / filter write up to cap records to d_out and set *n_out to the full count (FTK_ERR_CAPACITY
+ *   when it exceeds cap); the output order is unspecified. */
+FTK_API int ftk_post_adjacency(const ftk_desc* desc, const ftk_cp* d_rec, int64_t n, int64_t* d_nbr, void* d_ws,
+                               size_t ws_bytes, int64_t capacity, ftk_stream stream);
+FTK_API int ftk_post_slice(const ftk_desc* desc, const ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double t0,
+                           ftk_cp* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                           int64_t capacity, ftk_stream stream);
+FTK_API int ftk_post_filter(const ftk_desc* desc, const ftk_cp* d_rec, const int64_t* d_nbr, int64_t n,
+                            double min_duration, int32_t drop_loops, ftk_cp* d_out, int64_t cap, int64_t* n_out,
+                            void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream);
+FTK_API int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n,
+                                  int32_t half_window, void* d_ws, size_t ws_bytes, int64_t capacity,
+                                  ftk_stream stream);
+
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);

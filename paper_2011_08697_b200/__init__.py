@@ -41,6 +41,7 @@ EXPORTS = [
     "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
     "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
+    "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types",
 ]
 
 
@@ -98,6 +99,11 @@ def lib() -> ctypes.CDLL:
         L.ftk_tracker_push.argtypes = [P, P]
         L.ftk_tracker_finish.argtypes = [P, P]
         L.ftk_tracker_abort.argtypes = [P]
+        SZ = ctypes.c_size_t
+        L.ftk_post_adjacency.argtypes = [PD, P, I64, P, P, SZ, I64, P]
+        L.ftk_post_slice.argtypes = [PD, P, P, I64, ctypes.c_double, P, I64, P, P, SZ, I64, P]
+        L.ftk_post_filter.argtypes = [PD, P, P, I64, ctypes.c_double, ctypes.c_int32, P, I64, P, P, SZ, I64, P]
+        L.ftk_post_smooth_types.argtypes = [PD, P, P, I64, ctypes.c_int32, P, SZ, I64, P]
         _lib = L
     return _lib
 
@@ -302,6 +308,53 @@ class Tracker:
         if getattr(self, "_h", None):
             lib().ftk_tracker_abort(self._h)
             self._h = None
+
+
+class Trajectories:
+    """Post-processing of the labelled records of one track() call (PAPER.md:419, 470-479;
+    include/ftk_cp.h ftk_post_*): adjacency along the trajectories, slicing at a time t0, filtering by
+    duration / loops, type smoothing.  `buffers` are the ones the track call used (return_buffers=True);
+    `shape` is the tracked field's shape."""
+
+    def __init__(self, rec: torch.Tensor, buffers: Buffers, shape, dtype, scale_log2: int, vector: bool = False):
+        self.rec = rec
+        self.buffers = buffers
+        self.desc = make_desc(tuple(shape), dtype, scale_log2, vector=vector)
+        self.n = rec.shape[0]
+        self.nbr = torch.empty((max(self.n, 1), 2), dtype=torch.int64, device=rec.device)
+        _check(lib().ftk_post_adjacency(ctypes.byref(self.desc), ctypes.c_void_p(rec.data_ptr()), self.n,
+                                        ctypes.c_void_p(self.nbr.data_ptr()), *self._ws()), "ftk_post_adjacency")
+
+    def _ws(self):
+        b = self.buffers
+        return (ctypes.c_void_p(b.workspace.data_ptr()), b.workspace.numel(), b.capacity,
+                ctypes.c_void_p(_stream_ptr(self.rec.device)))
+
+    def _out(self, fn, *args):
+        cap = max(self.n, 16)
+        while True:
+            out = torch.empty(cap * RECORD_BYTES, dtype=torch.uint8, device=self.rec.device)
+            n_out = ctypes.c_int64(0)
+            st = fn(ctypes.byref(self.desc), ctypes.c_void_p(self.rec.data_ptr()), ctypes.c_void_p(self.nbr.data_ptr()),
+                    self.n, *args, ctypes.c_void_p(out.data_ptr()), cap, ctypes.byref(n_out), *self._ws())
+            if st == ERR_CAPACITY:
+                cap = n_out.value
+                continue
+            _check(st, fn.__name__)
+            return out[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
+
+    def slice(self, t0: float) -> torch.Tensor:
+        return self._out(lib().ftk_post_slice, ctypes.c_double(t0))
+
+    def filter(self, min_duration: float, drop_loops: bool = False) -> torch.Tensor:
+        return self._out(lib().ftk_post_filter, ctypes.c_double(min_duration), 1 if drop_loops else 0)
+
+    def smooth_types(self, half_window: int = 2) -> torch.Tensor:
+        """in place on the records (half-window of two in the paper's experiments)"""
+        _check(lib().ftk_post_smooth_types(ctypes.byref(self.desc), ctypes.c_void_p(self.rec.data_ptr()),
+                                           ctypes.c_void_p(self.nbr.data_ptr()), self.n, half_window, *self._ws()),
+               "ftk_post_smooth_types")
+        return self.rec
 
 
 def to_numpy(rec: torch.Tensor) -> np.ndarray:

@@ -30,6 +30,7 @@ enum Counter : int {
   CNT_HMASK = 10,     // pass 2: hash-table slot mask in use (set before the first insert)
   CNT_CUBES = 11,     // 2D: surviving cubes expanded from K1a's group entries (may exceed wcap)
   CNT_WIN_MAX = 12,   // streaming: max of CNT_WIN / CNT_CUBES over the chunks already processed
+  CNT_POST = 13,      // post-processing: output records (slice / filter)
   CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
   CNT_N = 32
 };

@@ -901,6 +901,101 @@ int ftk_tracker_abort(ftk_tracker* tr) {
   return FTK_OK;
 }
 
+// ------------------------------------------------------------------------------ post-processing
+static int post_setup(const ftk_desc* desc, int64_t n, void* d_ws, size_t ws_bytes, int64_t capacity, Layout& L) {
+  int st = validate(desc);
+  if (st) return st;
+  if (!d_ws || n < 0 || capacity < 0 || capacity > kMaxCapacity || n > capacity) return FTK_ERR_INVALID_ARG;
+  L = layout(capacity, esz_of(desc));
+  if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
+  return FTK_OK;
+}
+
+int ftk_post_adjacency(const ftk_desc* desc, const ftk_cp* d_rec, int64_t n, int64_t* d_nbr, void* d_ws,
+                       size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+  Layout L;
+  int st = post_setup(desc, n, d_ws, ws_bytes, capacity, L);
+  if (st) return st;
+  if (n > 0 && (!d_rec || !d_nbr)) return FTK_ERR_INVALID_ARG;
+  char* ws = static_cast<char*>(d_ws);
+  auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TrackParams TP = track_params(desc, const_cast<ftk_cp*>(d_rec), n, ws, L, counters, false);
+  FTK_CUDA_TRY(cudaMemsetAsync(counters + CNT_INVARIANT, 0, sizeof(u64), s));
+  const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
+  st = launch_post_adjacency(TP, desc->ndim, ext, n, reinterpret_cast<long long*>(d_nbr), s);
+  if (st) return st;
+  unsigned long long bad = 0;
+  FTK_CUDA_TRY(cudaMemcpyAsync(&bad, counters + CNT_INVARIANT, sizeof bad, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad) {
+    g_last_error = "post_adjacency: parent cells without exactly one partner: " + std::to_string(bad);
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
+static int post_op(int op, const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double t0,
+                   double dmin, int drop_loops, int half_window, ftk_cp* d_out, int64_t cap, int64_t* n_out,
+                   void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+  Layout L;
+  int st = post_setup(desc, n, d_ws, ws_bytes, capacity, L);
+  if (st) return st;
+  if (n > 0 && (!d_rec || !d_nbr)) return FTK_ERR_INVALID_ARG;
+  if (op != 2 && (!n_out || cap < 0 || (cap > 0 && !d_out))) return FTK_ERR_INVALID_ARG;
+  char* ws = static_cast<char*>(d_ws);
+  auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TrackParams TP = track_params(desc, d_rec, n, ws, L, counters, false);
+  PostCall c;
+  c.rec = d_rec;
+  c.rec_mut = d_rec;
+  c.nbr = reinterpret_cast<const long long*>(d_nbr);
+  c.n = n;
+  c.out = d_out;
+  c.cap = cap;
+  c.count = counters + CNT_POST;
+  c.scratch = reinterpret_cast<long long*>(ws + L.map);
+  c.t0 = t0;
+  c.dmin = dmin;
+  c.drop_loops = drop_loops;
+  c.half_window = half_window;
+  FTK_CUDA_TRY(cudaMemsetAsync(counters + CNT_POST, 0, sizeof(u64), s));
+  if (n > 0) {
+    st = launch_post(TP, op, c, s);
+    if (st) return st;
+  }
+  unsigned long long cnt = 0;
+  FTK_CUDA_TRY(cudaMemcpyAsync(&cnt, counters + CNT_POST, sizeof cnt, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  if (op == 2) return FTK_OK;
+  *n_out = (int64_t)cnt;
+  return (int64_t)cnt > cap ? FTK_ERR_CAPACITY : FTK_OK;
+}
+
+int ftk_post_slice(const ftk_desc* desc, const ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double t0,
+                   ftk_cp* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes, int64_t capacity,
+                   ftk_stream stream) {
+  if (!(t0 == t0)) return FTK_ERR_INVALID_ARG;
+  return post_op(0, desc, const_cast<ftk_cp*>(d_rec), d_nbr, n, t0, 0.0, 0, 0, d_out, cap, n_out, d_ws, ws_bytes,
+                 capacity, stream);
+}
+
+int ftk_post_filter(const ftk_desc* desc, const ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double min_duration,
+                    int32_t drop_loops, ftk_cp* d_out, int64_t cap, int64_t* n_out, void* d_ws, size_t ws_bytes,
+                    int64_t capacity, ftk_stream stream) {
+  if (!(min_duration == min_duration)) return FTK_ERR_INVALID_ARG;
+  return post_op(1, desc, const_cast<ftk_cp*>(d_rec), d_nbr, n, 0.0, min_duration, drop_loops != 0, 0, d_out, cap,
+                 n_out, d_ws, ws_bytes, capacity, stream);
+}
+
+int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, int32_t half_window,
+                          void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+  if (half_window < 1) return FTK_ERR_INVALID_ARG;
+  return post_op(2, desc, d_rec, d_nbr, n, 0.0, 0.0, 0, half_window, nullptr, 0, nullptr, d_ws, ws_bytes, capacity,
+                 stream);
+}
+
 int ftk_set_profiling(int enable) {
   g_profiling = enable;
   return FTK_OK;

@@ -388,7 +388,7 @@ __device__ __forceinline__ i64 encode(const Geo<D>& G, const i64* v, int m_idx) 
 // number of OTHER punctured faces of the cell given as a chain of D+1 cumulative masks w[0..D]
 template <int D>
 __device__ __forceinline__ int visit_cell(const TrackParams& P, u64 hm, const Geo<D>& G, const i64* A, const int* w,
-                                          i64 self) {
+                                          i64 self, long long* partner = nullptr) {
   int hits = 0;
 #pragma unroll
   for (int j = 0; j <= D; ++j) {
@@ -414,18 +414,33 @@ __device__ __forceinline__ int visit_cell(const TrackParams& P, u64 hm, const Ge
     }
     const i64 f = encode<D>(G, anc, idx);
     if (f == self) continue;
-    hits += lookup(P, hm, f) >= 0;
+    const long long r = lookup(P, hm, f);
+    if (r >= 0) {
+      ++hits;
+      if (partner) *partner = r;
+    }
   }
   return hits;
 }
 
-template <int D>
-__global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) {
+// Parent cells of every record in closed form (side_of): ADJ = false checks that each
+// holds exactly one other punctured face (FTK_VERIFY_LINK); ADJ = true writes that partner's record
+// index to nbr[2 i + k] (k-th existing parent cell; -1: no parent cell, i.e. the domain boundary).
+template <int D, bool ADJ = false>
+__global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G, long long* nbr = nullptr) {
   const i64 n = n_records(P);
   const u64 hm = table_mask(P);
   constexpr int FULL = (1 << D) - 1;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i64 self = P.fid[i];
+    int ns = 0;
+    auto cell = [&](const i64* anc, const int* w) {
+      long long partner = -1;
+      const int h = visit_cell<D>(P, hm, G, anc, w, self, &partner);
+      if (ADJ) nbr[2 * i + ns++] = h == 1 ? partner : -1;
+      return h != 1;
+    };
+    if (ADJ) nbr[2 * i] = nbr[2 * i + 1] = -1;
     i64 v[4];
     int type;
     decode<D>(G, self, v, type);
@@ -443,7 +458,7 @@ __global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) 
 #pragma unroll
         for (int k = 1; k < D; ++k) w[k] = m[k];
         w[D] = FULL;
-        bad |= visit_cell<D>(P, hm, G, v, w, self) != 1;
+        bad |= cell(v, w);
       }
       if (v[c] >= 1) {  // parent 2: prepend v0 - e_c (anchor moves down)
         i64 A[4];
@@ -453,7 +468,7 @@ __global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) 
         w[0] = 0;
 #pragma unroll
         for (int k = 1; k <= D; ++k) w[k] = cbit | m[k - 1];
-        bad |= visit_cell<D>(P, hm, G, A, w, self) != 1;
+        bad |= cell(A, w);
       }
     } else {
       // the face spans all axes: one step has two axes {a, b}; the parents split it both ways
@@ -475,14 +490,207 @@ __global__ void k_verify(const __grid_constant__ TrackParams P, const Geo<D> G) 
           if (k == step) w[o++] = m[k - 1] | (which ? b : a);
           w[o++] = m[k];
         }
-        bad |= visit_cell<D>(P, hm, G, v, w, self) != 1;
+        bad |= cell(v, w);
       }
     }
     if (bad) atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
   }
 }
 
+
+// ------------------------------------------------------------------------- post-processing
+// Over the labelled records of a track call and their adjacency nbr[n][2] (partners in the parent
+// cells; a trajectory is a path or a loop of faces).  Times are non-negative, so the IEEE bits of a
+// double order like the values.
+__global__ void k_post_prep(const __grid_constant__ TrackParams P, long long n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_NOUT] = (unsigned long long)n;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    P.fid[i] = P.rec[i].face_id;
+}
+
+struct PostArgs {
+  const ftk_cp* rec;
+  const long long* nbr;
+  long long n;
+  ftk_cp* out;
+  long long cap;
+  unsigned long long* count;  // output counter
+  long long* tmin;            // [n] per trajectory root record: min / max t (double bits), open ends
+  long long* tmax;
+  long long* nends;
+  int* newtype;               // [n]
+  double t0, dmin;
+  int drop_loops, half_window;
+};
+
+__device__ __forceinline__ void post_emit(const PostArgs& A, const ftk_cp& r) {
+  const unsigned long long k = atomicAdd(A.count, 1ull);
+  if (k < (unsigned long long)A.cap) A.out[k] = r;
+}
+
+// slice at t = t0: records with t == t0, and the point of every trajectory segment (the
+// straight segment between the two punctured faces of a cell) that strictly straddles t0
+__global__ void k_post_slice(const __grid_constant__ PostArgs A) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const ftk_cp a = A.rec[i];
+    if (a.t == A.t0) post_emit(A, a);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const long long j = A.nbr[2 * i + k];
+      if (j <= i) continue;  // each segment once
+      ftk_cp lo = a, hi = A.rec[j];
+      if (lo.t > hi.t) {
+        const ftk_cp tmp = lo;
+        lo = hi;
+        hi = tmp;
+      }
+      if (!(lo.t < A.t0 && A.t0 < hi.t)) continue;
+      const double s = __ddiv_rn(__dsub_rn(A.t0, lo.t), __dsub_rn(hi.t, lo.t));
+      ftk_cp r = __dsub_rn(A.t0, lo.t) <= __dsub_rn(hi.t, A.t0) ? lo : hi;  // type / id of the nearer end
+      r.x = __dadd_rn(lo.x, __dmul_rn(s, __dsub_rn(hi.x, lo.x)));
+      r.y = __dadd_rn(lo.y, __dmul_rn(s, __dsub_rn(hi.y, lo.y)));
+      r.z = __dadd_rn(lo.z, __dmul_rn(s, __dsub_rn(hi.z, lo.z)));
+      r.t = A.t0;
+      r.flags = 0;
+      post_emit(A, r);
+    }
+  }
+}
+
+// per-trajectory attributes: time extent and open ends, keyed by the root record (the one whose
+// face id is the label)
+__global__ void k_post_stats(const __grid_constant__ TrackParams P, const __grid_constant__ PostArgs A) {
+  const u64 hm = table_mask(P);
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const long long root = lookup(P, hm, A.rec[i].label);
+    if (root < 0) {
+      atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
+      continue;
+    }
+    const long long tb = __double_as_longlong(A.rec[i].t);
+    atomicMin(reinterpret_cast<unsigned long long*>(&A.tmin[root]), (unsigned long long)tb);
+    atomicMax(reinterpret_cast<unsigned long long*>(&A.tmax[root]), (unsigned long long)tb);
+    if (A.nbr[2 * i] < 0 || A.nbr[2 * i + 1] < 0) atomicAdd(reinterpret_cast<unsigned long long*>(&A.nends[root]), 1ull);
+  }
+}
+
+__global__ void k_post_stats_init(const __grid_constant__ PostArgs A) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    A.tmin[i] = 0x7fffffffffffffffll;
+    A.tmax[i] = 0;
+    A.nends[i] = 0;
+  }
+}
+
+// filtering: keep the records of trajectories lasting >= dmin (and, with drop_loops, not
+// loops -- a loop has no open end)
+__global__ void k_post_filter(const __grid_constant__ TrackParams P, const __grid_constant__ PostArgs A) {
+  const u64 hm = table_mask(P);
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const long long root = lookup(P, hm, A.rec[i].label);
+    if (root < 0) continue;
+    const double dur = __dsub_rn(__longlong_as_double(A.tmax[root]), __longlong_as_double(A.tmin[root]));
+    const bool loop = A.nends[root] == 0;
+    if (dur >= A.dmin && !(A.drop_loops && loop)) post_emit(A, A.rec[i]);
+  }
+}
+
+// type smoothing: walk half_window records along the trajectory on each side; when both
+// sides are non-empty and every record seen has one type T != own, the record takes T.  The marks are
+// computed from the unmodified types (newtype), then applied.
+__global__ void k_post_smooth(const __grid_constant__ PostArgs A) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const int own = A.rec[i].type;
+    int T = -1, seen[2] = {0, 0};
+    bool uniform = true;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      long long prev = i, cur = A.nbr[2 * i + side];
+      for (int step = 0; step < A.half_window && cur >= 0 && cur != i; ++step) {
+        const int ty = A.rec[cur].type;
+        if (T < 0) T = ty;
+        uniform = uniform && ty == T;
+        ++seen[side];
+        const long long a = A.nbr[2 * cur], b = A.nbr[2 * cur + 1];
+        const long long nx = a == prev ? b : a;
+        prev = cur;
+        cur = nx;
+      }
+    }
+    A.newtype[i] = (seen[0] > 0 && seen[1] > 0 && uniform && T != own) ? T : own;
+  }
+}
+
+__global__ void k_post_apply_types(const __grid_constant__ PostArgs A, ftk_cp* rec) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x)
+    rec[i].type = A.newtype[i];
+}
+
 }  // namespace trk
+
+// ------------------------------------------------------------------------- post-processing launchers
+int launch_post_adjacency(const TrackParams& P0, int ndim, const i64* ext, long long n, long long* nbr,
+                          cudaStream_t stream) {
+  using namespace trk;
+  const int sms = num_sms(), threads = 256, blocks = sms * 8;
+  TrackParams P = P0;
+  P.prelinked = true;  // keep parent[]
+  P.lookup_types = ~0ull;
+  k_post_prep<<<blocks, threads, 0, stream>>>(P, n);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_clear<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_hash_insert<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  if (ndim == 2) {
+    Geo<3> G;
+    G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[3];
+    G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1];
+    k_verify<3, true><<<blocks, threads, 0, stream>>>(P, G, nbr);
+  } else {
+    Geo<4> G;
+    G.ext[0] = ext[0]; G.ext[1] = ext[1]; G.ext[2] = ext[2]; G.ext[3] = ext[3];
+    G.stride[0] = 1; G.stride[1] = ext[0]; G.stride[2] = ext[0] * ext[1]; G.stride[3] = ext[0] * ext[1] * ext[2];
+    k_verify<4, true><<<blocks, threads, 0, stream>>>(P, G, nbr);
+  }
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t stream) {
+  using namespace trk;
+  const int sms = num_sms(), threads = 256, blocks = sms * 8;
+  PostArgs A;
+  A.rec = c.rec;
+  A.nbr = c.nbr;
+  A.n = c.n;
+  A.out = c.out;
+  A.cap = c.cap;
+  A.count = c.count;
+  A.tmin = c.scratch;
+  A.tmax = c.scratch + c.n;
+  A.nends = c.scratch + 2 * c.n;
+  A.newtype = reinterpret_cast<int*>(c.scratch + 3 * c.n);
+  A.t0 = c.t0;
+  A.dmin = c.dmin;
+  A.drop_loops = c.drop_loops;
+  A.half_window = c.half_window;
+  if (op == 0) {
+    k_post_slice<<<blocks, threads, 0, stream>>>(A);
+  } else if (op == 1) {
+    k_post_stats_init<<<blocks, threads, 0, stream>>>(A);
+    FTK_CUDA_TRY(cudaGetLastError());
+    k_post_stats<<<blocks, threads, 0, stream>>>(P, A);
+    FTK_CUDA_TRY(cudaGetLastError());
+    k_post_filter<<<blocks, threads, 0, stream>>>(P, A);
+  } else {
+    k_post_smooth<<<blocks, threads, 0, stream>>>(A);
+    FTK_CUDA_TRY(cudaGetLastError());
+    k_post_apply_types<<<blocks, threads, 0, stream>>>(A, c.rec_mut);
+  }
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
 
 int launch_export(const TrackParams& P, cudaStream_t stream) {
   using namespace trk;

@@ -41,6 +41,22 @@ int launch_export(const TrackParams& P, cudaStream_t stream);
 
 // ext = {nx, ny, nz, nt_global}
 int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t stream);
+// post-processing
+struct PostCall {
+  const ftk_cp* rec;
+  ftk_cp* rec_mut;            // smoothing writes the types here (== rec)
+  const long long* nbr;       // [n][2]
+  long long n;
+  ftk_cp* out;
+  long long cap;
+  unsigned long long* count;  // device output counter
+  long long* scratch;         // [3 n] int64 + [n] int32
+  double t0, dmin;
+  int drop_loops, half_window;
+};
+int launch_post_adjacency(const TrackParams& P, int ndim, const i64* ext, long long n, long long* nbr,
+                          cudaStream_t stream);
+int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t stream);  // 0 slice, 1 filter, 2 smooth
 
 }  // namespace ftk
 
