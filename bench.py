@@ -346,6 +346,31 @@ def run_ours(args):
                        "h2d_bytes_per_step": field.numel() * esz, "timing": "wall clock, synchronised"}
         del ws, host, planes
 
+    # trajectory post-processing over this step's records: adjacency, a slice,
+    # a duration filter and type smoothing, each synchronous; wall clock per operation
+    post_line = None
+    if world == 1 and not args.no_stream and not d3:
+        rec_p, buf_p = ftk.track(field, cfg.scale_log2, buffers=buf, vector=vec, return_buffers=True)
+        rec_p = rec_p.clone()
+        tp = {}
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        tj = ftk.Trajectories(rec_p, buf_p, tuple(field.shape), field.dtype, cfg.scale_log2, vector=vec)
+        tp["adjacency_ms"] = (time.perf_counter() - t) * 1000.0
+        t = time.perf_counter()
+        n_slice = tj.slice(nt_global / 2 + 0.5).shape[0]
+        tp["slice_ms"] = (time.perf_counter() - t) * 1000.0
+        t = time.perf_counter()
+        n_filt = tj.filter(nt_global / 4, drop_loops=True).shape[0]
+        tp["filter_ms"] = (time.perf_counter() - t) * 1000.0
+        t = time.perf_counter()
+        tj.smooth_types(2)
+        torch.cuda.synchronize(dev)
+        tp["smooth_ms"] = (time.perf_counter() - t) * 1000.0
+        post_line = {**tp, "records": int(rec_p.shape[0]), "slice_points": int(n_slice), "filtered_records": int(n_filt),
+                     "timing": "wall clock per synchronous call, after one warm track"}
+        del tj, rec_p
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -369,6 +394,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "stream": stream_line,
+        "post": post_line,
         # K1a (+ k_expand2d in 2D) + K1b + k_clear + k_hash_insert + k_edges + k_label; time slabs add
         # k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
         "gpu_launches": ((6 if d3 else 7) + (6 if world > 1 else 0)) * args.steps,
