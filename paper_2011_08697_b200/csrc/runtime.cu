@@ -168,6 +168,18 @@ struct Events {  // profiling events, created once per host thread and reused
   }
 };
 
+// Pinned host copy of the device counters (one per host thread): the end-of-call read is a true
+// asynchronous D2H copy followed by one stream synchronisation (a pageable destination would stage).
+static unsigned long long* pinned_counters() {
+  thread_local unsigned long long* p = nullptr;
+  thread_local unsigned long long fallback[CNT_N];
+  if (!p && cudaHostAlloc(reinterpret_cast<void**>(&p), CNT_N * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    p = fallback;
+  }
+  return p;
+}
+
 static ExtractParams extract_params(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
                                     char* ws, const Layout& L, unsigned long long* counters, bool track) {
   ExtractParams EP;
@@ -289,8 +301,8 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     }
   }
   ev.rec(3, stream);
-  unsigned long long host_cnt[CNT_N];
-  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, sizeof host_cnt, cudaMemcpyDeviceToHost, stream));
+  unsigned long long* host_cnt = pinned_counters();
+  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
   if (getenv("FTK_PRINT_PROF")) {
@@ -886,8 +898,8 @@ int ftk_tracker_finish(ftk_tracker* tr, int64_t* n_out) {
   const i64 ext[4] = {f.n[0], f.n[1], f.n[2], f.nt_global};
   st = launch_track(TP, f.ndim, ext, tr->stream);
   if (st) return st;
-  unsigned long long host_cnt[CNT_N];
-  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, sizeof host_cnt, cudaMemcpyDeviceToHost, tr->stream));
+  unsigned long long* host_cnt = pinned_counters();
+  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, tr->stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(tr->stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
   ftk_num_faces(&f, &g_stats[0]);

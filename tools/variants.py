@@ -8,6 +8,9 @@ VARIANTS = {
     "mixhash": ["FTK_LOCAL_HASH=0"],
     "xminb2": ["FTK_X_MINB=2"],
     "xminb4": ["FTK_X_MINB=4"],
+    "s2m3": ["FTK_K1_NSTAGE=2", "FTK_K1_MINB=3"],
+    "rw4": ["FTK_K1_RW=4"],
+    "rw4m3": ["FTK_K1_RW=4", "FTK_K1_NSTAGE=3", "FTK_K1_MINB=3"],
     "vminb3": ["FTK_V_MINB=3"],
     "vminb4": ["FTK_V_MINB=4"],
     "vminb6": ["FTK_V_MINB=6"],
