@@ -124,14 +124,15 @@ def cpu_baseline(cfg, seconds_budget: float = 20.0):
     w = cfg.make()
     if len(spatial) == 3:
         # 3D: a 64^3 block of the same field kind as its own domain keeps the oracle within ~20 s
-        w = fi.Woven(64, 64, nt_s, nz=64, scale_log2=cfg.scale_log2) if cfg.kind == "woven3d" else \
+        w = fi.ABCFlow(64, 64, 64, nt_s, scale_log2=cfg.scale_log2) if cfg.kind == "abc3d" else \
+            fi.Woven(64, 64, nt_s, nz=64, scale_log2=cfg.scale_log2) if cfg.kind == "woven3d" else \
             fi.MovingExtremum((64, 64, 64), nt_s, c0=(30.0, 31.0, 32.0), v=(0.25, 0.125, -0.0625),
                               scale_log2=cfg.scale_log2)
         spatial = (64, 64, 64)
     f = w.generate(nt=nt_s).numpy()
     cores = os.cpu_count() or 1
     t = time.perf_counter()
-    rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
+    rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind in ("gyre2d", "abc3d"))
     dt = time.perf_counter() - t
     return {"value": nf / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"oracle track (plain C, OpenMP {cores} threads) on {'x'.join(map(str, spatial))}x{nt_s} "
@@ -161,7 +162,7 @@ def run_reference(args):
     while True:
         f = f_full[:, :rows, :].copy()
         t = time.perf_counter()
-        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind in ("gyre2d", "abc3d"))
         dt = time.perf_counter() - t
         if dt > per_step * 0.5 or rows >= ny:
             break
@@ -169,7 +170,7 @@ def run_reference(args):
     times = []
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
-        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind == "gyre2d")
+        rec, nf, info = oracle.track(f, cfg.scale_log2, nthreads=cores, vector=cfg.kind in ("gyre2d", "abc3d"))
         dt = time.perf_counter() - t
         if i >= args.warmup:
             times.append(dt)
@@ -206,7 +207,7 @@ def run_ours(args):
 
     cfg = fi.CONFIGS[args.config]
     spatial, nt = cfg.shape[:-1], cfg.shape[-1]
-    vec = cfg.kind == "gyre2d"  # 2D vector field (FTK_VECTOR_FIELD), SURVEY.md 8(f) NEXT row 2
+    vec = cfg.kind in ("gyre2d", "abc3d")  # vector fields (FTK_VECTOR_FIELD), SURVEY.md 8(f) NEXT row 2
     w = cfg.make()
     if world > 1:
         nt_global = nt * world
@@ -290,13 +291,16 @@ def run_ours(args):
     kb_avg = sum(kb_ms) / len(kb_ms)
     _, st3 = ftk.last_timings()
     n_surv = st3[1]
-    alg_bytes = field.numel() * esz + (16 if (field.dim() == 4 and not vec) else 12) * n_surv
+    d3 = len(spatial) == 3
+    alg_bytes = field.numel() * esz + (16 if d3 else 12) * n_surv
     achieved = alg_bytes / (ka_avg / 1000.0) / 1e9
     peak, peak_src = _peaks()
-    d3 = field.dim() == 4 and not vec
-    kscan, kexact = ("k_scan3d", "k_exact3d") if d3 else (("k_scanvec2d", "k_exactvec2d") if vec else ("k_scan2d", "k_exact2d"))
-    # the exact kernel's window per survivor: 4x4[x4]x2 values (scalar), the 8 corner vectors (vector)
-    win_bytes = (256 if d3 else (16 if vec else 32)) * esz
+    if d3:
+        kscan, kexact = ("k_scanvec3d", "k_exact3d") if vec else ("k_scan3d", "k_exact3d")
+    else:
+        kscan, kexact = ("k_scanvec2d", "k_exactvec2d") if vec else ("k_scan2d", "k_exact2d")
+    # the exact kernel's window per survivor: 4x4[x4]x2 values (scalar), the corner vectors (vector)
+    win_bytes = ((48 if vec else 256) if d3 else (16 if vec else 32)) * esz
     traffic = _ncu_traffic(cfg.name, kscan)
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)

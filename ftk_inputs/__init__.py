@@ -258,6 +258,65 @@ class MovingLinear:
         return out
 
 
+@dataclass
+class MovingLinear3:
+    """3D vector field v(x, t) = A (x - c(t)), [t][z][y][x][3]; as MovingLinear, one zero per timestep
+    at c(t), typed by the 3x3 integer matrix A."""
+    n: tuple
+    nt: int
+    A: tuple
+    c0: tuple
+    w: tuple
+    scale_log2: int = 8
+
+    def center(self, t: float):
+        return tuple(c + vv * t for c, vv in zip(self.c0, self.w))
+
+    def plane(self, t_global: int, device="cpu") -> torch.Tensor:
+        c = self.center(t_global)
+        axes = [torch.arange(N, dtype=torch.float64, device=device) - cc for N, cc in zip(self.n, c)]
+        Z, Y, X = torch.meshgrid(axes[2], axes[1], axes[0], indexing="ij")
+        comps = [self.A[j][0] * X + self.A[j][1] * Y + self.A[j][2] * Z for j in range(3)]
+        return torch.stack(comps, dim=-1)
+
+    def generate(self, t0: int = 0, nt: int | None = None, device="cpu", dtype=torch.float32):
+        nt = self.nt - t0 if nt is None else nt
+        out = torch.empty((nt, self.n[2], self.n[1], self.n[0], 3), dtype=dtype, device=device)
+        for k in range(nt):
+            out[k] = self.plane(t0 + k, device).to(dtype)
+        return out
+
+
+@dataclass
+class ABCFlow:
+    """Time-periodic 3D ABC-like flow on [0, 2 pi)^3 grid coordinates (our 3D vector workload; the paper
+    shows no 3D vector field): u = A sin z + C cos y, v = B sin x + A cos z, w = C sin y + B cos x, with
+    A = sqrt(3) + 0.5 sin(w t), B = sqrt(2), C = 1; stagnation points are isolated and move in time."""
+    nx: int
+    ny: int
+    nz: int
+    nt: int
+    dt: float = 0.1
+    scale_log2: int = 26
+
+    def plane(self, t_global: int, device="cpu") -> torch.Tensor:
+        t = t_global * self.dt
+        A, B, C = math.sqrt(3.0) + 0.5 * math.sin(2.0 * math.pi * t / 10.0), math.sqrt(2.0), 1.0
+        ax = [torch.arange(n, dtype=torch.float64, device=device) * (2.0 * math.pi / n) for n in (self.nx, self.ny, self.nz)]
+        Z, Y, X = torch.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+        u = A * torch.sin(Z) + C * torch.cos(Y)
+        v = B * torch.sin(X) + A * torch.cos(Z)
+        w = C * torch.sin(Y) + B * torch.cos(X)
+        return torch.stack([u, v, w], dim=-1)
+
+    def generate(self, t0: int = 0, nt: int | None = None, device="cpu", dtype=torch.float32):
+        nt = self.nt - t0 if nt is None else nt
+        out = torch.empty((nt, self.nz, self.ny, self.nx, 3), dtype=dtype, device=device)
+        for k in range(nt):
+            out[k] = self.plane(t0 + k, device).to(dtype)
+        return out
+
+
 def random_degenerate(shape, values=(-1.0, 0.0, 1.0), seed=0, dtype=torch.float32):
     """Massively degenerate field: every vertex value drawn from a tiny set (ties everywhere)."""
     g = torch.Generator().manual_seed(seed)
@@ -271,7 +330,7 @@ def random_degenerate(shape, values=(-1.0, 0.0, 1.0), seed=0, dtype=torch.float3
 @dataclass
 class Config:
     name: str
-    kind: str          # woven2d | moving3d | woven3d | gyre2d (vector field)
+    kind: str          # woven2d | moving3d | woven3d | gyre2d / abc3d (vector fields)
     shape: tuple       # (nx, ny, [nz,] nt)
     scale_log2: int
     desc: str
@@ -283,6 +342,9 @@ class Config:
         if self.kind == "woven3d":
             nx, ny, nz, T = self.shape
             return Woven(nx, ny, nt or T, nz=nz, scale_log2=self.scale_log2)
+        if self.kind == "abc3d":
+            nx, ny, nz, T = self.shape
+            return ABCFlow(nx, ny, nz, nt or T, scale_log2=self.scale_log2)
         if self.kind == "gyre2d":
             nx, ny, T = self.shape
             return DoubleGyre(nx, ny, nt or T, scale_log2=self.scale_log2)
@@ -301,5 +363,6 @@ CONFIGS = {
     "C5": Config("C5", "woven3d", (256, 256, 256, 64), 26, "3D woven 256^3x64 per GPU, weak scaling"),
     # SURVEY.md 8(f) NEXT row 2 (vector-field input); not a BASELINE.json config
     "V2": Config("V2", "gyre2d", (2048, 1024, 256), 26, "2D double-gyre vector field 2048x1024x256 (vector path)"),
+    "V5": Config("V5", "abc3d", (256, 256, 256, 64), 26, "3D ABC-flow vector field 256^3x64 (3D vector path)"),
 }
 

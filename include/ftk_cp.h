@@ -66,7 +66,9 @@ typedef enum {
   FTK_CP_SADDLE2 = 4, /* 3D, Morse index 2 */
   FTK_CP_MAX = 5,
   /* vector fields (FTK_VECTOR_FIELD; "sources, sinks, and saddles"), from the mu-interpolated
-   * Jacobian J: det J < 0 saddle (FTK_CP_SADDLE); det J > 0: trace > 0 source, < 0 sink, == 0 centre */
+   * Jacobian J: 2D: det J < 0 saddle (FTK_CP_SADDLE); det J > 0: trace > 0 source, < 0 sink, == 0
+   * centre.  3D: eigenvalues with positive real part by Routh-Hurwitz: none sink, all source, else
+   * saddle; an imaginary pair (a1 a2 == a3, a2 > 0) centre; det J == 0 degenerate (R17) */
   FTK_CP_SOURCE = 6,
   FTK_CP_SINK = 7,
   FTK_CP_CENTER = 8
@@ -76,9 +78,9 @@ typedef enum {
 #define FTK_GHOST_PLANE 1u      /* the buffer's last plane is a read-only ghost (time slab):
                                    faces anchored on it are tested for linking but not returned */
 #define FTK_SORTED 2u           /* return records sorted by face_id */
-#define FTK_VECTOR_FIELD 4u     /* the field is a 2D VECTOR field: 2 components per vertex,
-                                   interleaved, layout [t][y][x][2]; its own zeros are tracked (no
-                                   gradient step) and typed from its Jacobian; ndim must be 2 */
+#define FTK_VECTOR_FIELD 4u     /* the field is a VECTOR field: ndim components per vertex,
+                                   interleaved, layout [t][y][x][2] (2D) or [t][z][y][x][3] (3D); its
+                                   own zeros are tracked (no gradient step) and typed from its Jacobian */
 
 /* ftk_cp.flags */
 #define FTK_CP_ORDINAL 1u       /* all vertices in one timestep */

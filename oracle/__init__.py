@@ -119,15 +119,20 @@ def cvt(v: int) -> float:
 
 def _desc(field: np.ndarray, scale_log2: int, t0: int, nt_global: int | None, nthreads: int,
           vector: bool = False):
-    """vector=True: a 2D vector field [t][y][x][2] (components interleaved), tracked as given."""
+    """vector=True: a vector field [t][y][x][2] (2D) or [t][z][y][x][3] (3D), components interleaved,
+    tracked as given."""
     if field.dtype not in (np.float32, np.float64):
         raise TypeError("field must be float32 or float64")
     field = np.ascontiguousarray(field)
     if vector:
-        if field.ndim != 4 or field.shape[3] != 2:
-            raise ValueError("vector field must be [t][y][x][2]")
-        nt, ny, nx, _ = field.shape
-        nz, ndim = 1, 2
+        if field.ndim == 4 and field.shape[3] == 2:
+            nt, ny, nx, _ = field.shape
+            nz, ndim = 1, 2
+        elif field.ndim == 5 and field.shape[4] == 3:
+            nt, nz, ny, nx, _ = field.shape
+            ndim = 3
+        else:
+            raise ValueError("vector field must be [t][y][x][2] or [t][z][y][x][3]")
     elif field.ndim == 3:
         nt, ny, nx = field.shape
         nz, ndim = 1, 2

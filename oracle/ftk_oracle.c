@@ -366,16 +366,37 @@ static void jacobian(const ctx_t* C, const int64_t* c, int64_t* J) {
     }
 }
 
-/* Vector-field type from the mu-interpolated Jacobian (2D; "sources, sinks, and saddles"):
- * det < 0 saddle; det > 0: trace > 0 source, trace < 0 sink, trace == 0 centre; det == 0
- * degenerate (reading R17).  No tolerance. */
-static int classify_vec(const double* Jb) {
-  double a = Jb[0], b = Jb[1], c = Jb[2], d = Jb[3];
-  double det = a * d - b * c;
-  double tr = a + d;
-  if (det < 0) return CP_SADDLE;
-  if (det > 0) return tr > 0 ? CP_SOURCE : (tr < 0 ? CP_SINK : CP_CENTER);
-  return CP_DEGENERATE;
+/* Vector-field type from the mu-interpolated Jacobian ("sources, sinks, and saddles"; reading
+ * R17).  2D: det < 0 saddle; det > 0: trace > 0 source, trace < 0 sink, trace == 0 centre; det == 0
+ * degenerate.  3D: the number of eigenvalues with positive real part from the Routh-Hurwitz array of
+ * det(lambda I - J) = lambda^3 + a1 lambda^2 + a2 lambda + a3 (a1 = -tr, a2 = sum of the principal 2x2
+ * minors, a3 = -det): first column 1, a1, (a1 a2 - a3) / a1, a3, counted by sign changes -- 0 sink,
+ * 3 source, else saddle; det == 0 degenerate; zero pivots as below.  No tolerance. */
+static int classify_vec(int n, const double* Jb) {
+  if (n == 2) {
+    double a = Jb[0], b = Jb[1], c = Jb[2], d = Jb[3];
+    double det = a * d - b * c;
+    double tr = a + d;
+    if (det < 0) return CP_SADDLE;
+    if (det > 0) return tr > 0 ? CP_SOURCE : (tr < 0 ? CP_SINK : CP_CENTER);
+    return CP_DEGENERATE;
+  }
+  double a = Jb[0], b = Jb[1], c = Jb[2], d = Jb[3], e = Jb[4], f = Jb[5], g = Jb[6], h = Jb[7], k = Jb[8];
+  double tr = (a + e) + k;
+  double m2 = ((a * e - b * d) + (a * k - c * g)) + (e * k - f * h);
+  double det = (a * (e * k - f * h) - b * (d * k - f * g)) + c * (d * h - e * g);
+  if (det == 0) return CP_DEGENERATE;
+  double a1 = -tr, a2 = m2, a3 = -det;
+  double r3 = a1 * a2 - a3; /* third Routh entry times a1 */
+  /* zero pivots: a1 == 0 (eigenvalues sum to zero, det != 0) is a saddle (Routh's epsilon rule);
+   * r3 == 0 factors p = (lambda + a1)(lambda^2 + a2): an imaginary pair (a2 > 0, centre) or a
+   * real pair +-sqrt(-a2) (saddle) */
+  if (a1 == 0) return CP_SADDLE;
+  if (r3 == 0) return a2 > 0 ? CP_CENTER : CP_SADDLE;
+  int s[4] = {1, a1 > 0 ? 1 : -1, (r3 > 0) == (a1 > 0) ? 1 : -1, a3 > 0 ? 1 : -1};
+  int changes = 0;
+  for (int i = 1; i < 4; i++) changes += s[i] != s[i - 1];
+  return changes == 0 ? CP_SINK : (changes == 3 ? CP_SOURCE : CP_SADDLE);
 }
 
 /* step 6: type from the mu-interpolated Hessian ("based on the eigensystem"; reading R9) */
@@ -510,7 +531,7 @@ static int test_face(const ctx_t* C, const int64_t* anchor, int type, ftko_cp* r
   rec->y = pos[1];
   rec->z = n == 3 ? pos[2] : 0.0;
   rec->t = pos[d - 1];
-  rec->type = vec ? classify_vec(Hb) : classify(n, Hb);
+  rec->type = vec ? classify_vec(n, Hb) : classify(n, Hb);
   rec->flags = flags;
   return 1;
 }
@@ -536,7 +557,6 @@ static int check_desc(const ftko_desc* D) {
   if (D->nt < 1 || D->t0 < 0 || D->t0 + D->nt > D->nt_global) return 0;
   if (D->scale_log2 < -64 || D->scale_log2 > 64) return 0;
   if (D->kind != 0 && D->kind != 1) return 0;
-  if (D->kind == 1 && D->ndim != 2) return 0; /* vector fields: 2D for now */
   return 1;
 }
 

@@ -110,14 +110,18 @@ def lib() -> ctypes.CDLL:
 
 def make_desc(shape, dtype, scale_log2: int, t0: int = 0, nt_global: int | None = None,
               ghost: bool = False, sorted_output: bool = False, vector: bool = False) -> Desc:
-    """shape: [t][y][x] (2D scalar), [t][z][y][x] (3D scalar) or, with vector=True, [t][y][x][2] (2D
-    vector field, components interleaved; FTK_VECTOR_FIELD)."""
+    """shape: [t][y][x] (2D scalar), [t][z][y][x] (3D scalar) or, with vector=True, [t][y][x][2] /
+    [t][z][y][x][3] (2D / 3D vector field, components interleaved; FTK_VECTOR_FIELD)."""
     d = Desc()
     if vector:
-        if len(shape) != 4 or shape[3] != 2:
-            raise ValueError("vector field must be [t][y][x][2]")
-        nt, ny, nx, _ = shape
-        nz, d.ndim = 1, 2
+        if len(shape) == 4 and shape[3] == 2:
+            nt, ny, nx, _ = shape
+            nz, d.ndim = 1, 2
+        elif len(shape) == 5 and shape[4] == 3:
+            nt, nz, ny, nx, _ = shape
+            d.ndim = 3
+        else:
+            raise ValueError("vector field must be [t][y][x][2] or [t][z][y][x][3]")
     elif len(shape) == 3:
         nt, ny, nx = shape
         nz, d.ndim = 1, 2

@@ -39,6 +39,7 @@ struct ExtractParams {
 
 int launch_extract2d(const ExtractParams& P, cudaStream_t stream);
 int launch_extract_vec2d(const ExtractParams& P, cudaStream_t stream);  // 2D vector fields
+int launch_extract_vec3d(const ExtractParams& P, cudaStream_t stream);  // 3D vector fields
 int launch_expand2d(const ExtractParams& P, cudaStream_t stream, int sms);  // group entries -> cube list
 int launch_extract3d(const ExtractParams& P, cudaStream_t stream);
 

@@ -239,6 +239,50 @@ __device__ __forceinline__ int classify3(const double* h) {
   return changes == 3 ? FTK_CP_MIN : changes == 2 ? FTK_CP_SADDLE1 : changes == 1 ? FTK_CP_SADDLE2 : FTK_CP_MAX;
 }
 
+// Vector-field type (FTK_VECTOR_FIELD, R17) from the interpolated 3x3 Jacobian
+// h = [u_x u_y u_z v_x v_y v_z w_x w_y w_z]: Routh-Hurwitz count of the eigenvalues with positive real
+// part on det(lambda I - J) = lambda^3 + a1 lambda^2 + a2 lambda + a3 -- 0 sink, 3 source, else
+// saddle; det == 0 degenerate; a1 == 0 saddle; a1 a2 == a3 centre if a2 > 0 (an imaginary pair) else
+// saddle.  Fixed-order FP64, no FMA, as the oracle.
+__device__ __forceinline__ int classify_vec3(const double* h) {
+  const double a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7], k = h[8];
+  const double tr = __dadd_rn(__dadd_rn(a, e), k);
+  const double m2 = __dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(a, e), __dmul_rn(b, d)), __dsub_rn(__dmul_rn(a, k), __dmul_rn(c, g))),
+                              __dsub_rn(__dmul_rn(e, k), __dmul_rn(f, hh)));
+  const double det = __dadd_rn(__dsub_rn(__dmul_rn(a, __dsub_rn(__dmul_rn(e, k), __dmul_rn(f, hh))),
+                                         __dmul_rn(b, __dsub_rn(__dmul_rn(d, k), __dmul_rn(f, g)))),
+                               __dmul_rn(c, __dsub_rn(__dmul_rn(d, hh), __dmul_rn(e, g))));
+  if (det == 0) return FTK_CP_DEGENERATE;
+  const double a1 = -tr, a2 = m2, a3 = -det;
+  const double r3 = __dsub_rn(__dmul_rn(a1, a2), a3);
+  if (a1 == 0) return FTK_CP_SADDLE;
+  if (r3 == 0) return a2 > 0 ? FTK_CP_CENTER : FTK_CP_SADDLE;
+  const int s1 = a1 > 0 ? 1 : -1, s2 = (r3 > 0) == (a1 > 0) ? 1 : -1, s3 = a3 > 0 ? 1 : -1;
+  const int changes = (s1 != 1) + (s2 != s1) + (s3 != s2);
+  return changes == 0 ? FTK_CP_SINK : (changes == 3 ? FTK_CP_SOURCE : FTK_CP_SADDLE);
+}
+
+// Jacobian of a 3D vector field at (x, y, z, t): the gradient rule of R7 on each component;
+// J[3 j + a] = d(component j) / d(axis a), 2x scale, one-sided doubled at the boundary
+template <typename T>
+__device__ void jac3(const ExtractParams& P, const Geo3& G, i64 x, i64 y, i64 z, i64 t, i64* J) {
+  const T* base = reinterpret_cast<const T*>(P.field) + (t - P.t0) * G.nx * G.ny * G.nz * 3;
+  auto q = [&](i64 xx, i64 yy, i64 zz, int j) { return quant3(base[((zz * G.ny + yy) * G.nx + xx) * 3 + j], G); };
+  const i64 N[3] = {G.nx, G.ny, G.nz};
+  const i64 c[3] = {x, y, z};
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      i64 lo[3] = {x, y, z}, hi[3] = {x, y, z};
+      i64 f = 1;
+      if (c[a] == 0) { hi[a] = 1; lo[a] = 0; f = 2; }
+      else if (c[a] == N[a] - 1) { hi[a] = N[a] - 1; lo[a] = N[a] - 2; f = 2; }
+      else { hi[a] = c[a] + 1; lo[a] = c[a] - 1; }
+      J[3 * j + a] = f * (q(hi[0], hi[1], hi[2], j) - q(lo[0], lo[1], lo[2], j));
+    }
+}
+
 // The 24 cells (pentachora) of a hypercube: axis permutations (p1..p4) of {x=1, y=2, z=4, t=8};
 // chain w0 = 0, w_k = w_{k-1} | p_k.  Dropping w1..w4 leaves own faces; dropping w0 leaves the upper
 // face (w1, w2, w3, 15) owned by the neighbour hypercube anchored at v + p1.
@@ -779,6 +823,190 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
 }
 }  // namespace s3
 
+// ------------------------------------------------------------------------------ K1a (3D vector field)
+// FTK_VECTOR_FIELD, [t][z][y][x][3]: no stencil, so a plain warp-persistent scan (as k_scanvec2d): a
+// work item is a 128 x 8 x 1 anchor tile (x, y, z0) x a chunk of timesteps; per plane the warp codes
+// the slices z0 and z0 + 1 (9 rows each, plus their column x0 + 128), 6-bit "strict sign holds" codes
+// (u, v, w against +-2^-s; bits 7..2, 0xFC neutral), ANDs y- and x-pairs in registers, the z-pair of
+// the two slices and the t-pair with the previous plane; a zero byte is a surviving hypercube, handed
+// to k_exact3d<T, true> one entry per hypercube.
+namespace v3 {
+constexpr int LX = 128, RW = 8, CHUNK = 32;
+constexpr uint32_t NEUTRAL = 0xFCFCFCFCu;
+
+template <typename T>
+__device__ __forceinline__ uint32_t vcode3(T u, T v, T w, T thr) {
+  auto sb = [](T a) -> uint32_t {
+    if constexpr (sizeof(T) == 4) return __float_as_uint(a) >> 31;
+    else return (uint32_t)((unsigned long long)__double_as_longlong(a) >> 63);
+  };
+  return (sb(thr - u) << 7) | (sb(u + thr) << 6) | (sb(thr - v) << 5) | (sb(v + thr) << 4) | (sb(thr - w) << 3) |
+         (sb(w + thr) << 2);
+}
+
+template <typename T>
+__device__ __forceinline__ void track_max(T a, uint32_t& maxb, double& maxd) {
+  if constexpr (sizeof(T) == 4) {
+    maxb = max(maxb, __float_as_uint(a) & 0x7fffffffu);
+  } else {
+    const double x = fabs(a);
+    maxd = (x != x || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, x);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t row_code(const T* plane, i64 nx, i64 ny, i64 nz, i64 y, i64 z, i64 xl, T thr,
+                                             bool aligned, uint32_t& maxb, double& maxd) {
+  if (y >= ny || z >= nz) return NEUTRAL;
+  const T* r = plane + 3 * ((z * ny + y) * nx + xl);
+  T q[12];
+  if (xl + 3 < nx && aligned) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(r));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(r + 4));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(r + 8));
+    q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w; q[4] = b.x; q[5] = b.y;
+    q[6] = b.z; q[7] = b.w; q[8] = c.x; q[9] = c.y; q[10] = c.z; q[11] = c.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) q[k] = xl + k / 3 < nx ? __ldg(r + k) : (T)0;
+  }
+  uint32_t code = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool in = xl + i < nx;
+    code |= (in ? vcode3<T>(q[3 * i], q[3 * i + 1], q[3 * i + 2], thr) : 0xFCu) << (8 * i);
+    if (in) {
+      track_max<T>(q[3 * i], maxb, maxd);
+      track_max<T>(q[3 * i + 1], maxb, maxd);
+      track_max<T>(q[3 * i + 2], maxb, maxd);
+    }
+  }
+  return code;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_scanvec3d(const __grid_constant__ ExtractParams P) {
+  const int lane = threadIdx.x & 31;
+  const i64 nx = P.nx, ny = P.ny, nz = P.nz;
+  const int ntx = (int)((nx + LX - 1) / LX), nty = (int)((ny + RW - 1) / RW);
+  const int tch = (int)P.tchunk;
+  const int ntc = (int)((P.tb - P.ta + tch - 1) / tch);
+  const long long nitems = (long long)ntx * nty * nz * ntc;
+  const T thr = (T)P.thr;
+  const T* F = reinterpret_cast<const T*>(P.field);
+  const bool aligned = sizeof(T) == 4 && (nx % 4 == 0) && ((reinterpret_cast<uintptr_t>(F) & 15) == 0);
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  long long cur = 0, end = 0;
+  unsigned long long mysurv = 0;
+  uint32_t maxb = 0;
+  double maxd = 0.0;
+  // one list entry per surviving hypercube (survivors are rare in 3D): ranks from a ballot when every
+  // lane has at most one, else one lane-serial round per survivor bit
+  auto enqueue = [&](uint32_t mask, int tflag, int xl, int y0, int z) {
+    while (__any_sync(0xffffffffu, mask != 0)) {
+      const uint32_t bit = mask & (0u - mask);
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit != 0);
+      const int n = __popc(bal), rank = __popc(bal & lt_mask);
+      const int avail = (int)(end - cur);
+      long long e = cur + rank;
+      if (n > avail) {
+        long long c = 0;
+        if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], (unsigned long long)CHUNK);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (rank >= avail) e = c + (rank - avail);
+        cur = c + (n - avail);
+        end = c + CHUNK;
+      } else {
+        cur += n;
+      }
+      if (bit && e < P.wcap) {
+        const int bb = __ffs(bit) - 1;
+        P.wx[e] = xl + (bb >> 3);
+        P.wy[e] = y0 + (bb & 7);
+        P.wz[e] = z;
+        P.wt[e] = tflag;
+      }
+      mysurv += n;
+      mask &= mask - 1;
+    }
+  };
+  while (true) {
+    long long item = 0;
+    if (lane == 0) item = (long long)atomicAdd(&P.counters[CNT_WORK], 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= nitems) break;
+    long long r = item;
+    const int tx = (int)(r % ntx); r /= ntx;
+    const int ty = (int)(r % nty); r /= nty;
+    const i64 z0 = r % nz; r /= nz;
+    const i64 x0 = (i64)tx * LX, y0 = (i64)ty * RW;
+    const i64 ta = P.ta + r * tch, tb = min(ta + tch, P.tb);
+    const i64 plast = min(tb, P.nt_global - 1);
+    const i64 xl = x0 + 4 * lane;
+    uint32_t prevK[RW];
+    for (i64 p = ta; p <= plast; ++p) {
+      const T* plane = F + (p - P.t0) * nx * ny * nz * 3;
+      uint32_t K[RW];
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        const i64 z = z0 + sl;
+        uint32_t C[RW + 1];
+#pragma unroll
+        for (int rr = 0; rr <= RW; ++rr) C[rr] = row_code<T>(plane, nx, ny, nz, y0 + rr, z, xl, thr, aligned, maxb, maxd);
+        uint32_t Ye;
+        {
+          const int k = min(lane, RW);
+          const i64 y = y0 + k, x = x0 + LX;
+          uint32_t ce = 0xFCu;
+          if (x < nx && y < ny && z < nz) {
+            const T* q = plane + 3 * ((z * ny + y) * nx + x);
+            ce = vcode3<T>(__ldg(q), __ldg(q + 1), __ldg(q + 2), thr);
+          }
+          Ye = ce & __shfl_down_sync(0xffffffffu, ce, 1);
+        }
+#pragma unroll
+        for (int rr = 0; rr < RW; ++rr) {
+          const uint32_t Y = C[rr] & C[rr + 1];
+          uint32_t nb = __shfl_down_sync(0xffffffffu, Y, 1);
+          const uint32_t ne = __shfl_sync(0xffffffffu, Ye, rr);
+          if (lane == 31) nb = ne;
+          const uint32_t Sq = Y & ((Y >> 8) | (nb << 24));
+          K[rr] = sl == 0 ? Sq : (K[rr] & Sq);  // z-pair
+        }
+      }
+      auto survivors_of = [&](const uint32_t* Q) {
+        uint32_t mask = 0;
+#pragma unroll
+        for (int rr = 0; rr < RW; ++rr) mask |= (((Q[rr] - 0x01010101u) & ~Q[rr] & 0x80808080u) >> (7 - rr));
+        return mask;
+      };
+      if (p > ta) {
+        uint32_t Q[RW];
+#pragma unroll
+        for (int rr = 0; rr < RW; ++rr) Q[rr] = prevK[rr] & K[rr];
+        enqueue(survivors_of(Q), (int)((uint32_t)(p - 1) | 0x80000000u), (int)xl, (int)y0, (int)z0);
+      }
+      if (p == P.nt_global - 1 && p < tb) enqueue(survivors_of(K), (int)p, (int)xl, (int)y0, (int)z0);
+#pragma unroll
+      for (int rr = 0; rr < RW; ++rr) prevK[rr] = K[rr];
+    }
+  }
+  for (long long e = cur + lane; e < end; e += 32)
+    if (e < P.wcap) P.wt[e] = -1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    maxb = max(maxb, __shfl_xor_sync(0xffffffffu, maxb, o));
+    const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
+    maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
+  }
+  if (lane == 0) {
+    atomicAdd(&P.counters[CNT_SURVIVORS], mysurv);
+    atomicMax(&P.counters[CNT_MAXBITS],
+              sizeof(T) == 4 ? (unsigned long long)maxb : (unsigned long long)__double_as_longlong(maxd));
+  }
+}
+}  // namespace v3
+
 // ------------------------------------------------------------------------------ K1b (3D)
 // One warp per surviving hypercube of the list: lanes 0..15 take the 16 corner gradients (exact
 // int64, straight from the field), the 60 face types are spread over the lanes (two each) for the
@@ -788,10 +1016,13 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
 // FP64.  A hypercube's 60 faces with their SoS chains are far too much serial work for one thread.
 constexpr int XW3 = 4;  // warps per block
 
-template <typename T>
+// VEC: a 3D vector field [t][z][y][x][3] (FTK_VECTOR_FIELD): the corner values are the quantized
+// vectors themselves and the type comes from the Jacobian (R17)
+template <typename T, bool VEC = false>
 __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ ExtractParams P) {
+  constexpr int NH = VEC ? 9 : 6;
   __shared__ i64 sg[XW3][16][3];
-  __shared__ i64 sH[XW3][16][6];  // corner Hessians (hypercubes with punctured faces)
+  __shared__ i64 sH[XW3][16][NH];  // corner Hessians / Jacobians (hypercubes with punctured faces)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Geo3 G;
   G.nx = P.nx;
@@ -803,7 +1034,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
   G.x0 = G.y0 = G.z0 = 0;
   const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
   const T* field = reinterpret_cast<const T*>(P.field);
-  const i64 plane = G.nx * G.ny * G.nz;
+  const i64 plane = G.nx * G.ny * G.nz * (VEC ? 3 : 1);
   i64(&g)[16][3] = sg[w];
   for (long long e = (long long)blockIdx.x * XW3 + w; e < nwin; e += (long long)gridDim.x * XW3) {
     const int et = P.wt[e];
@@ -821,7 +1052,15 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
       const bool e1 = cx < G.nx && cy < G.ny && cz < G.nz && ((c & 8) == 0 || hasB);
       if (lane < 16) {
         i64 gc[3] = {0, 0, 0};
-        if (e1) grad3<T>((c & 8) ? B : A, G, cx, cy, cz, gc);
+        if (e1) {
+          if constexpr (VEC) {
+            const T* q = ((c & 8) ? B : A).S + ((cz * G.ny + cy) * G.nx + cx) * 3;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) gc[j] = quant3(__ldg(q + j), G);
+          } else {
+            grad3<T>((c & 8) ? B : A, G, cx, cy, cz, gc);
+          }
+        }
         g[c][0] = gc[0];
         g[c][1] = gc[1];
         g[c][2] = gc[2];
@@ -862,7 +1101,10 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
     if (npunct) {  // integer Hessians of the 16 corners, one per lane, for the records below
       const int c = lane & 15;
       if (lane < 16 && ((ex >> c) & 1))
-        hess3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+      {
+        if constexpr (VEC) jac3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+        else hess3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+      }
       __syncwarp();
     }
     unsigned long long rbase = 0;
@@ -942,7 +1184,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
         mu[3] = __ddiv_rn(i128_to_double_rn(D3), sd);
       }
       double pv[4][4];  // x, y, z, t of each vertex
-      double Hd[6][4];
+      double Hd[NH][4];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const i64 vx = x + (m[kk] & 1), vy = y + ((m[kk] >> 1) & 1), vz = z + ((m[kk] >> 2) & 1),
@@ -952,12 +1194,12 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
         pv[2][kk] = (double)vz;
         pv[3][kk] = (double)vt;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) Hd[q][kk] = __ll2double_rn(sH[w][m[kk]][q]);
+        for (int q = 0; q < NH; ++q) Hd[q][kk] = __ll2double_rn(sH[w][m[kk]][q]);
       }
-      double Hb[6];
+      double Hb[NH];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) Hb[q] = dot4_nofma(mu, Hd[q]);
-      const int type = classify3(Hb);
+      for (int q = 0; q < NH; ++q) Hb[q] = dot4_nofma(mu, Hd[q]);
+      const int type = VEC ? classify_vec3(Hb) : classify3(Hb);
       const int span = m[3];
       if (!(span & 8)) flags |= FTK_CP_ORDINAL;
       if (span != 15) {
@@ -1021,6 +1263,36 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   k_exact3d<T><<<(unsigned)(sms * std::max(xper, 1)), XW3 * 32, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
+}
+
+template <typename T>
+static int launch_vec3_t(const ExtractParams& P, cudaStream_t stream) {
+  using namespace k3d;
+  auto scan = v3::k_scanvec3d<T>;
+  const sm100::LaunchGeom lg = sm100::launch_geom(scan, 256, 0);
+  if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scanvec3d launch geometry");
+  const long long tiles = ((P.nx + v3::LX - 1) / v3::LX) * ((P.ny + v3::RW - 1) / v3::RW) * P.nz;
+  const long long warps = (long long)lg.sms * lg.per_sm * 8;
+  ExtractParams Q = P;
+  Q.tchunk = 16;
+  while (Q.tchunk > 2 && tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk) < 4 * warps) Q.tchunk /= 2;
+  const long long items = tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk);
+  if (items <= 0) return FTK_OK;
+  const long long blocks = std::min<long long>((items + 7) / 8, (long long)lg.sms * lg.per_sm);
+  scan<<<(unsigned)blocks, 256, 0, stream>>>(Q);
+  FTK_CUDA_TRY(cudaGetLastError());
+  if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
+  const sm100::LaunchGeom xg = sm100::launch_geom(k_exact3d<T, true>, XW3 * 32, 0);
+  if (xg.err != cudaSuccess) return set_cuda_error(xg.err, "k_exact3d launch geometry");
+  k_exact3d<T, true><<<(unsigned)(lg.sms * std::max(xg.per_sm, 1)), XW3 * 32, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+int launch_extract_vec3d(const ExtractParams& P, cudaStream_t stream) {
+  if (P.nx >= (1ll << 31) - 256 || P.ny >= (1ll << 31) - 64 || P.nz >= (1ll << 31) - 64 || P.nt_global >= (1ll << 30))
+    return FTK_ERR_INVALID_ARG;
+  return P.dtype == FTK_F32 ? launch_vec3_t<float>(P, stream) : launch_vec3_t<double>(P, stream);
 }
 
 int launch_extract3d(const ExtractParams& P, cudaStream_t stream) {

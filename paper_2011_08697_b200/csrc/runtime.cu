@@ -94,7 +94,7 @@ static constexpr int64_t kMaxCapacity = (1ll << 31) - 2;
 static int esz_of(const ftk_desc* d) { return d->dtype == FTK_F32 ? 4 : 8; }
 static bool is_vector(const ftk_desc* d) { return (d->flags & FTK_VECTOR_FIELD) != 0; }
 // bytes of one vertex's values (2 interleaved components for a vector field)
-static size_t vertex_bytes(const ftk_desc* d) { return (size_t)esz_of(d) * (is_vector(d) ? 2 : 1); }
+static size_t vertex_bytes(const ftk_desc* d) { return (size_t)esz_of(d) * (is_vector(d) ? d->ndim : 1); }
 
 // Face types an edge can look up: the upper face of a cell, seen from the neighbour cube that owns
 // it, is the chain (0, p2, p2|p3[, p2|p3|p4]) -- its last mask misses exactly one axis.  The other
@@ -122,7 +122,6 @@ static int validate(const ftk_desc* d) {
   if (d->scale_log2 < -64 || d->scale_log2 > 64) return FTK_ERR_INVALID_ARG;
   if ((d->flags & FTK_GHOST_PLANE) && d->nt < 2) return FTK_ERR_INVALID_ARG;
   if (d->flags & ~(FTK_GHOST_PLANE | FTK_SORTED | FTK_VECTOR_FIELD)) return FTK_ERR_INVALID_ARG;
-  if ((d->flags & FTK_VECTOR_FIELD) && d->ndim != 2) return FTK_ERR_INVALID_ARG;  // 2D vector fields
   if (d->n[0] * d->n[1] * d->n[2] > (1ll << 40)) return FTK_ERR_INVALID_ARG;
   return FTK_OK;
 }
@@ -286,7 +285,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   EP.ev_mid = ev.on ? (void*)ev.e[4] : nullptr;
   if (ev.on) cudaEventRecord(ev.e[4], stream);  // a recorded default for paths that skip K1a
   ev.rec(1, stream);
-  st = is_vector(desc) ? launch_extract_vec2d(EP, stream)
+  st = is_vector(desc) ? (desc->ndim == 2 ? launch_extract_vec2d(EP, stream) : launch_extract_vec3d(EP, stream))
                        : (desc->ndim == 2 ? launch_extract2d(EP, stream) : launch_extract3d(EP, stream));
   if (st) return st;
   ev.rec(2, stream);
@@ -677,7 +676,7 @@ static int tracker_window(ftk_tracker* tr, bool last) {
   FTK_CUDA_TRY(cudaGetLastError());
   ExtractParams EP = extract_params(&c, tr->buf, tr->out, tr->capacity, tr->ws, tr->L, counters, true);
   EP.table = nullptr;
-  int st = is_vector(&c) ? launch_extract_vec2d(EP, tr->stream)
+  int st = is_vector(&c) ? (c.ndim == 2 ? launch_extract_vec2d(EP, tr->stream) : launch_extract_vec3d(EP, tr->stream))
                          : (c.ndim == 2 ? launch_extract2d(EP, tr->stream) : launch_extract3d(EP, tr->stream));
   if (st) return st;
   if (!last) {  // the ghost plane becomes plane 0 of the next window
@@ -813,7 +812,7 @@ int ftk_cp_track_host(const ftk_desc* desc, const void* h_field, void* d_stage, 
   if (!h_field || !d_stage || !h_out || !n_out) return FTK_ERR_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t esz = desc->dtype == FTK_F32 ? 4 : 8;
-  const size_t bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * desc->nt * esz * (is_vector(desc) ? 2 : 1);
+  const size_t bytes = (size_t)desc->n[0] * desc->n[1] * desc->n[2] * desc->nt * esz * (is_vector(desc) ? desc->ndim : 1);
   FTK_CUDA_TRY(cudaMemcpyAsync(d_stage, h_field, bytes, cudaMemcpyHostToDevice, s));
   st = run(desc, d_stage, d_out, capacity, n_out, d_ws, ws_bytes, s, true);
   if (st) return st;

@@ -87,3 +87,49 @@ def test_zero_or_two_vector_degenerate(oracle_lib, seed):
     v = torch.tensor([-1.0, 0.0, 1.0], dtype=torch.float64)[torch.randint(0, 3, (4, 6, 7, 2), generator=g)]
     rec, _, info = oracle_lib.track(v.numpy().astype(np.float32), 0, vector=True)
     assert info["bad_cells"] == 0 and len(rec) > 0
+
+
+# ------------------------------------------------------------------------------------ 3D vector fields
+def int_gradient3(f: np.ndarray, s: int) -> np.ndarray:
+    """[t][z][y][x] -> [t][z][y][x][3] integer gradient (R7), components x, y, z"""
+    q = np.rint(np.ldexp(f.astype(np.float64), s)).astype(np.int64)
+    g = np.zeros(q.shape + (3,), np.int64)
+    for a, ax in ((0, 3), (1, 2), (2, 1)):
+        n = q.shape[ax]
+        sl = lambda i: tuple(slice(None) if k != ax else i for k in range(4))
+        g[sl(slice(1, n - 1)) + (a,)] = q[sl(slice(2, n))] - q[sl(slice(0, n - 2))]
+        g[sl(0) + (a,)] = 2 * (q[sl(1)] - q[sl(0)])
+        g[sl(n - 1) + (a,)] = 2 * (q[sl(n - 1)] - q[sl(n - 2)])
+    return g
+
+
+def test_gradient_equivalence_3d(oracle_lib):
+    s = 26
+    f = fi.Woven(12, 11, 5, L=15.0, nz=10).generate().numpy()
+    v = np.ldexp(int_gradient3(f, s).astype(np.float64), -s)
+    vec, _, vinfo = oracle_lib.track(v, s, vector=True)
+    sca, _, _ = oracle_lib.track(f, s)
+    assert vinfo["bad_cells"] == 0 and len(vec) == len(sca) > 0
+    for k in ("face_id", "label", "x", "y", "z", "t", "flags"):
+        assert np.array_equal(vec[k], sca[k]), k
+
+
+@pytest.mark.parametrize("A,expect", [
+    (((1, 0, 0), (0, 2, 0), (0, 0, 3)), "SOURCE"),
+    (((-1, 0, 0), (0, -2, 0), (0, 0, -3)), "SINK"),
+    (((1, 0, 0), (0, 2, 0), (0, 0, -3)), "SADDLE"),     # trace 0: Routh's epsilon rule
+    (((1, 1, 0), (0, 1, 0), (0, 0, -1)), "SADDLE"),     # eigenvalues 1, 1, -1: a1 a2 == a3, a2 < 0
+    (((-1, -2, 0), (2, -1, 0), (0, 0, -1)), "SINK"),    # spiral sink
+    (((0, -1, 0), (1, 0, 0), (0, 0, -1)), "CENTER"),    # +-i and -1: a1 a2 == a3, a2 > 0
+])
+def test_moving_linear_3d(oracle_lib, A, expect):
+    m = fi.MovingLinear3((9, 8, 10), 5, A=A, c0=(3.0, 3.0, 4.0), w=(0.5, 0.25, 0.125))
+    rec, _, info = oracle_lib.track(m.generate().numpy(), m.scale_log2, vector=True)
+    assert info["bad_cells"] == 0
+    ordn = rec[(rec["flags"] & oracle_lib.FL_ORDINAL) != 0]
+    assert len(ordn) == 5
+    for r in ordn:
+        c = m.center(r["t"])
+        assert max(abs(r["x"] - c[0]), abs(r["y"] - c[1]), abs(r["z"] - c[2])) < 1e-12
+    assert set(rec["type"].tolist()) == {getattr(oracle_lib, expect)}
+    assert len(set(rec["label"].tolist())) == 1

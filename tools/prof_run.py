@@ -8,7 +8,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else 'C2'
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cfg = fi.CONFIGS[name]
 f = cfg.make().generate(device='cuda')
-vec = cfg.kind == 'gyre2d'
+vec = cfg.kind in ('gyre2d', 'abc3d')
 ftk.set_profiling(True)
 rec, buf = ftk.track(f, cfg.scale_log2, return_buffers=True, vector=vec)
 for i in range(reps):
