@@ -14,6 +14,7 @@ VARIANTS = {
     "vminb3": ["FTK_V_MINB=3"],
     "vminb4": ["FTK_V_MINB=4"],
     "vminb6": ["FTK_V_MINB=6"],
+    "v3m3": ["FTK_V3_MINB=3"],
     "vminb8": ["FTK_V_MINB=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
