@@ -353,7 +353,7 @@ def run_ours(args):
     # trajectory post-processing over this step's records: adjacency, a slice,
     # a duration filter and type smoothing, each synchronous; wall clock per operation
     post_line = None
-    if world == 1 and not args.no_stream and not d3:
+    if world == 1 and not args.no_stream and not args.no_e2e and not d3:
         rec_p, buf_p = ftk.track(field, cfg.scale_log2, buffers=buf, vector=vec, return_buffers=True)
         rec_p = rec_p.clone()
         tp = {}

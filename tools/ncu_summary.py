@@ -26,7 +26,9 @@ per = collections.defaultdict(list)
 for r in rows[start + 1:]:
     if len(r) > vi and num(r[vi]) is not None:
         per[r[ki]].append(num(r[vi]) / 1000.0)
-ours = {k: v for k, v in per.items() if any(s in k for s in ("k2d::", "trk::", "k3d::", "ftk::", "k_"))}
+# the step's kernels (the bench's post-processing leg -- k_verify adjacency, k_post_* -- is not part of it)
+ours = {k: v for k, v in per.items() if any(s in k for s in ("k2d::", "trk::", "k3d::", "ftk::", "k_"))
+        and "k_verify" not in k and "k_post" not in k}
 tot = sum(sum(v) for v in ours.values())
 lines = [f"# ncu launch list ({tag}, {config}): gpu__time_duration.sum, --clock-control none, cold-cache serialised",
          "# kernel | launches | mean us | share of our kernels' time"]
