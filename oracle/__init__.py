@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
         L.ftko_extract.argtypes = [ctypes.POINTER(_Desc), P, ctypes.c_int64, ctypes.c_int64, P,
                                    ctypes.c_int64, P, P]
         L.ftko_track.argtypes = [ctypes.POINTER(_Desc), P, P, ctypes.c_int64, P, P, P]
+        L.ftko_iso_track.argtypes = [ctypes.POINTER(_Desc), P, ctypes.c_double, P, ctypes.c_int64, P, P, P]
     return _lib
 
 
@@ -194,3 +195,25 @@ def track(field: np.ndarray, scale_log2: int, nthreads: int = 0, check: bool = T
     info = dict(cells=int(stats[0]), bad_cells=int(stats[1]), components=int(stats[2]),
                 pairs=int(stats[3]), status=st)
     return out[: n_out.value], n_faces.value, info
+
+
+def iso_track(field: np.ndarray, scale_log2: int, isovalue: float, nthreads: int = 0, check: bool = True):
+    """Isovolume tracking: crossed spacetime edges of f = isovalue with Eq. 2
+    locations and component labels (min edge id).  Returns (records sorted by edge id, n_edges, stats)."""
+    d, field = _desc(field, scale_log2, 0, None, nthreads)
+    n_out = ctypes.c_int64(0)
+    n_edges = ctypes.c_int64(0)
+    stats = np.zeros(4, np.int64)
+    cap = 1 << 16
+    while True:
+        out = np.zeros(cap, CP_DTYPE)
+        st = lib().ftko_iso_track(ctypes.byref(d), field.ctypes.data, ctypes.c_double(isovalue), out.ctypes.data, cap,
+                                  ctypes.byref(n_out), ctypes.byref(n_edges), stats.ctypes.data)
+        if st == CAPACITY:
+            cap = n_out.value
+            continue
+        break
+    if st != OK and (check or st != INVARIANT):
+        raise OracleError(st, "iso_track")
+    info = dict(cells=int(stats[0]), bad_cells=int(stats[1]), components=int(stats[2]), status=st)
+    return out[: n_out.value], n_edges.value, info

@@ -842,3 +842,128 @@ int ftko_track(const ftko_desc* D, const void* field, ftko_cp* out, int64_t capa
   teardown(&C);
   return st;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Isovolume tracking (Alg. 1 right): the level set f = c of a 2D+t / 3D+t scalar     */
+/* field on the same Kuhn spacetime mesh.                                                      */
+/*   edge pass   every spacetime edge (1-simplex, anchor v, mask m != 0) is tested: with        */
+/*               g = q - rint(c 2^s), the 1D SoS point-in-simplex test of P:640 reduces to      */
+/*               "the two SoS signs differ", the SoS sign of a single value being its sign with */
+/*               0 counted as positive (the +eps of the only row); location by Eq. 2 (n = 1).   */
+/*   cell pass   every cell (d-simplex) of the mesh: its crossed edges (0, d or 2(d-1) of them, */
+/*               P:629-633 cases I / II) are united; label = minimum edge id of the component.  */
+/* Edge id = I(anchor) * (2^d - 1) + (m - 1).  Record type: 1 if g increases along the edge     */
+/* (g_a < 0 <= g_b), else 0; flags: ordinal (m has no t bit).                                   */
+/* ------------------------------------------------------------------------------------------ */
+int ftko_iso_track(const ftko_desc* D, const void* field, double isovalue, ftko_cp* out, int64_t capacity,
+                   int64_t* n_out, int64_t* n_edges, int64_t* stats) {
+  if (!check_desc(D) || D->kind != 0 || !field || !n_out) return FTKO_INVALID_ARG;
+  if (D->t0 != 0 || D->nt != D->nt_global) return FTKO_INVALID_ARG;
+  ctx_t C;
+  memset(&C, 0, sizeof C);
+  C.D = D;
+  C.n = D->ndim;
+  C.d = D->ndim + 1;
+  for (int a = 0; a < C.n; a++) C.ext[a] = D->n[a];
+  C.ext[C.d - 1] = D->nt_global;
+#ifdef _OPENMP
+  if (D->nthreads > 0) omp_set_num_threads(D->nthreads);
+#endif
+  int64_t nv = D->n[0] * D->n[1] * D->n[2] * D->nt;
+  C.q = (int64_t*)malloc((size_t)nv * sizeof(int64_t));
+  if (!C.q) return FTKO_NOMEM;
+  int st = quantize_all(&C, field);
+  double cqd = nearbyint(ldexp(isovalue, D->scale_log2));
+  if (st == FTKO_OK && !(fabs(cqd) < ldexp(1.0, C.n == 2 ? 59 : 38))) st = FTKO_RANGE;
+  if (st != FTKO_OK) { free(C.q); return st; }
+  const int64_t cq = (int64_t)cqd;
+  const int d = C.d, E = (1 << d) - 1;
+  vec_t S = {0, 0, 0};
+  int64_t ne = 0;
+  /* edge pass, anchors in id order */
+  for (int64_t i = 0; i < nv; i++) {
+    int64_t v[MAXD], rem = i;
+    for (int a = 0; a < d; a++) {
+      int64_t N = C.ext[a];
+      v[a] = a < d - 1 ? rem % N : rem;
+      rem = a < d - 1 ? rem / N : 0;
+    }
+    for (int m = 1; m <= E; m++) {
+      int64_t b[MAXD];
+      int ok = 1;
+      for (int a = 0; a < d; a++) {
+        b[a] = v[a] + ((m >> a) & 1);
+        if (b[a] > C.ext[a] - 1) ok = 0;
+      }
+      if (!ok) continue;
+      ne++;
+      int64_t ga = C.q[bidx(&C, v)] - cq, gb = C.q[bidx(&C, b)] - cq;
+      if ((ga >= 0) == (gb >= 0)) continue;
+      i128 D0 = -(i128)gb, D1 = (i128)ga, Ssum = D0 + D1;
+      double s = cvt(Ssum), mu0 = cvt(D0) / s, mu1 = cvt(D1) / s;
+      double pos[MAXD];
+      for (int a = 0; a < d; a++) pos[a] = mu0 * (double)v[a] + mu1 * (double)b[a];
+      ftko_cp r;
+      r.face_id = vid(&C, v) * E + (m - 1);
+      r.label = -1;
+      r.x = pos[0];
+      r.y = pos[1];
+      r.z = C.n == 3 ? pos[2] : 0.0;
+      r.t = pos[d - 1];
+      r.type = gb >= 0 ? 1 : 0;
+      r.flags = ((m >> (d - 1)) & 1) ? 0 : FL_ORDINAL;
+      if (!vec_push(&S, &r)) { free(S.v); free(C.q); return FTKO_NOMEM; }
+    }
+  }
+  if (n_edges) *n_edges = ne;
+  /* cell pass */
+  build_tables();
+  int64_t P = S.n;
+  int64_t* ids = (int64_t*)malloc((size_t)(P ? P : 1) * sizeof(int64_t));
+  int64_t* parent = (int64_t*)malloc((size_t)(P ? P : 1) * sizeof(int64_t));
+  for (int64_t i = 0; i < P; i++) { ids[i] = S.v[i].face_id; parent[i] = i; } /* ascending already */
+  int64_t ncells = 0, nbad = 0;
+  int64_t ncube = 1;
+  for (int a = 0; a < d; a++) ncube *= C.ext[a] - 1;
+  for (int64_t i = 0; i < ncube; i++) {
+    int64_t w0[MAXD], rem = i;
+    for (int a = 0; a < d; a++) { w0[a] = rem % (C.ext[a] - 1); rem /= (C.ext[a] - 1); }
+    for (int p = 0; p < g_nperm[d]; p++) {
+      int64_t w[MAXD + 1][MAXD];
+      memcpy(w[0], w0, sizeof w0);
+      for (int k = 1; k <= d; k++) {
+        memcpy(w[k], w[k - 1], sizeof w0);
+        w[k][g_perm[d][p][k - 1]] += 1;
+      }
+      ncells++;
+      int64_t hit[16];
+      int nh = 0;
+      for (int a = 0; a <= d; a++)
+        for (int b = a + 1; b <= d; b++) {
+          int m = 0;
+          for (int x = 0; x < d; x++) m |= (int)(w[b][x] - w[a][x]) << x;
+          int64_t key = vid(&C, w[a]) * E + (m - 1);
+          int64_t* f = (int64_t*)bsearch(&key, ids, (size_t)P, sizeof(int64_t), cmp_i64);
+          if (f) hit[nh++] = f - ids;
+        }
+      if (!(nh == 0 || nh == d || nh == 2 * (d - 1))) nbad++;
+      for (int k = 1; k < nh; k++) {
+        int64_t ra = uf_find(parent, hit[0]), rb = uf_find(parent, hit[k]);
+        if (ra != rb) { if (ra < rb) parent[rb] = ra; else parent[ra] = rb; }
+      }
+    }
+  }
+  int64_t ncomp = 0;
+  for (int64_t i = 0; i < P; i++) {
+    int64_t r = uf_find(parent, i);
+    S.v[i].label = ids[r]; /* roots are component minima: ids ascend with the index */
+    ncomp += r == i;
+  }
+  if (stats) { stats[0] = ncells; stats[1] = nbad; stats[2] = ncomp; stats[3] = 0; }
+  *n_out = P;
+  st = nbad ? FTKO_INVARIANT : FTKO_OK;
+  if (P > capacity) st = FTKO_CAPACITY;
+  else if (out && P) memcpy(out, S.v, (size_t)P * sizeof(ftko_cp));
+  free(ids); free(parent); free(S.v); free(C.q);
+  return st;
+}
