@@ -255,6 +255,21 @@ FTK_API int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int
                                   int32_t half_window, void* d_ws, size_t ws_bytes, int64_t capacity,
                                   ftk_stream stream);
 
+/* Isovolume tracking (Alg. 1 right): the level set f = isovalue of a 2D+t / 3D+t SCALAR
+ * field (desc as for track, the whole domain: t0 = 0, nt = nt_global >= 2, no ghost plane) on the same
+ * Kuhn spacetime mesh.  Edge pass: every spacetime edge v -> v + m (m a nonzero axis mask) is crossed
+ * iff g = rint(f 2^s) - rint(isovalue 2^s) has different SoS signs at its two ends, 0 counting as
+ * positive (the 1D case of P:640: a level set through a vertex is owned by exactly one of its edges).
+ * Each crossed edge is one record: face_id = edge id = I(v) (2^(n+1) - 1) + m - 1 (I as for faces),
+ * location by Eq. 2 with n = 1 (FP64, no FMA), type 1 when g increases along the edge else 0, flags
+ * FTK_CP_ORDINAL when m has no t bit.  Cell pass: the crossed edges of every cell (0, n+1 or 2n of them,
+ * P:629-633 cases I / II; else FTK_ERR_INVARIANT) are joined; label = minimum edge id of the connected
+ * isovolume piece (its "trajectory").  d_out / d_ws / capacity as for track (workspace of
+ * ftk_workspace_size(desc, capacity)); FTK_ERR_CAPACITY sets *n_out to the capacity needed for the
+ * records AND the cell links (several per crossed edge). */
+FTK_API int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                          int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream);
+
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);

@@ -41,7 +41,7 @@ EXPORTS = [
     "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
     "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
-    "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types",
+    "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types", "ftk_iso_track",
 ]
 
 
@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         L.ftk_post_slice.argtypes = [PD, P, P, I64, ctypes.c_double, P, I64, P, P, SZ, I64, P]
         L.ftk_post_filter.argtypes = [PD, P, P, I64, ctypes.c_double, ctypes.c_int32, P, I64, P, P, SZ, I64, P]
         L.ftk_post_smooth_types.argtypes = [PD, P, P, I64, ctypes.c_int32, P, SZ, I64, P]
+        L.ftk_iso_track.argtypes = [PD, ctypes.c_double, P, P, I64, P, P, SZ, P]
         _lib = L
     return _lib
 
@@ -213,6 +214,33 @@ def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global,
         _check(st, fn_name)
         rec = buffers.records[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
         return rec, buffers
+
+
+def iso_track(field: torch.Tensor, scale_log2: int, isovalue: float, capacity: int | None = None,
+              buffers: Buffers | None = None, return_buffers: bool = False):
+    """Isovolume tracking: the crossed spacetime edges of f = isovalue as 56-byte
+    records (face_id = edge id, Eq. 2 location, type 1 = upward crossing, label = min edge id of the
+    connected isovolume piece).  field: [t][y][x] or [t][z][y][x] on the device, the whole domain."""
+    if not field.is_cuda:
+        raise FtkError(ERR_INVALID_ARG, "iso_track: field must be a CUDA tensor (no CPU fallback)")
+    field = field.contiguous()
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2)
+    cap = capacity if capacity is not None else (buffers.capacity if buffers else default_capacity(field))
+    while True:
+        if buffers is None or buffers.capacity < cap:
+            buffers = Buffers.allocate(desc, cap, field.device)
+        n_out = ctypes.c_int64(0)
+        st = lib().ftk_iso_track(ctypes.byref(desc), ctypes.c_double(isovalue), ctypes.c_void_p(field.data_ptr()),
+                                 ctypes.c_void_p(buffers.records.data_ptr()), buffers.capacity, ctypes.byref(n_out),
+                                 ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
+                                 ctypes.c_void_p(_stream_ptr(field.device)))
+        if st == ERR_CAPACITY and cap < MAX_CAPACITY:
+            cap = min(MAX_CAPACITY, int(n_out.value * 1.25) + 1024)
+            buffers = None
+            continue
+        _check(st, "ftk_iso_track")
+        rec = buffers.records[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
+        return (rec, buffers) if return_buffers else rec
 
 
 def extract(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,

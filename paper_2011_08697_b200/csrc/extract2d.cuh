@@ -41,6 +41,7 @@ int launch_extract2d(const ExtractParams& P, cudaStream_t stream);
 int launch_extract_vec2d(const ExtractParams& P, cudaStream_t stream);  // 2D vector fields
 int launch_extract_vec3d(const ExtractParams& P, cudaStream_t stream);  // 3D vector fields
 int launch_expand2d(const ExtractParams& P, cudaStream_t stream, int sms);  // group entries -> cube list
+int launch_iso(const ExtractParams& P, long long cq, int ndim, cudaStream_t stream);  // isovolume edge + cell pass
 int launch_extract3d(const ExtractParams& P, cudaStream_t stream);
 
 }  // namespace ftk

@@ -1,0 +1,273 @@
+// iso.cu -- isovolume tracking (Alg. 1 right) on the
+// Kuhn spacetime mesh of a 2D+t / 3D+t scalar field.
+//
+// k_iso<D> -- one thread per grid vertex v (D = 3: 2D+t, D = 4: 3D+t), x fastest across the threads:
+//   * the 2^D corners of the cube anchored at v, quantized (q = rint(f 2^s)) minus the quantized
+//     isovalue: g = q - rint(c 2^s);  a cube whose corners all share one SoS sign (g >= 0 counts as
+//     positive, the +eps of the 1D SoS test) holds no crossed edge and no isovolume piece;
+//   * edge pass: the 2^D - 1 edges anchored at v (v -> v + m) whose two signs differ are crossed: one
+//     record each, located by Eq. 2 with n = 1 (mu_a = -g_b / (g_a - g_b), mu_b = g_a / (g_a - g_b),
+//     FP64 without FMA), id = I(v) (2^D - 1) + m - 1, type 1 if g increases along the edge, flags
+//     ordinal when m has no t bit;
+//   * cell pass (full cubes): the D! cells (axis permutations) of the cube; the crossed edges of each
+//     (0, D or 2 (D - 1) of them -- cases I and II, else FTK_ERR_INVARIANT) are united in a
+//     cube-local union-find over the cube's comparable corner pairs, and every local component is
+//     emitted as trajectory-graph links (representative, member) -- an end is a record index when the
+//     edge is anchored at v, else -1 - edge id (resolved by pass 2 through the hash).
+// Pass 2 (track.cu: hash of every record, links, lock-free union-find, min-id labels) is shared.
+#include <cstdio>
+
+#include "common.cuh"
+#include "extract2d.cuh"
+#include "sm100.cuh"
+
+namespace ftk {
+namespace iso {
+
+// comparable corner pairs (a subset of b, a != b) of the D-cube, and the slot of each
+template <int D>
+struct Pairs {
+  static constexpr int NC = 1 << D;
+  int n;
+  int8_t a[81], b[81];
+  int8_t slot[NC][NC];  // -1 if not comparable
+};
+template <int D>
+constexpr Pairs<D> make_pairs() {
+  Pairs<D> p{};
+  p.n = 0;
+  for (int a = 0; a < (1 << D); ++a)
+    for (int b = 0; b < (1 << D); ++b) {
+      p.slot[a][b] = -1;
+      if (a != b && (a & ~b) == 0) {
+        p.a[p.n] = (int8_t)a;
+        p.b[p.n] = (int8_t)b;
+        p.slot[a][b] = (int8_t)p.n;
+        ++p.n;
+      }
+    }
+  return p;
+}
+static_assert(make_pairs<3>().n == 19 && make_pairs<4>().n == 65, "comparable corner pairs");
+__constant__ Pairs<3> cP3 = make_pairs<3>();
+__constant__ Pairs<4> cP4 = make_pairs<4>();
+
+template <int D>
+struct Perms {
+  int n;
+  int8_t p[24][4];
+};
+template <int D>
+constexpr Perms<D> make_perms() {
+  Perms<D> r{};
+  r.n = 0;
+  int a[4] = {0, 1, 2, 3};
+  // lexicographic permutations of 0..D-1
+  for (int i0 = 0; i0 < D; ++i0)
+    for (int i1 = 0; i1 < D; ++i1)
+      for (int i2 = 0; i2 < (D > 2 ? D : 1); ++i2)
+        for (int i3 = 0; i3 < (D > 3 ? D : 1); ++i3) {
+          const int idx[4] = {i0, i1, i2, i3};
+          bool ok = true;
+          for (int x = 0; x < D; ++x)
+            for (int y = x + 1; y < D; ++y)
+              if (idx[x] == idx[y]) ok = false;
+          if (!ok) continue;
+          for (int x = 0; x < D; ++x) r.p[r.n][x] = (int8_t)a[idx[x]];
+          ++r.n;
+        }
+  return r;
+}
+__constant__ Perms<3> cPm3 = make_perms<3>();
+__constant__ Perms<4> cPm4 = make_perms<4>();
+
+template <int D>
+__device__ __forceinline__ const Pairs<D>& pairs() {
+  if constexpr (D == 3) return cP3;
+  else return cP4;
+}
+template <int D>
+__device__ __forceinline__ const Perms<D>& perms() {
+  if constexpr (D == 3) return cPm3;
+  else return cPm4;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractParams P, long long cq) {
+  constexpr int NC = 1 << D, E = NC - 1, NP = D == 3 ? 19 : 65;
+  const i64 ext[4] = {P.nx, P.ny, D == 4 ? P.nz : P.nt_global, P.nt_global};
+  const i64 nv = P.nx * P.ny * P.nz * P.nt_global;
+  const T* F = reinterpret_cast<const T*>(P.field);
+  uint32_t maxb = 0;
+  double maxd = 0.0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (i64)gridDim.x * blockDim.x) {
+    i64 v[4], rem = i;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      v[a] = a < D - 1 ? rem % ext[a] : rem;
+      rem = a < D - 1 ? rem / ext[a] : 0;
+    }
+    // corner values
+    i64 g[NC];
+    uint32_t exist = 0, pos = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      bool in = true;
+      i64 off = 0, stride = 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const i64 w = v[a] + ((c >> a) & 1);
+        in = in && w < ext[a];
+        off += w * stride;
+        stride *= ext[a];
+      }
+      g[c] = 0;
+      if (in) {
+        const T f = __ldg(F + off);
+        if (c == 0) {
+          if constexpr (sizeof(T) == 4) maxb = max(maxb, __float_as_uint(f) & 0x7fffffffu);
+          else {
+            const double x = fabs((double)f);
+            maxd = (x != x || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, x);
+          }
+        }
+        g[c] = __double2ll_rn(__dmul_rn((double)f, P.scale)) - cq;
+        exist |= 1u << c;
+        pos |= (g[c] >= 0 ? 1u : 0u) << c;
+      }
+    }
+    if (pos == 0 || pos == exist) continue;  // one sign on every corner: nothing crosses this cube
+    // edge pass: crossed edges anchored at v
+    uint32_t emask = 0;
+    const uint32_t s0 = pos & 1u;
+#pragma unroll
+    for (int m = 1; m < NC; ++m)
+      if (((exist >> m) & 1u) && (((pos >> m) & 1u) != s0)) emask |= 1u << m;
+    const int nrec = __popc(emask);
+    unsigned long long rbase = 0;
+    if (nrec) rbase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)nrec);
+    i64 vid = 0;
+    {
+      i64 stride = 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        vid += v[a] * stride;
+        stride *= ext[a];
+      }
+    }
+    auto rec_of = [&](int m) { return (long long)(rbase + __popc(emask & ((1u << m) - 1u))); };
+    uint32_t em = emask;
+    while (em) {
+      const int m = __ffs(em) - 1;
+      em &= em - 1;
+      const unsigned long long slot = (unsigned long long)rec_of(m);
+      const i64 ga = g[0], gb = g[m];
+      const i64 D0 = -gb, D1 = ga, S = D0 + D1;
+      const double sd = __ll2double_rn(S);
+      const double mu0 = __ddiv_rn(__ll2double_rn(D0), sd), mu1 = __ddiv_rn(__ll2double_rn(D1), sd);
+      double p[4];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        p[a] = __dadd_rn(__dmul_rn(mu0, (double)v[a]), __dmul_rn(mu1, (double)(v[a] + ((m >> a) & 1))));
+      if (slot < (unsigned long long)P.capacity) {
+        ftk_cp* r = P.out + slot;
+        r->face_id = vid * E + (m - 1);
+        P.fid[slot] = r->face_id;
+        r->label = -1;
+        r->x = p[0];
+        r->y = p[1];
+        r->z = D == 4 ? p[2] : 0.0;
+        r->t = p[D - 1];
+        r->type = gb >= 0 ? 1 : 0;
+        r->flags = ((m >> (D - 1)) & 1) ? 0u : FTK_CP_ORDINAL;
+      }
+    }
+    // cell pass (full cubes only)
+    if (exist != (1u << NC) - 1u && NC < 32) continue;
+    const Pairs<D>& PR = pairs<D>();
+    const Perms<D>& PM = perms<D>();
+    int8_t up[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) up[k] = (int8_t)k;
+    auto find = [&](int k) {
+      while (up[k] != k) k = up[k];
+      return k;
+    };
+    bool any = false;
+    for (int pi = 0; pi < PM.n; ++pi) {
+      int chain[D + 1];
+      chain[0] = 0;
+#pragma unroll
+      for (int k = 1; k <= D; ++k) chain[k] = chain[k - 1] | (1 << PM.p[pi][k - 1]);
+      int first = -1, cnt = 0;
+#pragma unroll
+      for (int a = 0; a <= D; ++a)
+#pragma unroll
+        for (int b = a + 1; b <= D; ++b) {
+          const int ca = chain[a], cb = chain[b];
+          if (((pos >> ca) & 1u) == ((pos >> cb) & 1u)) continue;
+          ++cnt;
+          const int sl = PR.slot[ca][cb];
+          if (first < 0) {
+            first = sl;
+          } else {
+            const int r1 = find(first), r2 = find(sl);
+            if (r1 != r2) up[max(r1, r2)] = (int8_t)min(r1, r2);
+          }
+        }
+      if (cnt != 0 && cnt != D && cnt != 2 * (D - 1)) atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
+      any = any || cnt > 0;
+    }
+    if (!any) continue;
+    // links: every crossed slot of a local component to the component's root slot
+    auto end_of = [&](int sl) -> long long {
+      const int ca = PR.a[sl], cb = PR.b[sl];
+      if (ca == 0) return rec_of(cb);
+      i64 id = 0, stride = 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        id += (v[a] + ((ca >> a) & 1)) * stride;
+        stride *= ext[a];
+      }
+      return -1 - (id * E + ((cb ^ ca) - 1));
+    };
+    for (int k = 0; k < NP; ++k) {
+      const int r = find(k);
+      if (r == k) continue;  // roots and untouched slots
+      const unsigned long long es = atomicAdd(&P.counters[CNT_EDGES], 1ull);
+      if (es < (unsigned long long)P.capacity) {
+        P.edges[2 * es] = end_of(r);
+        P.edges[2 * es + 1] = end_of(k);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    maxb = max(maxb, __shfl_xor_sync(0xffffffffu, maxb, o));
+    const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
+    maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
+  }
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(&P.counters[CNT_MAXBITS],
+              sizeof(T) == 4 ? (unsigned long long)maxb : (unsigned long long)__double_as_longlong(maxd));
+}
+
+template <typename T>
+static int launch_t(const ExtractParams& P, long long cq, int ndim, cudaStream_t stream) {
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (ndim == 2) k_iso<T, 3><<<sms * 16, 256, 0, stream>>>(P, cq);
+  else k_iso<T, 4><<<sms * 16, 256, 0, stream>>>(P, cq);
+  FTK_CUDA_TRY(cudaGetLastError());
+  return FTK_OK;
+}
+
+}  // namespace iso
+
+int launch_iso(const ExtractParams& P, long long cq, int ndim, cudaStream_t stream) {
+  return P.dtype == FTK_F32 ? iso::launch_t<float>(P, cq, ndim, stream) : iso::launch_t<double>(P, cq, ndim, stream);
+}
+
+}  // namespace ftk

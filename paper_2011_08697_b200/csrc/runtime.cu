@@ -1007,6 +1007,54 @@ int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_
                  stream);
 }
 
+// ------------------------------------------------------------------------------ isovolume tracking
+int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                  int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream_) {
+  int st = validate(desc);
+  if (st) return st;
+  if (is_vector(desc) || (desc->flags & FTK_GHOST_PLANE) || desc->t0 != 0 || desc->nt != desc->nt_global || desc->nt < 2)
+    return FTK_ERR_INVALID_ARG;
+  if (!d_field || !n_out || !d_ws || capacity < 0 || capacity > kMaxCapacity || (capacity > 0 && !d_out) ||
+      !(isovalue == isovalue))
+    return FTK_ERR_INVALID_ARG;
+  const Layout L = layout(capacity, esz_of(desc));
+  if (ws_bytes < L.total) return FTK_ERR_INVALID_ARG;
+  const double cqd = std::nearbyint(std::ldexp(isovalue, desc->scale_log2));
+  if (!(std::fabs(cqd) < std::ldexp(1.0, desc->ndim == 2 ? 59 : 38))) return FTK_ERR_RANGE;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  char* ws = static_cast<char*>(d_ws);
+  auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  FTK_CUDA_TRY(cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), stream));
+  ExtractParams EP = extract_params(desc, d_field, d_out, capacity, ws, L, counters, false);
+  st = launch_iso(EP, (long long)cqd, desc->ndim, stream);
+  if (st) return st;
+  TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters, false);
+  TP.T = desc->ndim == 2 ? 7 : 15;           // edge types per cube
+  TP.lookup_types = (1ull << TP.T) - 1ull;   // links may name any edge
+  TP.prelinked = false;
+  TP.verify = false;
+  TP.ghost_t = -1;
+  TP.first_t = -1;
+  const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
+  st = launch_track(TP, desc->ndim, ext, stream);
+  if (st) return st;
+  unsigned long long* host_cnt = pinned_counters();
+  FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+  FTK_CUDA_TRY(cudaStreamSynchronize(stream));
+  *n_out = (int64_t)host_cnt[CNT_NOUT];
+  st = range_status(desc, host_cnt[CNT_MAXBITS]);
+  if (st) return st;
+  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity) {
+    *n_out = std::max<int64_t>((int64_t)host_cnt[CNT_NOUT], (int64_t)host_cnt[CNT_EDGES]);
+    return FTK_ERR_CAPACITY;
+  }
+  if (host_cnt[CNT_INVARIANT]) {
+    g_last_error = "isovolume cells with a crossed-edge count not in {0, d, 2(d-1)}: " + std::to_string(host_cnt[CNT_INVARIANT]);
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
 int ftk_set_profiling(int enable) {
   g_profiling = enable;
   return FTK_OK;

@@ -127,8 +127,9 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   // one contiguous run per thread -- are within 15% on C2 but 3x slower on C4, where the union-find
   // working set is far beyond L2 and the shallow trees of the in-order unions matter.
   for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (i64)gridDim.x * blockDim.x) {
-    const long long a = P.edges[2 * e];
+    long long a = P.edges[2 * e];
     long long b = P.edges[2 * e + 1];
+    if (a < 0) a = lookup(P, hm, -1 - a);  // isovolume links may name both ends by id
     if (b < 0) {
       const long long f = -1 - b;
       b = lookup(P, hm, f);  // face owned by the neighbour cube
