@@ -375,6 +375,35 @@ def run_ours(args):
                      "timing": "wall clock per synchronous call, after one warm track"}
         del tj, rec_p
 
+    # isovolume tracking on the same field: spacetime edges
+    # tested per second by ftk_iso_track (isovalue 0.5 in 2D; 1.9 near the maxima of the 3D fields, whose
+    # 0.5-level isovolume would not fit next to the field), CUDA events around the synchronous call
+    iso_line = None
+    if world == 1 and not args.no_e2e and not vec:
+        iso_val = 1.9 if d3 else 0.5
+        rec_i, buf_i = ftk.iso_track(field, cfg.scale_log2, iso_val, return_buffers=True)
+        ext = list(spatial) + [nt_global]
+        n_edges = 0
+        for m in range(1, 1 << len(ext)):
+            k = 1
+            for a, n in enumerate(ext):
+                k *= n - ((m >> a) & 1)
+            n_edges += k
+        i_ms = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ftk.iso_track(field, cfg.scale_log2, iso_val, buffers=buf_i)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            i_ms.append(e0.elapsed_time(e1))
+        i_best = min(i_ms)
+        iso_line = {"isovalue": iso_val, "edges_per_step": n_edges, "value": n_edges / (i_best / 1000.0),
+                    "unit": "spacetime edges/s", "ms": i_best, "records": int(rec_i.shape[0]),
+                    "components": int(len(torch.unique(rec_i[:, 1]))) if rec_i.shape[0] else 0,
+                    "timing": "CUDA events around ftk_iso_track (edge + cell pass + pass 2), best of 5"}
+        del rec_i, buf_i
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -399,6 +428,7 @@ def run_ours(args):
         "e2e": e2e,
         "stream": stream_line,
         "post": post_line,
+        "iso": iso_line,
         # K1a (+ k_expand2d in 2D) + K1b + k_clear + k_hash_insert + k_edges + k_label; time slabs add
         # k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
         "gpu_launches": ((6 if d3 else 7) + (6 if world > 1 else 0)) * args.steps,

@@ -100,8 +100,12 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
   const T* F = reinterpret_cast<const T*>(P.field);
   uint32_t maxb = 0;
   double maxd = 0.0;
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += (i64)gridDim.x * blockDim.x) {
-    i64 v[4], rem = i;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform loop (the record and link slots are reserved with one atomic per warp)
+  for (i64 base = (i64)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nv; base += (i64)gridDim.x * blockDim.x) {
+    const i64 i = base + lane;
+    const bool active = i < nv;
+    i64 v[4], rem = active ? i : 0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       v[a] = a < D - 1 ? rem % ext[a] : rem;
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
         stride *= ext[a];
       }
       g[c] = 0;
-      if (in) {
+      if (in && active) {
         const T f = __ldg(F + off);
         if (c == 0) {
           if constexpr (sizeof(T) == 4) maxb = max(maxb, __float_as_uint(f) & 0x7fffffffu);
@@ -136,16 +140,30 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
         pos |= (g[c] >= 0 ? 1u : 0u) << c;
       }
     }
-    if (pos == 0 || pos == exist) continue;  // one sign on every corner: nothing crosses this cube
+    const bool mixed = !(pos == 0 || pos == exist);  // one sign on every corner: nothing crosses this cube
     // edge pass: crossed edges anchored at v
     uint32_t emask = 0;
     const uint32_t s0 = pos & 1u;
+    if (mixed) {
 #pragma unroll
-    for (int m = 1; m < NC; ++m)
-      if (((exist >> m) & 1u) && (((pos >> m) & 1u) != s0)) emask |= 1u << m;
+      for (int m = 1; m < NC; ++m)
+        if (((exist >> m) & 1u) && (((pos >> m) & 1u) != s0)) emask |= 1u << m;
+    }
     const int nrec = __popc(emask);
-    unsigned long long rbase = 0;
-    if (nrec) rbase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)nrec);
+    auto warp_reserve = [&](int n, int ctr) -> unsigned long long {
+      int incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned long long b0 = 0;
+      if (lane == 31 && total) b0 = atomicAdd(&P.counters[ctr], (unsigned long long)total);
+      b0 = __shfl_sync(0xffffffffu, b0, 31);
+      return b0 + (unsigned long long)(incl - n);
+    };
+    const unsigned long long rbase = warp_reserve(nrec, CNT_NOUT);
     i64 vid = 0;
     {
       i64 stride = 1;
@@ -183,7 +201,7 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
       }
     }
     // cell pass (full cubes only)
-    if (exist != (1u << NC) - 1u && NC < 32) continue;
+    const bool cells = mixed && exist == (1u << NC) - 1u;
     const Pairs<D>& PR = pairs<D>();
     const Perms<D>& PM = perms<D>();
     int8_t up[NP];
@@ -193,8 +211,7 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
       while (up[k] != k) k = up[k];
       return k;
     };
-    bool any = false;
-    for (int pi = 0; pi < PM.n; ++pi) {
+    for (int pi = 0; cells && pi < PM.n; ++pi) {
       int chain[D + 1];
       chain[0] = 0;
 #pragma unroll
@@ -216,9 +233,7 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
           }
         }
       if (cnt != 0 && cnt != D && cnt != 2 * (D - 1)) atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
-      any = any || cnt > 0;
     }
-    if (!any) continue;
     // links: every crossed slot of a local component to the component's root slot
     auto end_of = [&](int sl) -> long long {
       const int ca = PR.a[sl], cb = PR.b[sl];
@@ -231,14 +246,17 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
       }
       return -1 - (id * E + ((cb ^ ca) - 1));
     };
-    for (int k = 0; k < NP; ++k) {
+    int nlink = 0;
+    for (int k = 0; cells && k < NP; ++k) nlink += up[k] != k;
+    unsigned long long es = warp_reserve(nlink, CNT_EDGES);
+    for (int k = 0; cells && k < NP; ++k) {
+      if (up[k] == k) continue;  // roots and untouched slots
       const int r = find(k);
-      if (r == k) continue;  // roots and untouched slots
-      const unsigned long long es = atomicAdd(&P.counters[CNT_EDGES], 1ull);
       if (es < (unsigned long long)P.capacity) {
         P.edges[2 * es] = end_of(r);
         P.edges[2 * es + 1] = end_of(k);
       }
+      ++es;
     }
   }
 #pragma unroll
