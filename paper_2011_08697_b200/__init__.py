@@ -419,9 +419,10 @@ def _np_ptr(a):
     return ctypes.c_void_p(a.ctypes.data) if a is not None and a.size else None
 
 
-def stitch_export(field: torch.Tensor, scale_log2: int, t0: int, nt_global: int, ghost: bool, buffers: Buffers):
+def stitch_export(field: torch.Tensor, scale_log2: int, t0: int, nt_global: int, ghost: bool, buffers: Buffers,
+                  vector: bool = False):
     """After track() on a slab with these buffers: the slab's (A, B) pair lists as int64 [n, 2]."""
-    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost)
+    desc = make_desc(tuple(field.shape), field.dtype, scale_log2, t0, nt_global, ghost, vector=vector)
     nA, nB = ctypes.c_int64(0), ctypes.c_int64(0)
     args = lambda a, b, ca, cb: [ctypes.byref(desc), ctypes.c_void_p(buffers.workspace.data_ptr()),
                                  buffers.workspace.numel(), buffers.capacity, _np_ptr(a), ca, ctypes.byref(nA),

@@ -20,15 +20,15 @@ def ftk():
     return m
 
 
-def run_slabs(ftk, field_cpu, s, G):
+def run_slabs(ftk, field_cpu, s, G, vector=False):
     nt = field_cpu.shape[0]
     b = ftk.slab_bounds(nt, G)
     parts = []
     for r in range(G):
         ghost = r < G - 1
         sub = field_cpu[b[r]: b[r + 1] + (1 if ghost else 0)].contiguous().cuda()
-        rec, buf = ftk.track(sub, s, t0=b[r], nt_global=nt, ghost=ghost, return_buffers=True)
-        A, B = ftk.stitch_export(sub, s, b[r], nt, ghost, buf)
+        rec, buf = ftk.track(sub, s, t0=b[r], nt_global=nt, ghost=ghost, return_buffers=True, vector=vector)
+        A, B = ftk.stitch_export(sub, s, b[r], nt, ghost, buf, vector=vector)
         parts.append((sub, rec, buf, A, B))
     GA = np.concatenate([p[3] for p in parts])
     GB = np.concatenate([p[4] for p in parts])
@@ -64,6 +64,18 @@ def test_virtual_slabs_3d(ftk, oracle_lib):
     ref, _, _ = oracle_lib.track(f.numpy(), 26)
     ref = _sorted(ref)
     assert np.array_equal(got["face_id"], ref["face_id"]) and np.array_equal(got["label"], ref["label"])
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_virtual_slabs_vector(ftk, oracle_lib, G):
+    """time slabs of 2D and 3D vector fields (FTK_VECTOR_FIELD): same records and labels as one domain"""
+    for f, s in ((fi.DoubleGyre(150, 75, 23).generate(), 26), (fi.ABCFlow(24, 20, 18, 9).generate(), 26)):
+        got = _sorted(run_slabs(ftk, f, s, G, vector=True))
+        single = _sorted(ftk.to_numpy(ftk.track(f.cuda(), s, vector=True)))
+        ref, _, _ = oracle_lib.track(f.numpy(), s, vector=True)
+        ref = _sorted(ref)
+        assert got.tobytes() == single.tobytes()
+        assert np.array_equal(got["face_id"], ref["face_id"]) and np.array_equal(got["label"], ref["label"])
 
 
 def test_nccl_communicator_single_rank(ftk):
