@@ -545,9 +545,11 @@ __device__ __forceinline__ void emit_record(const Win<T>& w, const Geo& G, const
     pt[k] = (double)(t + pl);
     // interior vertex: the Hessian stencil centre is the vertex itself, window (mx+1, my+1)
     const int* Q = q + pl * 16 + (my + 1) * 4 + (mx + 1);
-    Hd[k][0] = __ll2double_rn(4ll * ((i64)Q[1] - 2ll * Q[0] + Q[-1]));
-    Hd[k][1] = __ll2double_rn((i64)Q[5] - Q[-3] - Q[3] + Q[-5]);
-    Hd[k][2] = __ll2double_rn(4ll * ((i64)Q[4] - 2ll * Q[0] + Q[-4]));
+    // |q| < 2^29 on the fast path: every second difference fits int32, and the 4x scale is an exact
+    // FP64 multiply (the same values as the int64 expressions of the general path)
+    Hd[k][0] = __dmul_rn(4.0, __int2double_rn(Q[1] - 2 * Q[0] + Q[-1]));
+    Hd[k][1] = __int2double_rn(Q[5] - Q[-3] - Q[3] + Q[-5]);
+    Hd[k][2] = __dmul_rn(4.0, __int2double_rn(Q[4] - 2 * Q[0] + Q[-4]));
   }
   const double lx = dot3_nofma(mu, px[0], px[1], px[2]);
   const double ly = dot3_nofma(mu, py[0], py[1], py[2]);
