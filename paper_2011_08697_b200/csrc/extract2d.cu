@@ -1,35 +1,31 @@
-// extract2d.cu -- K1: pass 1 of Alg. 1 for 2D+t on sm_100a.
+// extract2d.cu -- K1: pass 1 of Alg. 1 for 2D+t on sm_100a, split into three
+// kernels:
 //
-// Persistent kernel, 2 CTAs per SM.  A work item is a 124 x 32 tile of anchors (x, y) times a chunk
-// of anchor timesteps; CTAs pull items from a global counter and march t through them.  Each CTA is
-// warp-specialised:
-//
-//   producer warp -- fetches items and, plane after plane, stages the tile with its halo
-//     (x0-4 .. x0+131, y0-2 .. y0+34) into an NSTAGE-deep shared-memory ring with TMA
-//     (cp.async.bulk.tensor) under full/empty mbarriers, so every vertex is read from HBM once and
-//     reused by all 12 faces of the 8 cubes it belongs to (north_star (2)).
-//
-//   8 scan warps (4 anchor rows x 124 columns each; lane = 4 consecutive x, lane 31 is a halo lane)
-//     -- a CONSERVATIVE sign prefilter on raw field values.  For the gradient component
-//     g_a = q[+a] - q[-a] (q = rint(f 2^s)) the float test d = f[+a] - f[-a] >= 2^(1-s) implies
-//     g_a > 0 exactly, and d < -2^(1-s) implies g_a < 0.  The sign bits of
-//     d -+ 2^(1-s) (paired FADD2) are funnel-shifted into a 4-bit code per vertex (bit = 1: that
-//     strict sign condition does NOT hold) and ORed over the 8 corners of each spacetime cube: a
-//     nibble with a zero bit means one gradient component has one strict sign on every corner, so no
-//     face of the cube can contain the origin -- even under SoS (the perturbation is infinitesimal).
-//     Grid boundaries are handled by patching the neighbour values in registers (one-sided
-//     differences) and masking codes of positions outside the grid.  The plane stage is released as
-//     soon as all scan warps are through it; the anchors of the surviving cubes (~0.5% on the woven
-//     field, ~2 per warp and plane) go into a CTA survivor queue (3 words each).
-//
-//   3 exact warps -- take the queue in batches of 32 cubes (one per lane), fetch each cube's 4x4x2
-//     window from global memory (it was streamed through L2 microseconds earlier), exact int32
-//     quantization and gradients, the 19 distinct 2x2 determinants of the cube's 12 faces, SoS
-//     point-in-simplex (an exact int64/int128 path covers boundary cubes, zero
-//     determinants and large values); the punctured faces are then spread over the lanes and each gets
-//     its Eq. 2 location and Hessian type in fixed-order FP64 (no FMA), written with one global atomic
-//     per batch.  Exact work never holds a plane stage, so the TMA pipeline keeps NSTAGE-1 planes in
-//     flight per CTA whatever the survivor density.
+//   K1a k_scan2d -- persistent, 2 CTAs per SM.  A work item is a 128 x 64 tile of anchors (x, y) times
+//     a chunk of anchor timesteps; CTAs pull items from a global counter and march t through them.
+//     Warp-specialised:
+//     producer warp -- stages each plane of the tile with its halo (x0-4 .. x0+131, y0-1 .. y0+65)
+//       into an NSTAGE-deep shared-memory ring with TMA (cp.async.bulk.tensor) under full/empty
+//       mbarriers, so every vertex is read from HBM once and reused by all 12 faces of the 8 cubes it
+//       belongs to (north_star (2));
+//     8 scan warps (8 anchor rows x 128 columns each; lane = 4 consecutive x) -- a CONSERVATIVE sign
+//       prefilter on raw field values: for g_a = q[+a] - q[-a] (q = rint(f 2^s)) the float test
+//       d = f[+a] - f[-a] > 2^(1-s) implies g_a > 0 exactly, d < -2^(1-s) implies g_a < 0.  The sign
+//       bits of 2^(1-s) - d and d + 2^(1-s) (paired FADD2) are gathered into a 4-bit "strict sign
+//       holds" code per vertex and ANDed over the 8 corners of each spacetime cube (y-pair in
+//       registers, x-pair by one shuffle plus the codes of column x0 + 128, t-pair with the previous
+//       plane); a zero byte means no component has one strict sign on every corner, so the cube may
+//       hold a punctured face -- a survivor.  A cube with a one-signed component cannot, even under
+//       SoS (the perturbation is infinitesimal).  Grid boundaries: neighbour values patched in
+//       registers (one-sided differences), out-of-grid positions AND-neutral.  Survivors leave as
+//       group entries (one per lane: first anchor, plane flag, 32-bit survivor mask).
+//   k_expand2d -- group entries -> dense cube list (one atomic per block).
+//   K1b k_exact2d -- one warp per batch of 32 cubes (one per lane): the cube's 4x4x2 window from the
+//     field, exact int32 quantization and gradients, the 19 distinct 2x2 determinants of the 12 faces,
+//     SoS point-in-simplex (an exact int64/int128 path covers boundary cubes, zero
+//     determinants and large values), the 6 cells (in-cube pairs joined, pairs with a neighbour cube's
+//     face emitted as edges), then the punctured faces spread over the lanes for the Eq. 2 location
+//     and Hessian type in fixed-order FP64 (no FMA).
 #include <cuda.h>
 
 #include <algorithm>
