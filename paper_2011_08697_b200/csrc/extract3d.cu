@@ -3,18 +3,20 @@
 // Pass 1 of Alg. 1 (generalised at P:439) plus the per-hypercube cell evaluation of
 // pass 2, split like the 2D path:
 //
-//   K1a k_scan3d (namespace s3): TMA 4D halo boxes of 124 x 8 x 8 anchor tiles per timestep, one warp
+//   K1a k_scan3d (namespace s3): TMA 4D halo boxes of 128 x 8 x 8 anchor tiles per timestep, one warp
 //     per z-slice; per vertex a 6-bit "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) on raw
 //     values, thr = 2^(1-s), which implies the exact integer gradient component is strictly
 //     positive/negative; ANDed over the 16 corners of the spacetime hypercube
 //     (y/x pairs in registers, z pairs through shared memory, t pairs across planes); a zero code is a
 //     survivor and its anchor goes to the survivor list.
-//   K1b k_exact3d: one surviving hypercube per thread, straight from the field: int64 gradients, the
-//     60 face types with exact 3x3 determinants (int128) and the SoS epsilon-expansion of det(M + E)
-//     evaluated term by term in decreasing magnitude (R4/R5), Eq. 2
-//     location and the Descartes-rule Hessian type in fixed-order FP64, and the 24 cells
-//     (pentachora) of the hypercube: 0 or 2 punctured sides each, emitted as
-//     trajectory edges.
+//   K1b k_exact3d: one warp per surviving hypercube, straight from the field: int64 gradients of the 16
+//     corners, the 60 face types two per lane with 3x3 determinant signs from an FP64 filter (exact
+//     int128 and the SoS epsilon-expansion of det(M + E) when it cannot decide; PAPER.md:465-467;
+//     DESIGN.md R4/R5), Eq. 2 location and the Descartes-rule Hessian type in fixed-order FP64, and
+//     the 24 cells (pentachora) of the hypercube: 0 or 2 punctured sides each, emitted
+//     as trajectory edges.
+//   Vector fields (FTK_VECTOR_FIELD): k_scanvec3d (namespace v3) and k_exact3d<T, true> (quantized
+//     corner vectors, Routh-Hurwitz Jacobian type).
 #include <cstdio>
 #include <cstring>
 #include <utility>
