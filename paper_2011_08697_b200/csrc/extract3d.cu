@@ -1045,6 +1045,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
   constexpr int NH = VEC ? 9 : 6;
   __shared__ i64 sg[XW3][16][3];
   __shared__ i64 sH[XW3][16][NH];  // corner Hessians / Jacobians (hypercubes with punctured faces)
+  __shared__ i64 sW[XW3][128];     // interior hypercubes: the quantized 4x4x4 x 2-plane window
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Geo3 G;
   G.nx = P.nx;
@@ -1066,6 +1067,21 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
     const i64 x = P.wx[e], y = P.wy[e], z = P.wz[e];
     const GTile<T> A{field + (t - P.t0) * plane};
     const GTile<T> B{hasB ? A.S + plane : A.S};
+    // interior hypercube (scalar field): the window x-1..x+2, y-1..y+2, z-1..z+2 of planes t, t+1,
+    // quantized once into shared memory (4 values per lane); every corner is an interior vertex, so
+    // its central differences and compact Hessian stencil read the window only
+    const bool inner = !VEC && hasB && x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny && z >= 1 && z + 2 < G.nz;
+    i64* W = sW[w];
+    auto wat = [&](int pl, int zz, int yy, int xx) -> i64 { return W[pl * 64 + zz * 16 + yy * 4 + xx]; };
+    if (inner) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = lane * 4 + j;
+        const int xx = k & 3, yy = (k >> 2) & 3, zz = (k >> 4) & 3, pl = k >> 6;
+        W[k] = quant3((pl ? B : A).at(G, x - 1 + xx, y - 1 + yy, z - 1 + zz), G);
+      }
+      __syncwarp();
+    }
     // corner gradients
     uint32_t ex = 0;
     {
@@ -1074,7 +1090,12 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
       const bool e1 = cx < G.nx && cy < G.ny && cz < G.nz && ((c & 8) == 0 || hasB);
       if (lane < 16) {
         i64 gc[3] = {0, 0, 0};
-        if (e1) {
+        if (inner) {
+          const int lx = 1 + (c & 1), ly = 1 + ((c >> 1) & 1), lz = 1 + ((c >> 2) & 1), pl = c >> 3;
+          gc[0] = wat(pl, lz, ly, lx + 1) - wat(pl, lz, ly, lx - 1);
+          gc[1] = wat(pl, lz, ly + 1, lx) - wat(pl, lz, ly - 1, lx);
+          gc[2] = wat(pl, lz + 1, ly, lx) - wat(pl, lz - 1, ly, lx);
+        } else if (e1) {
           if constexpr (VEC) {
             const T* q = ((c & 8) ? B : A).S + ((cz * G.ny + cy) * G.nx + cx) * 3;
 #pragma unroll
@@ -1124,8 +1145,22 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
       const int c = lane & 15;
       if (lane < 16 && ((ex >> c) & 1))
       {
-        if constexpr (VEC) jac3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
-        else hess3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+        if constexpr (VEC) {
+          jac3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+        } else if (inner) {  // compact stencil inside the window (order xx xy xz yy yz zz, as hess3)
+          const int l[3] = {1 + (c & 1), 1 + ((c >> 1) & 1), 1 + ((c >> 2) & 1)};
+          const int pl = c >> 3;
+          auto q = [&](int dx, int dy, int dz) { return wat(pl, l[2] + dz, l[1] + dy, l[0] + dx); };
+          i64* H = sH[w][c];
+          H[0] = 4 * (q(1, 0, 0) - 2 * q(0, 0, 0) + q(-1, 0, 0));
+          H[1] = q(1, 1, 0) - q(1, -1, 0) - q(-1, 1, 0) + q(-1, -1, 0);
+          H[2] = q(1, 0, 1) - q(1, 0, -1) - q(-1, 0, 1) + q(-1, 0, -1);
+          H[3] = 4 * (q(0, 1, 0) - 2 * q(0, 0, 0) + q(0, -1, 0));
+          H[4] = q(0, 1, 1) - q(0, 1, -1) - q(0, -1, 1) + q(0, -1, -1);
+          H[5] = 4 * (q(0, 0, 1) - 2 * q(0, 0, 0) + q(0, 0, -1));
+        } else {
+          hess3<T>(P, G, x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1), t + ((c >> 3) & 1), sH[w][c]);
+        }
       }
       __syncwarp();
     }
