@@ -74,6 +74,15 @@ constexpr PP3 make_pp3() {
 __constant__ PP3 cPP3 = make_pp3();
 static_assert(make_pp3().n == 34, "34 monomials for 3x3");
 
+// the same determinant when every entry is below 2^31 in magnitude: the 2x2 minors are exact in int64
+// (|.| < 2^63) and only the three outer products need 64 x 64 -> 128-bit multiplies
+__device__ __forceinline__ i128 det3_mid(const i64* a, const i64* b, const i64* c) {
+  const long long m0 = b[1] * c[2] - b[2] * c[1];
+  const long long m1 = b[0] * c[2] - b[2] * c[0];
+  const long long m2 = b[0] * c[1] - b[1] * c[0];
+  return (i128)a[0] * m0 - (i128)a[1] * m1 + (i128)a[2] * m2;
+}
+
 __device__ __forceinline__ i128 det3(const i64* a, const i64* b, const i64* c) {
   return (i128)a[0] * ((i128)b[1] * c[2] - (i128)b[2] * c[1]) - (i128)a[1] * ((i128)b[0] * c[2] - (i128)b[2] * c[0]) +
          (i128)a[2] * ((i128)b[0] * c[1] - (i128)b[1] * c[0]);
@@ -121,12 +130,13 @@ __device__ __forceinline__ int det3_sign_fp(const i64* a, const i64* b, const i6
   return d > bound ? 1 : (d < -bound ? -1 : 0);
 }
 
-__device__ __forceinline__ int sos3(const i64* r0, const i64* r1, const i64* r2, bool small) {
+// small: every entry < 2^26 (the FP64 filter applies); mid: every entry < 2^31 (det3_mid applies)
+__device__ __forceinline__ int sos3(const i64* r0, const i64* r1, const i64* r2, bool small, bool mid) {
   if (small) {
     const int f = det3_sign_fp(r0, r1, r2);
     if (f) return f;
   }
-  const i128 d = det3(r0, r1, r2);
+  const i128 d = mid ? det3_mid(r0, r1, r2) : det3(r0, r1, r2);
   if (d != 0) return d > 0 ? 1 : -1;
   return sos3_chain(r0, r1, r2);
 }
@@ -208,13 +218,13 @@ __device__ __forceinline__ double dot4_nofma(const double* mu, const double* v) 
 // punctured test of a face with vertex gradients g[0..3] (rows in global vertex order):
 // s_k = (-1)^(k+3) sos(rows != k), all equal
 // small: every entry |.| < 2^26 (the floating-point filter of det3_sign_fp applies)
-__device__ __forceinline__ bool punctured4(const i64 (&g)[4][3], bool small) {
-  const int s0 = -sos3(g[1], g[2], g[3], small);
-  const int s1 = sos3(g[0], g[2], g[3], small);
+__device__ __forceinline__ bool punctured4(const i64 (&g)[4][3], bool small, bool mid) {
+  const int s0 = -sos3(g[1], g[2], g[3], small, mid);
+  const int s1 = sos3(g[0], g[2], g[3], small, mid);
   if (s0 != s1) return false;
-  const int s2 = -sos3(g[0], g[1], g[3], small);
+  const int s2 = -sos3(g[0], g[1], g[3], small, mid);
   if (s0 != s2) return false;
-  const int s3 = sos3(g[0], g[1], g[2], small);
+  const int s3 = sos3(g[0], g[1], g[2], small, mid);
   return s0 == s3;
 }
 
@@ -1112,12 +1122,14 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
     }
     __syncwarp();
     // all 48 gradient components below 2^26 in magnitude: the FP64 determinant filter applies
-    bool small;
+    bool small, mid;
     {
       const int c = lane & 15;
-      const i64 lim = 1ll << 26;
+      const i64 lim = 1ll << 26, lim31 = 1ll << 31;
       small = __all_sync(0xffffffffu, g[c][0] > -lim && g[c][0] < lim && g[c][1] > -lim && g[c][1] < lim &&
                                           g[c][2] > -lim && g[c][2] < lim);
+      mid = __all_sync(0xffffffffu, g[c][0] > -lim31 && g[c][0] < lim31 && g[c][1] > -lim31 && g[c][1] < lim31 &&
+                                        g[c][2] > -lim31 && g[c][2] < lim31);
     }
     // the 60 face types, two per lane
     unsigned long long pmask = 0;
@@ -1135,7 +1147,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
           for (int j = 0; j < 3; ++j)
             rej |= (gv[0][j] > 0 && gv[1][j] > 0 && gv[2][j] > 0 && gv[3][j] > 0) ||
                    (gv[0][j] < 0 && gv[1][j] < 0 && gv[2][j] < 0 && gv[3][j] < 0);
-          pu = !rej && punctured4(gv, small);
+          pu = !rej && punctured4(gv, small, mid);
         }
       }
       pmask |= (unsigned long long)__ballot_sync(0xffffffffu, pu) << (32 * h);
@@ -1185,7 +1197,7 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
                               {g[cd.w[2]][0], g[cd.w[2]][1], g[cd.w[2]][2]},
                               {g[cd.w[3]][0], g[cd.w[3]][1], g[cd.w[3]][2]},
                               {g[15][0], g[15][1], g[15][2]}};
-        if (punctured4(gu, small)) {
+        if (punctured4(gu, small, mid)) {
           if (k < 2) {
             const int a1 = cd.w[1];
             const i64 fx = x + (a1 & 1), fy = y + ((a1 >> 1) & 1), fz = z + ((a1 >> 2) & 1), ft = t + ((a1 >> 3) & 1);
@@ -1223,10 +1235,10 @@ __global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ Ex
 #pragma unroll
         for (int j = 0; j < 3; ++j) gv[kk][j] = g[m[kk]][j];
       // D_k = (-1)^(k+3) det(rows != k)  (Eq. 2)
-      const i128 D0 = -det3(gv[1], gv[2], gv[3]);
-      const i128 D1 = det3(gv[0], gv[2], gv[3]);
-      const i128 D2 = -det3(gv[0], gv[1], gv[3]);
-      const i128 D3 = det3(gv[0], gv[1], gv[2]);
+      const i128 D0 = -(mid ? det3_mid(gv[1], gv[2], gv[3]) : det3(gv[1], gv[2], gv[3]));
+      const i128 D1 = mid ? det3_mid(gv[0], gv[2], gv[3]) : det3(gv[0], gv[2], gv[3]);
+      const i128 D2 = -(mid ? det3_mid(gv[0], gv[1], gv[3]) : det3(gv[0], gv[1], gv[3]));
+      const i128 D3 = mid ? det3_mid(gv[0], gv[1], gv[2]) : det3(gv[0], gv[1], gv[2]);
       const i128 S = D0 + D1 + D2 + D3;
       double mu[4];
       uint32_t flags = 0;
