@@ -1050,8 +1050,11 @@ constexpr int XW3 = 4;  // warps per block
 
 // VEC: a 3D vector field [t][z][y][x][3] (FTK_VECTOR_FIELD): the corner values are the quantized
 // vectors themselves and the type comes from the Jacobian (R17)
+#ifndef FTK_X3_MINB
+#define FTK_X3_MINB 8  // 8 blocks of 4 warps per SM (64 registers, ~240 B spilled to L1; C5 K1b 1.01 -> 0.79 ms, C3 0.107 -> 0.121 ms)
+#endif
 template <typename T, bool VEC = false>
-__global__ void __launch_bounds__(XW3 * 32) k_exact3d(const __grid_constant__ ExtractParams P) {
+__global__ void __launch_bounds__(XW3 * 32, FTK_X3_MINB) k_exact3d(const __grid_constant__ ExtractParams P) {
   constexpr int NH = VEC ? 9 : 6;
   __shared__ i64 sg[XW3][16][3];
   __shared__ i64 sH[XW3][16][NH];  // corner Hessians / Jacobians (hypercubes with punctured faces)

@@ -15,6 +15,10 @@ VARIANTS = {
     "vminb4": ["FTK_V_MINB=4"],
     "vminb6": ["FTK_V_MINB=6"],
     "v3m3": ["FTK_V3_MINB=3"],
+    "x3m1": ["FTK_X3_MINB=1"],
+    "x3m4": ["FTK_X3_MINB=4"],
+    "x3m6": ["FTK_X3_MINB=6"],
+    "x3m8": ["FTK_X3_MINB=8"],
     "vminb8": ["FTK_V_MINB=8"],
 }
 names = sys.argv[1:] or list(VARIANTS)
