@@ -348,8 +348,14 @@ template <typename T>
 constexpr int slices() { return nzw<T>() + 3; }         // z0-1 .. z0+NZW+1
 template <typename T>
 constexpr int nstage() { return sizeof(T) == 4 ? 3 : 2; }
+#ifndef FTK_S3_SPLIT
+#define FTK_S3_SPLIT 1  // 2 (16 + 2 scan warps of 4 code rows) measured on C5: K1a 1.885 -> 1.872 ms, kept at 1
+#endif
+constexpr int SPLIT = FTK_S3_SPLIT;  // warps per z-slice (each owns RW / SPLIT code-row pairs)
+constexpr int RWW = RW / SPLIT;
+static_assert(RW % SPLIT == 0, "SPLIT divides RW");
 template <typename T>
-constexpr int nthreads() { return (nzw<T>() + 2) * 32; }  // NZW slice warps + top warp + producer
+constexpr int nthreads() { return ((nzw<T>() + 1) * SPLIT + 1) * 32; }  // NZW + 1 slices x SPLIT warps + producer
 template <typename T>
 constexpr int stage_elems() { return (PITCH * ROWS * slices<T>() * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T); }
 constexpr uint32_t NEUTRAL = 0xFCFCFCFCu;
@@ -419,9 +425,9 @@ struct Ctx {
 // squares (AND over y-pair and x-pair) of the slice whose centre rows start at S (row 0 = y0-1),
 // with the z -+ 1 slices at S -/+ slice_stride.  MODE 0: interior; 1: x boundary only (one-sided
 // x differences, out-of-grid columns); 2: any boundary (fp64 input treats 1 as 2).
-template <typename T, int MODE>
+template <typename T, int MODE, int NR>
 __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx& c, f2 thr2, f2 nthr2, T thr,
-                                              uint32_t (&Sq)[RW], uint32_t& maxb, double& maxd, bool count) {
+                                              uint32_t (&Sq)[NR], uint32_t& maxb, double& maxd, bool count) {
   constexpr bool XE = MODE >= 1, EDGE = sizeof(T) == 4 ? MODE >= 2 : MODE >= 1;
   const bool lane0 = c.lane == 0, lane31 = c.lane == 31;
   const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
@@ -448,7 +454,7 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
     // computes code row k (centre row k + 1), Ye = the y-pair of code rows k, k + 1
     uint32_t Ye;
     {
-      const int k = min(c.lane, RW);
+      const int k = min(c.lane, NR);
       const int o = (k + 1) * PITCH + XOFF + LX;
       const float ctr = S[o], l = S[o - 1];
       float r = S[o + 1], u = S[o - PITCH], d = S[o + PITCH], zm = Zm[o], zp = Zp[o];
@@ -480,9 +486,9 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
     load(1, v1, l1, r1);
     uint32_t Cprev = 0;
 #pragma unroll
-    for (int k = 0; k <= RW; ++k) {
+    for (int k = 0; k <= NR; ++k) {
       load(k + 2, v2, l2, r2);
-      if (count && k < RW) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);
+      if (count && k < NR) maxb = max_abs_bits(maxb, v1.x, v1.y, v1.z, v1.w);
       const float4 zm = *reinterpret_cast<const float4*>(Zm + (k + 1) * PITCH + XOFF + 4 * c.lane);
       const float4 zp = *reinterpret_cast<const float4*>(Zp + (k + 1) * PITCH + XOFF + 4 * c.lane);
       uint32_t C;
@@ -528,7 +534,7 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
     };
     uint32_t Ye;  // codes of column x0 + 128 (as for fp32)
     {
-      const int k = min(c.lane, RW);
+      const int k = min(c.lane, NR);
       const int o = (k + 1) * PITCH + XOFF + LX;
       const double ctr = S[o], l = S[o - 1];
       double r = S[o + 1], u = S[o - PITCH], d = S[o + PITCH], zm = Zm[o], zp = Zp[o];
@@ -551,9 +557,9 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
     load(1, f1);
     uint32_t Cprev = 0;
 #pragma unroll
-    for (int k = 0; k <= RW; ++k) {
+    for (int k = 0; k <= NR; ++k) {
       load(k + 2, f2_);
-      if (count && k < RW)
+      if (count && k < NR)
 #pragma unroll
         for (int q = 1; q <= 4; ++q) {
           const double a = fabs(f1[q]);
@@ -593,7 +599,7 @@ template <typename T, bool TMA>
 __global__ void __launch_bounds__(nthreads<T>(), 1)
     k_scan3d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
   constexpr int NZW = nzw<T>(), SL = slices<T>(), NSTAGE = nstage<T>();
-  constexpr int PRODUCER = NZW + 1;
+  constexpr int PRODUCER = (NZW + 1) * SPLIT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t mis = smem_u32(smem_raw) & 127u;
   Smem<T>& sm = *reinterpret_cast<Smem<T>*>(smem_raw + (mis ? 128 - mis : 0));
@@ -609,7 +615,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     sm.maxbits64 = 0;
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], NZW + 1);
+      mbar_init(&sm.empty[s], (NZW + 1) * SPLIT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -670,16 +676,18 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
       mbar_arrive(&sm.full[s]);
     }
   } else {
-    // scan warps: warp w owns slice z0 + w (w = NZW: the top slice, squares only)
+    // scan warps: warp w owns slice z0 + w / SPLIT, code-row pairs r0 .. r0 + RWW - 1 (r0 = (w % SPLIT) *
+    // RWW); slice NZW is the top slice (squares only)
+    const int slice = warp / SPLIT, r0 = (warp % SPLIT) * RWW;
     const T thr = (T)P.thr;
     const f2 thr2 = pack2((float)P.thr, (float)P.thr);
     const f2 nthr2 = pack2(-(float)P.thr, -(float)P.thr);
     uint32_t maxb32 = 0;
     double maxd = 0.0;
     unsigned long long mysurv = 0;
-    uint32_t prevK[RW];
+    uint32_t prevK[RWW];
     long long cur = 0, end = 0;
-    const bool top = warp == NZW;
+    const bool top = slice == NZW;
     const uint32_t lt_mask = (1u << lane) - 1u;
     auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0, int z) {
       const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
@@ -762,8 +770,8 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
         y0 = m.y0;
         z0 = m.z0;
         const i64 gx = (i64)x0 + 4 * lane;
-        c.gy0 = y0;
-        c.gz = z0 + warp;
+        c.gy0 = y0 + r0;
+        c.gz = z0 + slice;
         c.lpat = gx == 0;
         c.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
         c.oob = 0;
@@ -776,40 +784,40 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
         c.xe_out = x0 + LX >= nx;
         c.xe_last = x0 + LX == nx - 1;
       }
-      const T* S = sm.plane[s] + (warp + 1) * (PITCH * ROWS);  // slice z0 + warp
-      uint32_t Sq[RW];
-      if (mode == 2) slice_squares<T, 2>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      else if (mode == 1) slice_squares<T, 1>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      else slice_squares<T, 0>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      const T* S = sm.plane[s] + (slice + 1) * (PITCH * ROWS) + r0 * PITCH;  // slice z0 + slice, row y0 + r0 - 1
+      uint32_t Sq[RWW];
+      if (mode == 2) slice_squares<T, 2, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      else if (mode == 1) slice_squares<T, 1, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
+      else slice_squares<T, 0, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       const int par = gk & 1;
 #pragma unroll
-      for (int r = 0; r < RW; ++r) sm.xch[par][warp][r][lane] = Sq[r];
-      asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * 32) : "memory");
+      for (int r = 0; r < RWW; ++r) sm.xch[par][slice][r0 + r][lane] = Sq[r];
+      asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * SPLIT * 32) : "memory");
       if (!top) {
-        uint32_t K[RW];
+        uint32_t K[RWW];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) K[r] = Sq[r] & sm.xch[par][warp + 1][r][lane];  // z-pair
+        for (int r = 0; r < RWW; ++r) K[r] = Sq[r] & sm.xch[par][slice + 1][r0 + r][lane];  // z-pair
         auto survivors_of = [&](const uint32_t* Q) {
           uint32_t mask = 0;
 #pragma unroll
-          for (int r = 0; r < RW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
+          for (int r = 0; r < RWW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
           return mask;
         };
-        const bool inz = z0 + warp < nz;
+        const bool inz = z0 + slice < nz;
         const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
         if (inz) {
           if (m.k > 0) {
-            uint32_t Q[RW];
+            uint32_t Q[RWW];
 #pragma unroll
-            for (int r = 0; r < RW; ++r) Q[r] = prevK[r] & K[r];
-            enqueue(survivors_of(Q), (int)((uint32_t)(m.p - 1) | 0x80000000u), x0, y0, z0 + warp);
+            for (int r = 0; r < RWW; ++r) Q[r] = prevK[r] & K[r];
+            enqueue(survivors_of(Q), (int)((uint32_t)(m.p - 1) | 0x80000000u), x0, y0 + r0, z0 + slice);
           }
-          if (lastg) enqueue(survivors_of(K), m.p, x0, y0, z0 + warp);
+          if (lastg) enqueue(survivors_of(K), m.p, x0, y0 + r0, z0 + slice);
         }
 #pragma unroll
-        for (int r = 0; r < RW; ++r) prevK[r] = K[r];
+        for (int r = 0; r < RWW; ++r) prevK[r] = K[r];
       }
       ++gk;
     }
