@@ -722,9 +722,34 @@ struct ScanCtx {
   long long ny;
 };
 
+#ifndef FTK_GATHER_SR
+#define FTK_GATHER_SR 1
+#endif
+__device__ __forceinline__ uint32_t prmt_sr(uint32_t a, uint32_t b) {
+  // result bytes [sign(a) x 8, sign(b) x 8, sign(a) x 8, sign(b) x 8]: PRMT selector nibbles with the
+  // msb set replicate the sign bit of the selected byte (byte 3 of a = index 3, of b = index 7)
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, 0xFBFB;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t m) { return (a & ~m) | (b & m); }
+
 // gather the sign bits of the 4 conditions x 4 positions into the byte-top-nibble layout
+// (FTK_GATHER_SR: bits 3..0 repeat bit 4, so a byte is zero iff its four condition bits are, and no
+// byte lies in 0x01..0x0F -- the per-byte zero test stays exact)
 __device__ __forceinline__ uint32_t gather_code(const f2 (&c)[8]) {
   // c[2*j] = condition j for positions 0,1; c[2*j+1] = condition j for positions 2,3
+  if (FTK_GATHER_SR) {
+    // per condition: two sign-replicating PRMTs (positions 0, 1 and 2, 3) and two bit-selects
+    uint32_t acc = bitsel(prmt_sr(lo32(c[0]), hi32(c[0])), prmt_sr(lo32(c[1]), hi32(c[1])), 0xFFFF0000u);
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+      const uint32_t m = j < 3 ? (0x80808080u >> j) : 0x1F1F1F1Fu;
+      acc = bitsel(acc, prmt_sr(lo32(c[2 * j]), hi32(c[2 * j])), m & 0x0000FFFFu);
+      acc = bitsel(acc, prmt_sr(lo32(c[2 * j + 1]), hi32(c[2 * j + 1])), m & 0xFFFF0000u);
+    }
+    return acc;
+  }
   uint32_t w[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
