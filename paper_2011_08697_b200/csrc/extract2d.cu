@@ -708,7 +708,7 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
 // thr - dy, dy + thr (1 = that strict sign of the gradient component is established).  ANDing the
 // codes over a cube's corners leaves a bit set iff that component has that sign on every corner, so
 // the cubes to keep are the ones whose byte is ZERO after the AND (found with the exact zero-byte
-// test below: low nibbles are always zero).  Positions outside the grid get 0xF0 (AND-neutral).
+// test below: low nibbles repeat bit 4, so no byte lies in 1..15).  Positions outside the grid get 0xF0 (AND-neutral).
 // ---------------------------------------------------------------------------------------------
 struct ScanCtx {
   int srow0;       // smem row of the warp's first anchor row
@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
       if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       pf.lap(PF_SCAN);
       // survivors: zero bytes after the AND over the cube's corners (exact zero-byte test: the
-      // low nibbles are zero, so no borrow can flag a nonzero byte); bit 8i + r <-> position i,
+      // low nibbles repeat bit 4 or are zero, so no borrow can flag a nonzero byte); bit 8i + r <-> position i,
       // anchor row r
       auto survivors_of = [&](const uint32_t* K) {
         uint32_t mask = 0;

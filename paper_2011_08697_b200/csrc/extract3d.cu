@@ -338,7 +338,7 @@ __constant__ Cells4 cCells4 = make_cells4();
 // "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) in the top of a byte; ANDed over the
 // y-pair and x-pair in registers, over the z-pair through a double-buffered shared exchange (one
 // named barrier per plane), over the t-pair with the previous plane's cube codes in registers; a
-// zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte are zero).
+// zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte repeat bit 2, so no byte is 1..3).
 namespace s3 {
 constexpr int LX = 128, TX = LX, RW = 8, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
 constexpr int ROWS = RW + 3;  // y0-1 .. y0+RW+1
