@@ -348,6 +348,9 @@ template <typename T>
 constexpr int slices() { return nzw<T>() + 3; }         // z0-1 .. z0+NZW+1
 template <typename T>
 constexpr int nstage() { return sizeof(T) == 4 ? 3 : 2; }
+#ifndef FTK_S3_PAIRSYNC
+#define FTK_S3_PAIRSYNC 1  // neighbour-pair mbarriers instead of one named barrier per plane
+#endif
 #ifndef FTK_S3_SPLIT
 #define FTK_S3_SPLIT 1  // 2 (16 + 2 scan warps of 4 code rows) measured on C5: K1a 1.885 -> 1.872 ms, kept at 1
 #endif
@@ -370,6 +373,8 @@ struct alignas(128) Smem {
   static constexpr int NSTAGE = nstage<T>(), NZW = nzw<T>();
   T plane[NSTAGE][stage_elems<T>()];
   uint32_t xch[2][NZW + 1][RW][32];  // per plane parity: squares of every slice
+  uint64_t xfull[2][NZW + 1];         // FTK_S3_PAIRSYNC: slice w's squares of this parity are written
+  uint64_t xempty[2][NZW + 1];        // ... and were read by the warp of slice w - 1
   Meta meta[NSTAGE];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
@@ -642,6 +647,10 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], (NZW + 1) * SPLIT);
     }
+    for (int i = 0; i < 2 * (NZW + 1); ++i) {
+      mbar_init(&sm.xfull[0][0] + i, SPLIT * 32);  // every lane arrives (release of its own accesses)
+      mbar_init(&sm.xempty[0][0] + i, SPLIT * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -817,13 +826,21 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       const int par = gk & 1;
+      if (FTK_S3_PAIRSYNC && slice > 0 && gk >= 2)  // slice - 1's warp has read this buffer (plane gk - 2)
+        mbar_wait_sleep(&sm.xempty[par][slice], (uint32_t)(((gk >> 1) - 1) & 1), 5, gk);
 #pragma unroll
       for (int r = 0; r < RWW; ++r) sm.xch[par][slice][r0 + r][lane] = Sq[r];
-      asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * SPLIT * 32) : "memory");
+      if (FTK_S3_PAIRSYNC) {
+        mbar_arrive(&sm.xfull[par][slice]);
+      } else {
+        asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * SPLIT * 32) : "memory");
+      }
       if (!top) {
+        if (FTK_S3_PAIRSYNC) mbar_wait_sleep(&sm.xfull[par][slice + 1], (uint32_t)((gk >> 1) & 1), 6, gk);
         uint32_t K[RWW];
 #pragma unroll
         for (int r = 0; r < RWW; ++r) K[r] = Sq[r] & sm.xch[par][slice + 1][r0 + r][lane];  // z-pair
+        if (FTK_S3_PAIRSYNC) mbar_arrive(&sm.xempty[par][slice + 1]);
         auto survivors_of = [&](const uint32_t* Q) {
           uint32_t mask = 0;
 #pragma unroll

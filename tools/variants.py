@@ -17,6 +17,7 @@ VARIANTS = {
     "v3m3": ["FTK_V3_MINB=3"],
     "s3sp2": ["FTK_S3_SPLIT=2"],
     "gsr0": ["FTK_GATHER_SR=0"],
+    "pair0": ["FTK_S3_PAIRSYNC=0"],
     "x3m1": ["FTK_X3_MINB=1"],
     "x3m4": ["FTK_X3_MINB=4"],
     "x3m6": ["FTK_X3_MINB=6"],
