@@ -336,8 +336,9 @@ __constant__ Cells4 cCells4 = make_cells4();
 // z-slice z0 + w (8 rows, rolled through a 3-row register window as in 2D, plus the slices z +- 1 of
 // the centre row for dz); warp 8 computes the squares of slice z0 + 8 only.  Per vertex a 6-bit
 // "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) in the top of a byte; ANDed over the
-// y-pair and x-pair in registers, over the z-pair through a double-buffered shared exchange (one
-// named barrier per plane), over the t-pair with the previous plane's cube codes in registers; a
+// y-pair and x-pair in registers, over the z-pair through a double-buffered shared exchange (per
+// neighbour pair: slice w's warp waits only for slice w + 1's squares, xfull / xempty mbarriers), over
+// the t-pair with the previous plane's cube codes in registers; a
 // zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte repeat bit 2, so no byte is 1..3).
 namespace s3 {
 constexpr int LX = 128, TX = LX, RW = 8, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
