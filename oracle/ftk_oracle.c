@@ -34,8 +34,10 @@
  *
  * Parity-pin status: Kuhn tables, counts, SoS, face test,
  * 0/2 invariant, location (closed forms), woven census and labels are pinned by tests under
- * tests/test_oracle_*.py.  Hessian types near exact degeneracy are "parity unpinned" beyond the
- * closed-form and census pins.
+ * tests/test_oracle_*.py; tests/test_bruteforce_pin.py re-derives labels, locations and the 2D and
+ * 3D Hessian types (3D by Sylvester inertia of the exact rational Hessian) on tiny grids.  Hessian
+ * types within a relative 1e-9 of exact degeneracy are "parity unpinned" beyond the closed-form and
+ * census pins.
  */
 #include <math.h>
 #include <stdint.h>

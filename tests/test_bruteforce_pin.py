@@ -12,7 +12,9 @@ follows the definitions rather than the oracle's algorithm:
 * cells are the full-span chains; each must hold 0 or 2 punctured faces, pairs are
   joined, labels are the minimum face id of a component (DESIGN.md R13);
 * locations are Eq. 2 in exact rationals; 2D types come from the exact sign of the
-  determinant of the mu-interpolated Hessian (R8/R9), compared where it is not a near tie.
+  determinant of the mu-interpolated Hessian (DESIGN.md R8/R9), compared where it is not a near tie;
+  3D types count the negative eigenvalues of the exact rational Hessian by Jacobi's rule on its
+  leading principal minors (Sylvester's law of inertia), not by the oracle's Descartes count.
 """
 import itertools
 from fractions import Fraction
@@ -63,6 +65,12 @@ EPS = Fraction(1, 2 ** 160)
 
 def sos_sign(rows):
     n = len(rows)
+    d0 = det([list(r) for r in rows])
+    if d0 != 0:
+        # integer rows: |det(M)| >= 1, while every epsilon term of det(M + E) is below 2^-60 here
+        # (entries < 2^40, epsilon <= 2^-160), so the unperturbed sign is the SoS sign
+        assert max(abs(x) for r in rows for x in r) < 2 ** 40
+        return 1 if d0 > 0 else -1
     M = [[Fraction(rows[r][j]) + EPS ** (2 ** (n * r + j)) for j in range(n)] for r in range(n)]
     d = det(M)
     assert d != 0
@@ -165,8 +173,55 @@ def brute_track(field, s):
             scale = a * a + b * b + dd * dd
             if dt != 0 and abs(dt) > Fraction(1, 10 ** 9) * scale:
                 typ = 2 if dt < 0 else (1 if a > 0 else 5)
+        else:
+            typ = type3d(q, dims, verts, mu)
         out[fid] = (find(fid), loc, typ, S == 0)
     return out, bad
+
+
+def hessian3d(q, dims, v):
+    """integer Hessian at v (R8): 4 x the compact second difference on the diagonal, the
+    4-point cross difference off it, stencil centre clamped into [1, N-2] per differentiated axis"""
+    H = [[0] * 3 for _ in range(3)]
+    for a in range(3):
+        for b in range(a, 3):
+            c = list(v)
+            c[a] = min(max(c[a], 1), dims[a] - 2)
+            c[b] = min(max(c[b], 1), dims[b] - 2)
+
+            def at(da, db):
+                w = list(c)
+                w[a] += da
+                w[b] += db
+                return q[tuple(w)]
+            if a == b:
+                w = list(c); w[a] += 1; p = q[tuple(w)]
+                w[a] -= 2; m = q[tuple(w)]
+                H[a][a] = 4 * (p - 2 * q[tuple(c)] + m)
+            else:
+                H[a][b] = H[b][a] = at(1, 1) - at(1, -1) - at(-1, 1) + at(-1, -1)
+    return H
+
+
+def type3d(q, dims, verts, mu):
+    """3D type from the inertia of H_bar = sum mu_k H_k (R9): by Sylvester's law of
+    inertia the number of negative eigenvalues is the number of sign changes in (1, D1, D2, D3) of
+    the leading principal minors, under any symmetric axis permutation with D1, D2 != 0.  None for a
+    near-singular H_bar (the oracle decides those in FP64) or when no permutation has nonzero minors."""
+    Hs = [hessian3d(q, dims, v) for v in verts]
+    Hb = [[sum(mu[k] * Hs[k][i][j] for k in range(4)) for j in range(3)] for i in range(3)]
+    D3 = det(Hb)
+    scale = max(abs(x) for r in Hb for x in r)
+    if D3 == 0 or abs(D3) <= Fraction(1, 10 ** 9) * scale ** 3:
+        return None
+    for perm in itertools.permutations(range(3)):
+        P = [[Hb[perm[i]][perm[j]] for j in range(3)] for i in range(3)]
+        D1, D2 = P[0][0], P[0][0] * P[1][1] - P[0][1] * P[1][0]
+        if D1 != 0 and D2 != 0:
+            seq = [1, D1, D2, D3]
+            neg = sum((seq[i] > 0) != (seq[i + 1] > 0) for i in range(3))
+            return {0: 1, 1: 3, 2: 4, 3: 5}[neg]  # MIN, SADDLE1, SADDLE2, MAX (oracle enum)
+    return None
 
 
 def check(oracle_lib, field, s):
@@ -212,3 +267,12 @@ def test_bruteforce_3d_degenerate(oracle_lib):
     f = fi.random_degenerate((2, 3, 3, 3), seed=5).numpy()
     n, _ = check(oracle_lib, f, 0)
     assert n > 0
+
+
+@pytest.mark.parametrize("nz,L,sigma", [(4, 4.0, 0.0), (5, 5.0, 0.05)])
+def test_bruteforce_3d_woven(oracle_lib, nz, L, sigma):
+    """3D woven windows (generic values, s = 26): labels, locations and the 3D Hessian types
+    (22 / 26 punctured faces, SADDLE1, SADDLE2 and MAX all present, every type decided)"""
+    f = fi.Woven(6, 6, 2, nz=nz, L=L, sigma=sigma).generate().numpy()
+    n, nt = check(oracle_lib, f, 26)
+    assert n > 0 and nt == n
