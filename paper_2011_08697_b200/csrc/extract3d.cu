@@ -353,7 +353,7 @@ constexpr int nstage() { return sizeof(T) == 4 ? 3 : 2; }
 #define FTK_S3_PAIRSYNC 1  // neighbour-pair mbarriers instead of one named barrier per plane
 #endif
 #ifndef FTK_S3_SPLIT
-#define FTK_S3_SPLIT 1  // 2 (16 + 2 scan warps of 4 code rows) measured on C5: K1a 1.885 -> 1.872 ms, kept at 1
+#define FTK_S3_SPLIT 1  // 2 (16 + 2 scan warps of 4 code rows) on C5: K1a 1.885 -> 1.872 ms with the named barrier, 1.737 -> 1.759 ms with pair sync; kept at 1
 #endif
 constexpr int SPLIT = FTK_S3_SPLIT;  // warps per z-slice (each owns RW / SPLIT code-row pairs)
 constexpr int RWW = RW / SPLIT;
