@@ -167,6 +167,20 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   }
 }
 
+#ifndef FTK_LABEL_JUMP
+#define FTK_LABEL_JUMP 0  // pointer-jumping passes over all records before K6; measured (r1f, tools/gpu_check3.sh):
+                          // 2 passes C2 pass 2 0.20 -> 0.20 ms, C4 5.63 -> 6.32, C5 0.131 -> 0.116; kept at 0
+#endif
+__global__ void k_jump(const __grid_constant__ TrackParams P) {
+  const i64 n = n_records(P);
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const int p = P.parent[i];
+    if (p == (int)i) continue;
+    const int gp = P.parent[p];
+    if (gp != p) P.parent[i] = gp;  // benign race, as in path halving
+  }
+}
+
 __global__ void k_label(const __grid_constant__ TrackParams P) {
   const i64 n = n_records(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
@@ -723,6 +737,7 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
   }
   k_edges<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
+  for (int j = 0; j < FTK_LABEL_JUMP; ++j) k_jump<<<blocks, threads, 0, stream>>>(P);
   k_label<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.verify) {

@@ -23,6 +23,8 @@ VARIANTS = {
     "x3m6": ["FTK_X3_MINB=6"],
     "x3m8": ["FTK_X3_MINB=8"],
     "vminb8": ["FTK_V_MINB=8"],
+    "jump2": ["FTK_LABEL_JUMP=2"],
+    "jump4": ["FTK_LABEL_JUMP=4"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
