@@ -62,7 +62,12 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// never hang the GPU: a wait that exceeds 2 s reports where it is stuck and traps
+// Watchdog: a wait longer than FTK_WAIT_WATCHDOG_NS of wall-clock (%globaltimer) reports where it is
+// stuck and traps instead of hanging the GPU.  The default (60 s) is far beyond any valid wait, also
+// under compute-sanitizer or time-slicing; build with -DFTK_WAIT_WATCHDOG_NS=0 to compile it out.
+#ifndef FTK_WAIT_WATCHDOG_NS
+#define FTK_WAIT_WATCHDOG_NS 60000000000ull
+#endif
 static __device__ __noinline__ void wait_timeout(int what, int a, int b) {
   if ((threadIdx.x & 31) == 0)
     printf("ftk k_extract2d: wait timeout what=%d a=%d b=%d block=%d warp=%d\n", what, a, b, blockIdx.x,
@@ -76,8 +81,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int wh
   int spins = 0;
   while (!mbar_try(bar, parity)) {
     __nanosleep(sleep_ns);
-    if ((++spins & 15) == 0) {
-      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
+    if (FTK_WAIT_WATCHDOG_NS && (++spins & 15) == 0) {
+      if (gtimer_ns() - t0 > FTK_WAIT_WATCHDOG_NS) wait_timeout(what, a, (int)parity);
     }
   }
 }
@@ -94,8 +99,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
         : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
         : "memory");
     if (done) return;
-    if ((++spins & 15) == 0) {
-      if (gtimer_ns() - t0 > 2000000000ull) wait_timeout(what, a, (int)parity);
+    if (FTK_WAIT_WATCHDOG_NS && (++spins & 15) == 0) {
+      if (gtimer_ns() - t0 > FTK_WAIT_WATCHDOG_NS) wait_timeout(what, a, (int)parity);
     }
   }
 }
