@@ -280,11 +280,12 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     value = total_faces / (ms_step / 1000.0)
 
-    # roofline of the extraction kernel north_star names, the scan kernel K1a:
-    # algorithmic bytes = the field read once + the survivors handed on (12 B per surviving cube);
-    # the exact kernel K1b (2D: with k_expand2d) is reported beside it -- window reads of the
-    # survivors + records -- with both kernels' shares of the step, since on C2 K1b takes the larger
-    # share (it is latency-bound)
+    # roofline of the extraction pass north_star names: algorithmic bytes = the field
+    # read once + 56 B per punctured face written (halo re-reads, ghost planes and workspace traffic --
+    # the survivor windows K1a hands to K1b, face ids, union-find parents, edges -- are not
+    # algorithmic); time = the whole pass, K1a scan + K1b exact (+ k_expand2d on the 2D vector path),
+    # from CUDA events the library records on the launch stream; K1a and K1b are broken out beside it
+    # with their own ncu dram traffic, and the whole step's fraction on the same bytes
     esz = field.element_size()
     k1_avg = sum(k1_ms) / len(k1_ms)
     ka_avg = sum(ka_ms) / len(ka_ms)
@@ -292,16 +293,17 @@ def run_ours(args):
     _, st3 = ftk.last_timings()
     n_surv = st3[1]
     d3 = len(spatial) == 3
-    alg_bytes = field.numel() * esz + (16 if d3 else 12) * n_surv
-    achieved = alg_bytes / (ka_avg / 1000.0) / 1e9
+    field_bytes = field.numel() * esz
+    rec_bytes = n_punct * ftk.RECORD_BYTES
+    alg_bytes = field_bytes + rec_bytes
+    achieved = alg_bytes / (k1_avg / 1000.0) / 1e9
     peak, peak_src = _peaks()
     if d3:
         kscan, kexact = ("k_scanvec3d", "k_exact3d") if vec else ("k_scan3d", "k_exact3d")
     else:
         kscan, kexact = ("k_scanvec2d", "k_exactvec2d") if vec else ("k_scan2d", "k_exact2d")
-    # the exact kernel's window per survivor: 4x4[x4]x2 values (scalar), the corner vectors (vector)
-    win_bytes = ((48 if vec else 256) if d3 else (16 if vec else 32)) * esz
-    traffic = _ncu_traffic(cfg.name, kscan)
+    t_scan, t_exact = _ncu_traffic(cfg.name, kscan), _ncu_traffic(cfg.name, kexact)
+    traffic = t_scan + t_exact if t_scan is not None and t_exact is not None else None
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
     e2e = None
@@ -422,20 +424,25 @@ def run_ours(args):
                    **({"stitch_ms": sum(st_ms) / len(st_ms)} if world > 1 else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": f"{kscan} (K1a, prefilter scan)", "alg_bytes_per_launch": alg_bytes,
-                     "share_of_step": ka_avg / ms_step,
-                     kexact: {"ms": kb_avg, "share_of_step": kb_avg / ms_step,
-                              "alg_bytes_per_launch": win_bytes * n_surv + n_punct * ftk.RECORD_BYTES,
-                              "achieved_gbs": (win_bytes * n_surv + n_punct * ftk.RECORD_BYTES) / (kb_avg / 1000.0) / 1e9,
-                              "traffic": _ncu_traffic(cfg.name, kexact)}},
+                     "kernel": f"extraction pass: {kscan} (K1a scan) + {kexact} (K1b exact)",
+                     "alg_bytes_per_launch": alg_bytes,
+                     "alg_bytes": "SURVEY.md 8(d): field read once (%d B) + 56 B x %d punctured faces" % (
+                         field_bytes, n_punct),
+                     "ms": k1_avg, "share_of_step": k1_avg / ms_step,
+                     "step_frac": alg_bytes / (ms_step / 1000.0) / 1e9 / peak,
+                     kscan: {"ms": ka_avg, "share_of_step": ka_avg / ms_step, "alg_bytes": field_bytes,
+                             "frac": field_bytes / (ka_avg / 1000.0) / 1e9 / peak, "traffic": t_scan},
+                     kexact: {"ms": kb_avg, "share_of_step": kb_avg / ms_step, "alg_bytes": rec_bytes,
+                              "frac": rec_bytes / (kb_avg / 1000.0) / 1e9 / peak if kb_avg > 0 else None,
+                              "traffic": t_exact}},
         "clocks": clk.summary(),
         "e2e": e2e,
         "stream": stream_line,
         "post": post_line,
         "iso": iso_line,
-        # K1a (+ k_expand2d in 2D) + K1b + k_clear + k_hash_insert + k_edges + k_label; time slabs add
-        # k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
-        "gpu_launches": ((6 if d3 else 7) + (6 if world > 1 else 0)) * args.steps,
+        # K1a + K1b (+ k_expand2d on the 2D vector path) + k_clear + k_hash_insert + k_edges + k_label;
+        # time slabs add k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
+        "gpu_launches": ((7 if vec and not d3 else 6) + (6 if world > 1 else 0)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)

@@ -77,7 +77,8 @@ typedef enum {
 /* ftk_desc.flags */
 #define FTK_GHOST_PLANE 1u      /* the buffer's last plane is a read-only ghost (time slab):
                                    faces anchored on it are tested for linking but not returned */
-#define FTK_SORTED 2u           /* return records sorted by face_id */
+#define FTK_SORTED 2u           /* return records sorted by face_id (a device radix sort after pass 2
+                                   and the stitch; without it the order of records is unspecified) */
 #define FTK_VECTOR_FIELD 4u     /* the field is a VECTOR field: ndim components per vertex,
                                    interleaved, layout [t][y][x][2] (2D) or [t][z][y][x][3] (3D); its
                                    own zeros are tracked (no gradient step) and typed from its Jacobian */
@@ -95,7 +96,7 @@ typedef struct {
   int64_t t0;          /* global timestep of the buffer's first plane (0 on a single GPU) */
   int64_t nt_global;   /* global number of timesteps; t0 + nt <= nt_global */
   int32_t scale_log2;  /* fixed point: q = rint(f * 2^scale_log2), round-half-even; [-64, 64] */
-  uint32_t flags;      /* FTK_GHOST_PLANE | FTK_SORTED */
+  uint32_t flags;      /* FTK_GHOST_PLANE | FTK_SORTED | FTK_VECTOR_FIELD */
 } ftk_desc;
 
 /* One punctured face (56 bytes). */
@@ -121,13 +122,12 @@ FTK_API const char* ftk_last_error(void);
 FTK_API int ftk_num_faces(const ftk_desc* desc, int64_t* n_faces);
 
 /* Device workspace needed by extract/track for up to `capacity` records (0 <= capacity < 2^31 - 1,
- * else FTK_ERR_INVALID_ARG).  It includes (2D) a
- * list of max(1024, capacity) prefilter-surviving cubes, handed from the scan kernel to the exact
- * kernel. */
+ * else FTK_ERR_INVALID_ARG).  It includes a list of max(1024, capacity) prefilter-surviving cubes,
+ * handed from the scan kernel to the exact kernel. */
 FTK_API int ftk_workspace_size(const ftk_desc* desc, int64_t capacity, size_t* bytes);
 
 /* Pass 1: test every owned face, write the punctured ones to d_out[0 .. *n_out)
- * (label = -1).  d_field: device pointer to the buffer; d_out: device array of `capacity`
+ * (label = -1; in face-id order with FTK_SORTED).  d_field: device pointer to the buffer; d_out: device array of `capacity`
  * records; d_ws: device workspace of ws_bytes >= ftk_workspace_size(). */
 FTK_API int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
                    int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream);
@@ -139,6 +139,12 @@ FTK_API int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_
  * are global (identical to a single-GPU run).  comm = NULL: single GPU. */
 FTK_API int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity,
                  int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream, ftk_comm* comm);
+/* With a communicator every rank must call ftk_cp_track the same number of times: each call ends in
+ * one exchange of seam blocks (NCCL allgather over NVLink) that every rank enters even when its own
+ * slab failed, carrying the failure code, so that ALL ranks return the same status (any error other
+ * than FTK_ERR_CAPACITY outranks a capacity shortfall; with FTK_ERR_CAPACITY every rank retries with
+ * its *n_out).  The exchange uses only the communicator's pre-sized blocks (no allocation); a seam list
+ * longer than the blocks takes a host path once, which re-sizes them. */
 
 /* End-to-end variant from HOST memory: h_field is a host buffer (pinned for full PCIe speed) of the
  * whole input; the library copies it to d_stage (device buffer of the field's size) on `stream`,
@@ -181,7 +187,8 @@ FTK_API int ftk_relabel(ftk_cp* d_out, int64_t n, const int64_t* h_map_old, cons
 
 /* Device seam path (used by ftk_cp_track with a communicator; exposed for tests and custom
  * transports).  A packed seam block holds one slab's lists:
- *   [0] nA, [1] nB, [2, 2 + 2 cap) A pairs, [2 + 2 cap, 2 + 4 cap) B pairs   (int64, 2 + 4 cap total).
+ *   [0] nA, [1] nB, [2, 2 + 2 cap) A pairs, [2 + 2 cap, 2 + 4 cap) B pairs   (int64, 2 + 4 cap total);
+ * a slab whose track failed publishes [0] = -code instead (no pairs).
  * ftk_seam_pack writes this slab's block (from the workspace of its last track call) to d_block
  * (device).  ftk_seam_resolve takes the world blocks concatenated in slab order (device, e.g. an
  * allgather), unions every A pair's label with the B label of the same face on the device and
@@ -274,7 +281,21 @@ FTK_API int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_f
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */
 FTK_API int ftk_comm_get_unique_id(uint8_t id[128]);
 FTK_API int ftk_comm_init(ftk_comm** comm, int rank, int world, const uint8_t id[128]);
+/* init allocates the seam blocks and resolve tables for 2^17 pairs per list and slab (every rank:
+ * world blocks of 2 + 4 * 2^17 int64 plus hash tables); reserve grows them for larger seams, outside
+ * the hot path (the same value on every rank).  Call both on the device the rank's track calls use. */
+FTK_API int ftk_comm_reserve(ftk_comm* comm, int64_t seam_pairs);
 FTK_API int ftk_comm_destroy(ftk_comm* comm);
+
+/* Testing switches of the calling thread (off by default; they never change results, only the
+ * path taken): FTK_DEBUG_FORCE_GENERIC stages the 2D planes with the generic loader instead of TMA,
+ * FTK_DEBUG_VERIFY_LINK re-derives every punctured face's parent cells in closed form after pass 2
+ * (side_of; a cell without exactly one partner counts as FTK_ERR_INVARIANT), FTK_DEBUG_STITCH_HOST
+ * resolves time-slab seams through the host path.  FTK_ERR_INVALID_ARG for unknown bits. */
+#define FTK_DEBUG_FORCE_GENERIC 1u
+#define FTK_DEBUG_VERIFY_LINK 2u
+#define FTK_DEBUG_STITCH_HOST 4u
+FTK_API int ftk_set_debug(uint32_t flags);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ OK, ERR_INVALID_ARG, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_INVARIANT,
 F32, F64 = 0, 1
 DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX, SOURCE, SINK, CENTER = range(9)
 GHOST_PLANE, SORTED, VECTOR_FIELD = 1, 2, 4
+DEBUG_FORCE_GENERIC, DEBUG_VERIFY_LINK, DEBUG_STITCH_HOST = 1, 2, 4
 CP_ORDINAL, CP_BOUNDARY, CP_DEGENERATE_LOC = 1, 2, 4
 
 RECORD_DTYPE = np.dtype(
@@ -38,7 +39,8 @@ EXPORTS = [
     "ftk_abi_version", "ftk_strerror", "ftk_last_error", "ftk_num_faces", "ftk_workspace_size",
     "ftk_cp_extract", "ftk_cp_track", "ftk_cp_track_host", "ftk_set_profiling", "ftk_last_timings",
     "ftk_last_kernel_timings",
-    "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_destroy", "ftk_stitch_export", "ftk_stitch_resolve",
+    "ftk_comm_get_unique_id", "ftk_comm_init", "ftk_comm_reserve", "ftk_comm_destroy", "ftk_stitch_export",
+    "ftk_stitch_resolve", "ftk_set_debug",
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
     "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
     "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types", "ftk_iso_track",
@@ -90,6 +92,8 @@ def lib() -> ctypes.CDLL:
         L.ftk_seam_resolve.argtypes = [P, ctypes.c_int, ctypes.c_int64, P, ctypes.c_int64, P]
         L.ftk_comm_get_unique_id.argtypes = [P]
         L.ftk_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+        L.ftk_comm_reserve.argtypes = [P, I64]
+        L.ftk_set_debug.argtypes = [ctypes.c_uint32]
         L.ftk_comm_destroy.argtypes = [P]
         L.ftk_stitch_export.argtypes = [PD, P, ctypes.c_size_t, I64, P, I64, P, P, I64, P, P]
         L.ftk_stitch_resolve.argtypes = [P, I64, P, I64, P, I64, P, P, P]
@@ -245,19 +249,23 @@ def iso_track(field: torch.Tensor, scale_log2: int, isovalue: float, capacity: i
 
 def extract(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
             capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
-            return_buffers: bool = False, vector: bool = False):
+            return_buffers: bool = False, vector: bool = False, sorted_output: bool = False):
     """Pass 1: punctured faces of the buffer's owned timesteps (label = -1).
-    Returns an int64 [n, 7] device tensor of 56-byte records (see RECORD_DTYPE)."""
-    rec, buf = _run("ftk_cp_extract", field, scale_log2, t0, nt_global, capacity, ghost, buffers, vector=vector)
+    Returns an int64 [n, 7] device tensor of 56-byte records (see RECORD_DTYPE); in face-id order with
+    sorted_output=True (FTK_SORTED), else in an unspecified order."""
+    rec, buf = _run("ftk_cp_extract", field, scale_log2, t0, nt_global, capacity, ghost, buffers, vector=vector,
+                    sorted_output=sorted_output)
     return (rec, buf) if return_buffers else rec
 
 
 def track(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,
           capacity: int | None = None, ghost: bool = False, buffers: Buffers | None = None,
-          comm=None, return_buffers: bool = False, vector: bool = False):
+          comm=None, return_buffers: bool = False, vector: bool = False, sorted_output: bool = False):
     """Pass 1 + pass 2: punctured faces labelled with their trajectory (min face_id).  vector=True:
-    field is a 2D vector field [t][y][x][2] whose own zeros are tracked."""
-    rec, buf = _run("ftk_cp_track", field, scale_log2, t0, nt_global, capacity, ghost, buffers, comm, vector=vector)
+    field is a vector field [t][y][x][2] / [t][z][y][x][3] whose own zeros are tracked.
+    sorted_output=True: records in face-id order (FTK_SORTED)."""
+    rec, buf = _run("ftk_cp_track", field, scale_log2, t0, nt_global, capacity, ghost, buffers, comm, vector=vector,
+                    sorted_output=sorted_output)
     return (rec, buf) if return_buffers else rec
 
 
@@ -300,10 +308,12 @@ class Tracker:
         self._h = ctypes.c_void_p(0)
         self._keep = collections.deque()  # (host plane, event after its copy): copies may be in flight
         self._window = window
+        # every copy and kernel of the stream runs on the stream current at construction
+        self.stream = torch.cuda.current_stream(self.device)
         _check(lib().ftk_tracker_begin(ctypes.byref(self._h), ctypes.byref(self.desc), window,
                                        ctypes.c_void_p(self.records.data_ptr()), self.capacity,
                                        ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
-                                       ctypes.c_void_p(_stream_ptr(self.device))), "ftk_tracker_begin")
+                                       ctypes.c_void_p(self.stream.cuda_stream)), "ftk_tracker_begin")
 
     @staticmethod
     def workspace_bytes(spatial_shape, dtype, scale_log2: int, capacity: int, window: int,
@@ -320,10 +330,17 @@ class Tracker:
         if tuple(plane.shape) != self.spatial_shape or plane.dtype != self.dtype:
             raise FtkError(ERR_INVALID_ARG, f"Tracker.push: plane must be {self.spatial_shape} {self.dtype}")
         plane = plane.contiguous()
+        # the plane may have been produced on another stream: order the tracker's copy after it, and
+        # keep the caching allocator from reusing a device plane before the copy has run
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+        if plane.is_cuda:
+            plane.record_stream(self.stream)
         _check(lib().ftk_tracker_push(self._h, ctypes.c_void_p(plane.data_ptr())), "ftk_tracker_push")
         if not plane.is_cuda:  # keep the host buffer alive until its asynchronous copy has run
             ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(self.device))
+            ev.record(self.stream)
             self._keep.append((plane, ev))
             while len(self._keep) > 2 * self._window + 2:
                 self._keep.popleft()[1].synchronize()
@@ -397,6 +414,12 @@ def to_numpy(rec: torch.Tensor) -> np.ndarray:
 
 def set_profiling(enable: bool):
     lib().ftk_set_profiling(1 if enable else 0)
+
+
+def set_debug(flags: int):
+    """Testing switches of the calling thread (DEBUG_FORCE_GENERIC | DEBUG_VERIFY_LINK |
+    DEBUG_STITCH_HOST; include/ftk_cp.h ftk_set_debug): they change the path taken, never the result."""
+    _check(lib().ftk_set_debug(int(flags)), "ftk_set_debug")
 
 
 def last_kernel_timings():
@@ -495,6 +518,10 @@ class Comm:
         self.ptr = ctypes.c_void_p()
         _check(lib().ftk_comm_init(ctypes.byref(self.ptr), rank, world, uid), "ftk_comm_init")
         self.rank, self.world = rank, world
+
+    def reserve(self, seam_pairs: int):
+        """grow the pre-sized seam blocks (same value on every rank; outside the hot path)"""
+        _check(lib().ftk_comm_reserve(self.ptr, int(seam_pairs)), "ftk_comm_reserve")
 
     def close(self):
         if self.ptr:

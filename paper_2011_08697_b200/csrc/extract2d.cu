@@ -125,12 +125,18 @@ struct BatchBuf {                   // one warp's batch in shared memory
   int* qy;
   int* qt;                          // t | (t+1 exists) << 31 | fast << 30, -1: no cube
   uint16_t* items;                  // punctured faces of the batch: entry | type << 5
+  unsigned long long* lp;           // [32] in-cube union-find of each entry (12 x 4-bit parents)
+  uint32_t* pm;                     // [32] punctured own faces of each entry
+  int* rs;                          // [32] first record of each entry, relative to the batch
 };
 
 template <typename T>
 struct ExSmem {
   uint32_t ring[EXW * 32 * ws_words<T>()];
   int qx[EXW * 32], qy[EXW * 32], qt[EXW * 32];
+  unsigned long long lp[EXW * 32];
+  uint32_t pm[EXW * 32];
+  int rs[EXW * 32];
   uint16_t items[EXW][MAXITEMS];
 };
 
@@ -143,23 +149,11 @@ __device__ __forceinline__ i64 quant(float f, float scale_f, double) {
 }
 __device__ __forceinline__ i64 quant(double f, float, double scale) { return __double2ll_rn(__dmul_rn(f, scale)); }
 
-// pass-2 bookkeeping of a new record (2D track): compact face id, union-find root, hash insert
-// (face ids are unique: the first empty slot of the probe sequence is claimed)
-__device__ __forceinline__ void register_record(const ExtractParams& P, unsigned long long slot, long long fid,
-                                                unsigned long long hm) {
-  P.fid[slot] = fid;
-  if (P.table) {
-    u64 h = hash_mix((u64)fid) & hm;
-    while (atomicCAS(&P.table[h], -1, (int)slot) != -1) h = (h + 1) & hm;
-  }
-}
-
 struct Geo {
   i64 nx, ny, ntg;   // grid extents (t = global)
   float scale_f;
   double scale;
   double qmax;       // |f| below this quantizes to |q| < 2^29 (int32 fast path)
-  unsigned long long hm;  // pass-2 hash-table slot mask (2D track)
 };
 
 template <typename T>
@@ -471,7 +465,7 @@ __device__ __noinline__ void emit_record_general(const Win<T>& w, const Geo& G, 
   if (slot < (unsigned long long)P.capacity) {
     ftk_cp* r = P.out + slot;
     r->face_id = ((t * G.ny + y) * G.nx + x) * 12 + ty;
-    register_record(P, slot, r->face_id, G.hm);
+    P.fid[slot] = r->face_id;  // compact face ids for pass 2
     r->label = -1;
     r->x = lx;
     r->y = ly;
@@ -482,12 +476,12 @@ __device__ __noinline__ void emit_record_general(const Win<T>& w, const Geo& G, 
   }
 }
 
-__device__ __forceinline__ void store_record(const ExtractParams& P, unsigned long long hm, unsigned long long slot,
-                                             long long fid, double lx, double ly, double lt, int type, uint32_t flags) {
+__device__ __forceinline__ void store_record(const ExtractParams& P, unsigned long long slot, long long fid, double lx,
+                                             double ly, double lt, int type, uint32_t flags) {
   if (slot < (unsigned long long)P.capacity) {
     ftk_cp* r = P.out + slot;
     r->face_id = fid;
-    register_record(P, slot, fid, hm);
+    P.fid[slot] = fid;  // compact face ids for pass 2
     r->label = -1;
     r->x = lx;
     r->y = ly;
@@ -561,20 +555,30 @@ __device__ __forceinline__ void emit_record(const Win<T>& w, const Geo& G, const
     const int c = 7 & ~span;
     if (c == 4 && (t == 0 || t == G.ntg - 1)) flags |= FTK_CP_BOUNDARY;
   }
-  store_record(P, G.hm, slot, ((t * G.ny + y) * G.nx + x) * 12 + ty, lx, ly, lt, type, flags);
+  store_record(P, slot, ((t * G.ny + y) * G.nx + x) * 12 + ty, lx, ly, lt, type, flags);
 }
 
-// One batch of 32 entries (one cube per lane): face tests, then the punctured faces spread over the
-// lanes for the record stage.
+// in-cube union-find over the 12 face types: 4-bit parent fields, the root is the smallest type of
+// its component (= the smallest face id)
+__device__ __forceinline__ int lfind(unsigned long long lp, int ty) {
+  int p = (int)((lp >> (4 * ty)) & 15);
+  while (p != ty) {
+    ty = p;
+    p = (int)((lp >> (4 * ty)) & 15);
+  }
+  return ty;
+}
+
+// One batch of 32 entries (one cube per lane): face tests, the 6 cells of every cube, slot
+// reservation, then the punctured faces spread over the lanes for the record stage.
 template <typename T>
 __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractParams& P, Prof& pf) {
   const int lane = threadIdx.x & 31;
-  const int e = lane;
-  const int qtv = bb.qt[e];
+  const int qtv = bb.qt[lane];
   const bool valid = qtv != -1;
-  const i64 x = bb.qx[e], y = bb.qy[e], t = qtv & 0x3fffffff;
+  const i64 x = bb.qx[lane], y = bb.qy[lane], t = qtv & 0x3fffffff;
   const bool hasB = (qtv >> 31) & 1;
-  const uint32_t* E = bb.ring + e * ws_words<T>();
+  const uint32_t* E = bb.ring + lane * ws_words<T>();
   const bool isq = (qtv >> 30) & 1;
   uint32_t m = 0;
   if (valid) {
@@ -584,100 +588,69 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
   pf.lap(PF_EXFACE);
   // pass 2 for the 6 cells anchored at this cube: every cell lies inside one
   // cube, so its 4 faces are tested right here; a cell holds 0 or 2 punctured faces under SoS
-  // (PAPER.md:437, 467).  A pair becomes an edge of the trajectory graph: (own record, own record)
-  // or (own record, -1 - face id of the upper face owned by the neighbour cube).
+  // (PAPER.md:437, 467).  Two own faces are joined in the cube's union-find (opm: such cells); a pair
+  // with the upper face (owned by the neighbour cube) becomes a trajectory-graph edge (edm).
   const bool full = valid && x + 1 < G.nx && y + 1 < G.ny && hasB;
-  uint32_t epair[6];  // per cell: 4-bit set of punctured faces (bit 0..2 own ta, tb, tc; bit 3 upper)
-  int ecnt = 0, bad = 0;
+  uint32_t opm = 0, edm = 0;
+  int bad = 0;
 #define FTK_CELLCNT(C)                                                                                   \
   {                                                                                                      \
     constexpr CellDef d = Cell3<C>::d;                                                                   \
     const uint32_t bits = ((pmask >> d.ta) & 1u) | (((pmask >> d.tb) & 1u) << 1) |                        \
                           (((pmask >> d.tc) & 1u) << 2) | (((umask >> C) & 1u) << 3);                     \
     const int k = __popc(bits);                                                                          \
-    epair[C] = (full && k == 2) ? bits : 0u;                                                             \
-    ecnt += (full && k == 2 && (bits & 8u)) ? 1 : 0;                                                     \
-    bad += (full && k != 0 && k != 2) ? 1 : 0;                                                           \
+    if (k == 2) (bits & 8u ? edm : opm) |= 1u << C;                                                      \
+    bad += (k != 0 && k != 2) ? 1 : 0;                                                                   \
   }
-  FTK_CELLCNT(0) FTK_CELLCNT(1) FTK_CELLCNT(2) FTK_CELLCNT(3) FTK_CELLCNT(4) FTK_CELLCNT(5)
+  if (full) {
+    FTK_CELLCNT(0) FTK_CELLCNT(1) FTK_CELLCNT(2) FTK_CELLCNT(3) FTK_CELLCNT(4) FTK_CELLCNT(5)
+  }
 #undef FTK_CELLCNT
-  // Pairs of two own faces are joined right here: a union-find over the cube's 12 face types
-  // (4-bit parent fields; the root is the smallest type = the smallest face id), written into the
-  // global parent array once the records have slots.  Only pairs with the upper face (owned by a
-  // neighbour cube) become trajectory-graph edges for pass 2.
-  unsigned long long lp = 0xBA9876543210ull;
-  auto lfind = [&](int ty) {
-    int p = (int)((lp >> (4 * ty)) & 15);
-    while (p != ty) {
-      ty = p;
-      p = (int)((lp >> (4 * ty)) & 15);
-    }
-    return ty;
-  };
-#pragma unroll 1
-  for (int C = 0; C < 6; ++C) {
-    const uint32_t bits = epair[C];
-    if (bits && !(bits & 8u)) {
-      const int cd = cCell[C];
-      const int t1 = (bits & 1u) ? (cd & 15) : ((cd >> 4) & 15);
-      const int t2 = (bits & 4u) ? ((cd >> 8) & 15) : ((cd >> 4) & 15);
-      const int r1 = lfind(t1), r2 = lfind(t2);
-      const int lo = min(r1, r2), hi = max(r1, r2);
-      lp = (lp & ~(15ull << (4 * hi))) | ((unsigned long long)lo << (4 * hi));
-    }
-  }
   if (bad) atomicAdd(&P.counters[CNT_INVARIANT], (unsigned long long)bad);
-  // spread the punctured faces over the lanes; reserve record and edge slots
-  const int cnt = __popc(pmask);
-  int incl = cnt, eincl = ecnt;
+  // record and edge slots: one warp scan of both counts (<= 12 and <= 6 per lane), one atomic each
+  const int cnt = __popc(pmask), ecnt = __popc(edm);
+  int incl = cnt | (ecnt << 16);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    const int ve = __shfl_up_sync(0xffffffffu, eincl, o);
-    if (lane >= o) {
-      incl += v;
-      eincl += ve;
-    }
+    if (lane >= o) incl += v;
   }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  const int etotal = __shfl_sync(0xffffffffu, eincl, 31);
+  const int tot = __shfl_sync(0xffffffffu, incl, 31);
+  const int total = tot & 0xFFFF, etotal = tot >> 16;
   if (total == 0) return;
-  unsigned long long ebase = 0;
-  if (lane == 0 && etotal) ebase = atomicAdd(&P.counters[CNT_EDGES], (unsigned long long)etotal);
-  uint16_t* items = bb.items;
-  {
-    int pos = incl - cnt;
-    uint32_t pm = pmask;
-    while (pm) {
-      const int ty = __ffs(pm) - 1;
-      pm &= pm - 1;
-      items[pos++] = (uint16_t)(lane | (ty << 5));
-    }
+  const int rstart = (incl & 0xFFFF) - cnt, estart = (incl >> 16) - ecnt;
+  unsigned long long obase = 0, ebase = 0;
+  if (lane == 0) {
+    obase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
+    if (etotal) ebase = atomicAdd(&P.counters[CNT_EDGES], (unsigned long long)etotal);
   }
-  unsigned long long obase = 0;
-  if (lane == 0) obase = atomicAdd(&P.counters[CNT_NOUT], (unsigned long long)total);
+  // own-own pairs, while the atomics are in flight
+  unsigned long long lp = 0xBA9876543210ull;
+  for (uint32_t mm = opm; mm; mm &= mm - 1) {
+    const int cd = cCell[__ffs(mm) - 1];  // ta | tb << 4 | tc << 8 | axis << 12 | tf << 16
+    const int ta = cd & 15, tb = (cd >> 4) & 15, tc = (cd >> 8) & 15;
+    const int t1 = ((pmask >> ta) & 1u) ? ta : tb;
+    const int t2 = ((pmask >> tc) & 1u) ? tc : tb;
+    const int r1 = lfind(lp, t1), r2 = lfind(lp, t2);
+    const int lo = min(r1, r2), hi = max(r1, r2);
+    lp = (lp & ~(15ull << (4 * hi))) | ((unsigned long long)lo << (4 * hi));
+  }
+  bb.lp[lane] = lp;
+  bb.pm[lane] = pmask;
+  bb.rs[lane] = rstart;
+  {
+    int pos = rstart;
+    for (uint32_t pm = pmask; pm; pm &= pm - 1) bb.items[pos++] = (uint16_t)(lane | ((__ffs(pm) - 1) << 5));
+  }
   obase = __shfl_sync(0xffffffffu, obase, 0);
   ebase = __shfl_sync(0xffffffffu, ebase, 0);
-  // record index of own face type ty = obase + (first slot of this lane) + rank of ty in pmask
-  const long long rbase = (long long)obase + (incl - cnt);
-  if (P.parent) {
-    uint32_t pm = pmask;
-    while (pm) {
-      const int ty = __ffs(pm) - 1;
-      pm &= pm - 1;
-      const long long r = rbase + __popc(pmask & ((1u << ty) - 1u));
-      const int root = lfind(ty);
-      if (r < P.capacity) P.parent[r] = (int)(rbase + __popc(pmask & ((1u << root) - 1u)));
-    }
-  }
-  if (ecnt) {
-    unsigned long long eslot = ebase + (unsigned long long)(eincl - ecnt);
-#pragma unroll 1
-    for (int C = 0; C < 6; ++C) {
-      const uint32_t bits = epair[C];
-      if (!(bits & 8u)) continue;
-      const int cd = cCell[C];  // ta | tb << 4 | tc << 8 | axis << 12 | tf << 16
-      const int ty = (bits & 1u) ? (cd & 15) : ((bits & 2u) ? ((cd >> 4) & 15) : ((cd >> 8) & 15));
+  if (edm) {
+    unsigned long long eslot = ebase + (unsigned long long)estart;
+    const long long rbase = (long long)obase + rstart;
+    for (uint32_t mm = edm; mm; mm &= mm - 1, ++eslot) {
+      const int cd = cCell[__ffs(mm) - 1];
+      const int ta = cd & 15, tb = (cd >> 4) & 15, tc = (cd >> 8) & 15;
+      const int ty = ((pmask >> ta) & 1u) ? ta : (((pmask >> tb) & 1u) ? tb : tc);
       const long long a = rbase + __popc(pmask & ((1u << ty) - 1u));
       const int axis = (cd >> 12) & 7, tf = (cd >> 16) & 15;
       const i64 fx = x + (axis & 1), fy = y + ((axis >> 1) & 1), ft = t + ((axis >> 2) & 1);
@@ -686,16 +659,21 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
         P.edges[2 * eslot] = a;
         P.edges[2 * eslot + 1] = b;
       }
-      ++eslot;
     }
   }
   __syncwarp();
   for (int i = lane; i < total; i += 32) {
-    const int it = items[i];
+    const int it = bb.items[i];
     const int le = it & 31, ty = it >> 5;
     const int lqt = bb.qt[le];
     const Win<T> w2{bb.ring + le * ws_words<T>(), ((lqt >> 30) & 1) != 0, G.scale_f, G.scale};
-    emit_record<T>(w2, G, P, bb.qx[le], bb.qy[le], lqt & 0x3fffffff, ty, obase + i);
+    const unsigned long long slot = obase + i;
+    emit_record<T>(w2, G, P, bb.qx[le], bb.qy[le], lqt & 0x3fffffff, ty, slot);
+    // union-find parent: the in-cube root of ty (its smallest punctured type)
+    if (P.parent && slot < (unsigned long long)P.capacity) {
+      const int root = lfind(bb.lp[le], ty);
+      P.parent[slot] = (int)((long long)obase + bb.rs[le] + __popc(bb.pm[le] & ((1u << root) - 1u)));
+    }
   }
   __syncwarp();
 }
@@ -1191,16 +1169,6 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
   }
 }
 
-// Between K1a and K1b: size the pass-2 hash table for at most min(12 survivors, capacity) records
-// (a cube has 12 faces) and clear that many slots; K1b inserts every record it stores.
-__global__ void k_table_prep(const __grid_constant__ ExtractParams P) {
-  const long long bound = min(12 * (long long)P.counters[CNT_SURVIVORS], (long long)P.capacity);
-  const u64 hm = hash_slots(bound, P.table_cap) - 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_HMASK] = hm;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
-    P.table[i] = -1;
-}
-
 // Between K1a and K1b: expand the group entries (one per scan lane with surviving cubes: first
 // anchor, plane flag, 32-bit survivor mask) into the dense cube list K1b takes in batches of 32.
 // A block takes EXPI x 256 consecutive entries (EXPI per thread), block-wide exclusive scan of the
@@ -1273,9 +1241,9 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
   G.scale = P.scale;
   G.scale_f = (float)P.scale;
   G.qmax = ldexp(1.0, 29) / P.scale - 1.0 / P.scale;  // |f| < qmax -> |rint(f 2^s)| < 2^29
-  G.hm = P.counters[CNT_HMASK];
   const float qmaxf = (float)G.qmax;
-  BatchBuf bb{sm.ring + w * 32 * ws_words<T>(), sm.qx + w * 32, sm.qy + w * 32, sm.qt + w * 32, sm.items[w]};
+  BatchBuf bb{sm.ring + w * 32 * ws_words<T>(), sm.qx + w * 32, sm.qy + w * 32, sm.qt + w * 32, sm.items[w],
+              sm.lp + w * 32, sm.pm + w * 32, sm.rs + w * 32};
   const long long nwin = min((long long)*(volatile unsigned long long*)&P.counters[CNT_CUBES], (long long)P.wcap);
   const long long nbat = (nwin + 31) / 32;
   const T* field = reinterpret_cast<const T*>(P.field);
@@ -1382,18 +1350,12 @@ static int launch_t(const ExtractParams& P, cudaStream_t stream) {
   ExtractParams Q = P;
   Q.tchunk = TCHUNK;
   if (tiles * ((P.tb - P.ta + TCHUNK - 1) / TCHUNK) < 16 * slots) Q.tchunk = TCHUNK / 2;
-  static const int env_tchunk = getenv("FTK_TCHUNK") ? atoi(getenv("FTK_TCHUNK")) : 0;  // experiments
-  if (env_tchunk > 0) Q.tchunk = env_tchunk;
   const long long items = tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk);
   if (items <= 0) return FTK_OK;
   const long long grid = std::min<long long>(items, slots);
   kern<<<(unsigned)grid, NTHREADS, smem, stream>>>(map, Q);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
-  if (P.table) {
-    k_table_prep<<<(unsigned)(sms * 8), 256, 0, stream>>>(P);
-    FTK_CUDA_TRY(cudaGetLastError());
-  }
   {
     const int st = launch_expand2d(P, stream, sms);
     if (st) return st;

@@ -21,9 +21,7 @@ struct ExtractParams {
   unsigned long long* counters;  // Counter enum
   long long* edges;    // [capacity][2] trajectory-graph edges: (record, record or -1 - face_id)
   long long* fid;      // [capacity] face id of every record (compact copy for pass 2)
-  // 2D: K1b also fills the pass-2 hash table (face id -> record) and the union-find parents
-  int* table;          // [table_cap] slots, cleared by K1's table preparation
-  unsigned long long table_cap;
+  // 2D: K1b also writes the union-find parents of its in-cube unions
   int* parent;         // [capacity]
   // K1a -> K1b survivor list.  3D: one entry per surviving hypercube, anchors wx, wy, wz and
   // wt = t | (t+1 in the buffer) << 31 (-1: no cube).  2D: group entries (first anchor wx, wy of a scan

@@ -15,14 +15,15 @@
 
 #include "common.cuh"
 #include "extract2d.cuh"
-#include "track.cuh"
 #include "kuhn.cuh"
-#include <algorithm>
+#include "sort.cuh"
+#include "track.cuh"
 
 namespace ftk {
 
 static thread_local std::string g_last_error;
 static thread_local int g_profiling = 0;
+static thread_local uint32_t g_debug = 0;  // ftk_set_debug: FTK_DEBUG_* testing switches
 static thread_local float g_ms[4] = {0, 0, 0, 0};
 static thread_local int64_t g_stats[3] = {0, 0, 0};
 
@@ -150,15 +151,19 @@ static int range_status(const ftk_desc* d, unsigned long long maxbits) {
 
 static thread_local float g_kms[4] = {0, 0, 0, 0};  // K1a, K1b, pass 2, stitch
 
-struct Events {  // profiling events, created once per host thread and reused
+struct Events {  // profiling events, created once per host thread and device, and reused
   cudaEvent_t* e = nullptr;  // 4: between K1a and K1b
   bool on = false;
   Events() {
-    thread_local cudaEvent_t pool[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    if (g_profiling) {
-      if (!pool[0])
+    thread_local std::unordered_map<int, std::vector<cudaEvent_t>> pools;
+    int dev = 0;
+    if (g_profiling && cudaGetDevice(&dev) == cudaSuccess) {
+      std::vector<cudaEvent_t>& pool = pools[dev];
+      if (pool.empty()) {
+        pool.resize(5);
         for (auto& x : pool) cudaEventCreate(&x);
-      e = pool;
+      }
+      e = pool.data();
       on = true;
     }
   }
@@ -202,11 +207,6 @@ static ExtractParams extract_params(const ftk_desc* desc, const void* d_field, f
   EP.counters = counters;
   EP.edges = reinterpret_cast<long long*>(ws + L.edges);
   EP.fid = reinterpret_cast<long long*>(ws + L.fid);
-  // experiment: K1b inserts into the pass-2 table itself (its CAS latency lands on K1b's record
-  // path, slower than the separate insert kernel on C2)
-  const bool k1_insert = track && desc->ndim == 2 && getenv("FTK_K1B_INSERT") != nullptr;
-  EP.table = k1_insert ? reinterpret_cast<int*>(ws + L.table) : nullptr;
-  EP.table_cap = L.hcap;
   EP.parent = reinterpret_cast<int*>(ws + L.parent);
   EP.wx = reinterpret_cast<int*>(ws + L.wx);
   EP.wy = reinterpret_cast<int*>(ws + L.wy);
@@ -216,12 +216,12 @@ static ExtractParams extract_params(const ftk_desc* desc, const void* d_field, f
   EP.cy = reinterpret_cast<int*>(ws + L.cy);
   EP.ct = reinterpret_cast<int*>(ws + L.ct);
   EP.wcap = L.wcap;
-  EP.force_generic = getenv("FTK_FORCE_GENERIC") != nullptr;
+  EP.force_generic = (g_debug & FTK_DEBUG_FORCE_GENERIC) != 0;
   return EP;
 }
 
 static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t capacity, char* ws, const Layout& L,
-                                unsigned long long* counters, bool k1_insert) {
+                                unsigned long long* counters) {
   TrackParams TP;
   TP.rec = d_out;
   TP.capacity = capacity;
@@ -229,10 +229,8 @@ static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t cap
   TP.table = reinterpret_cast<int*>(ws + L.table);
   TP.table_cap = L.hcap;
   TP.edges = reinterpret_cast<const long long*>(ws + L.edges);
-  TP.verify = getenv("FTK_VERIFY_LINK") != nullptr;
-  TP.inserted = k1_insert;
+  TP.verify = (g_debug & FTK_DEBUG_VERIFY_LINK) != 0;
   TP.prelinked = desc->ndim == 2 && !is_vector(desc);  // the vector kernel emits all pairs as edges
-  TP.diag = getenv("FTK_PASS2_DIAG") ? atoi(getenv("FTK_PASS2_DIAG")) : 0;
   TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
   TP.fid = reinterpret_cast<i64*>(ws + L.fid);
   TP.parent = reinterpret_cast<int*>(ws + L.parent);
@@ -290,7 +288,7 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   if (st) return st;
   ev.rec(2, stream);
   if (track) {
-    TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters, EP.table != nullptr);
+    TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters);
     const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
     st = launch_track(TP, desc->ndim, ext, stream);
     if (st) return st;
@@ -304,13 +302,6 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
-  if (getenv("FTK_PRINT_PROF")) {
-    const char* names[] = {"scan", "wait_full", "enqueue", "wait_ring", "exact_wait", "exact_load", "exact_faces",
-                           "exact_records", "producer_wait", "other"};
-    fprintf(stderr, "K1 cycle accounting (sum over warps, Gcycles):");
-    for (int i = 0; i < 10; ++i) fprintf(stderr, " %s=%.3f", names[i], host_cnt[CNT_PROF + i] * 1e-9);
-    fprintf(stderr, " edges=%llu find_steps=%llu cas_retries=%llu\n", host_cnt[CNT_EDGES], host_cnt[30], host_cnt[31]);
-  }
   if (ev.on) {
     cudaEventElapsedTime(&g_ms[0], ev.e[1], ev.e[2]);
     cudaEventElapsedTime(&g_ms[1], ev.e[2], ev.e[3]);
@@ -451,17 +442,23 @@ struct NcclApi {
 };
 static NcclApi g_nccl;
 
+// seam pairs per list the communicator's blocks hold from ftk_comm_init on (a seam plane carries
+// about one ordinal face per critical point: ~4.2e4 on C4); larger lists take the host path once,
+// which grows the blocks (or call ftk_comm_reserve)
+static constexpr long long kDefaultSeamPairs = 1ll << 17;
+
 }  // namespace ftk
 
 struct ftk_comm {
   ncclComm_t comm = nullptr;
-  int rank = 0, world = 1;
-  long long* d_send = nullptr;  // library-owned exchange buffers, grown on demand
+  int rank = 0, world = 1, device = 0;
+  long long* d_send = nullptr;  // host-path exchange buffers (list overflow only), grown on demand
   long long* d_recv = nullptr;
   size_t cap_pairs = 0;
-  long long seam_cap = 0;       // pairs per list of a packed seam block (0: not sized yet)
+  long long seam_cap = 0;       // pairs per list of a packed seam block
   long long* d_gather = nullptr;  // world packed seam blocks (in-place allgather)
-  size_t gather_elems = 0;
+  char* d_scratch = nullptr;    // device resolve tables (SeamScratch), sized for world * seam_cap
+  size_t scratch_bytes = 0;
 };
 
 namespace ftk {
@@ -473,27 +470,44 @@ static int nccl_check(ncclResult_t r, const char* what) {
 }
 
 // ------------------------------------------------------------------ device seam path
-// library-owned scratch of the device resolve, per host thread, grown on demand
-static int seam_scratch(int world, long long cap, SeamScratch& S) {
-  thread_local char* base = nullptr;
-  thread_local size_t bytes = 0;
+// resolve tables for world * cap pairs per list, carved from `base` (bytes: seam_scratch_bytes)
+static size_t seam_scratch_bytes(int world, long long cap) {
   const u64 hb = hash_slots(2 * (long long)world * cap, 1ull << 40);
   const u64 hl = hash_slots(4 * (long long)world * cap, 1ull << 40);
-  const size_t need = hb * 16 + hl * 12 + 64;
-  if (need > bytes) {
-    if (base) cudaFree(base);
-    base = nullptr;
-    bytes = 0;
-    FTK_CUDA_TRY(cudaMalloc(&base, need));
-    bytes = need;
-  }
+  return hb * 16 + hl * 12 + 64;
+}
+static void seam_scratch_carve(char* base, int world, long long cap, SeamScratch& S) {
+  const u64 hb = hash_slots(2 * (long long)world * cap, 1ull << 40);
+  const u64 hl = hash_slots(4 * (long long)world * cap, 1ull << 40);
   S.hb_key = reinterpret_cast<long long*>(base);
   S.hb_val = S.hb_key + hb;
   S.hb_mask = hb - 1;
   S.hl_key = S.hb_val + hb;
   S.hl_mask = hl - 1;
   S.flags = reinterpret_cast<unsigned long long*>(S.hl_key + hl);
-  S.hl_parent = reinterpret_cast<int*>(S.flags + 2);
+  S.hl_parent = reinterpret_cast<int*>(S.flags + 4);
+}
+
+// scratch of the stand-alone ftk_seam_resolve (virtual slabs): library-owned per host thread and
+// device, grown on demand
+static int seam_scratch(int world, long long cap, SeamScratch& S) {
+  struct Buf {
+    char* base = nullptr;
+    size_t bytes = 0;
+  };
+  thread_local std::unordered_map<int, Buf> bufs;
+  int dev = 0;
+  FTK_CUDA_TRY(cudaGetDevice(&dev));
+  Buf& b = bufs[dev];
+  const size_t need = seam_scratch_bytes(world, cap);
+  if (need > b.bytes) {
+    if (b.base) cudaFree(b.base);
+    b.base = nullptr;
+    b.bytes = 0;
+    FTK_CUDA_TRY(cudaMalloc(&b.base, need));
+    b.bytes = need;
+  }
+  seam_scratch_carve(b.base, world, cap, S);
   return FTK_OK;
 }
 
@@ -509,17 +523,26 @@ static int seam_pack(void* d_ws, int64_t capacity, long long* block, long long c
   return launch_seam_pack(TP, block, cap, s);
 }
 
-// resolve all packed blocks on the device and relabel d_out; FTK_ERR_CAPACITY when a list did not fit
-// its block (nothing relabelled), FTK_ERR_INVARIANT for an A face no slab exported
+// resolve all packed blocks on the device and relabel d_out; fl = the resolve's flags (overflow,
+// unmatched A faces, failed-slab code)
+static int seam_resolve_flags(const long long* all, int world, long long cap, const SeamScratch& S, ftk_cp* d_out,
+                              i64 n, cudaStream_t s, unsigned long long (&fl)[3]) {
+  int st = launch_seam_resolve(all, world, cap, S, d_out, n, s);
+  if (st) return st;
+  FTK_CUDA_TRY(cudaMemcpyAsync(fl, S.flags, sizeof fl, cudaMemcpyDeviceToHost, s));
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  return FTK_OK;
+}
+
+// FTK_ERR_CAPACITY when a list did not fit its block (nothing relabelled), FTK_ERR_INVARIANT for an A
+// face no slab exported
 static int seam_resolve(const long long* all, int world, long long cap, ftk_cp* d_out, i64 n, cudaStream_t s) {
   SeamScratch S;
   int st = seam_scratch(world, cap, S);
   if (st) return st;
-  st = launch_seam_resolve(all, world, cap, S, d_out, n, s);
+  unsigned long long fl[3];
+  st = seam_resolve_flags(all, world, cap, S, d_out, n, s, fl);
   if (st) return st;
-  unsigned long long fl[2];
-  FTK_CUDA_TRY(cudaMemcpyAsync(fl, S.flags, sizeof fl, cudaMemcpyDeviceToHost, s));
-  FTK_CUDA_TRY(cudaStreamSynchronize(s));
   if (fl[0]) return FTK_ERR_CAPACITY;
   if (fl[1]) {
     g_last_error = "seam faces without a partner slab: " + std::to_string(fl[1]);
@@ -528,33 +551,80 @@ static int seam_resolve(const long long* all, int world, long long cap, ftk_cp* 
   return FTK_OK;
 }
 
-// Fast path: pack this slab's lists into its block of the gather buffer, one in-place NCCL allgather
-// of the fixed-size blocks, resolve and relabel on the device -- no host round trip except the final
-// flag check.  The block size is learnt from the first (host-path) call.
-static int stitch_device(ftk_comm* c, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity, cudaStream_t s) {
-  const long long stride = seam_stride(c->seam_cap);
-  const size_t need = (size_t)stride * c->world;
-  if (need > c->gather_elems) {
-    cudaFree(c->d_gather);
-    c->d_gather = nullptr;
-    c->gather_elems = 0;
-    FTK_CUDA_TRY(cudaMalloc(&c->d_gather, need * sizeof(long long)));
-    c->gather_elems = need;
-  }
-  long long* mine = c->d_gather + (size_t)c->rank * stride;
-  int st = seam_pack(d_ws, capacity, mine, c->seam_cap, s);
-  if (st) return st;
-  st = nccl_check(g_nccl.allGather(mine, c->d_gather, (size_t)stride, ncclInt64, c->comm, s), "ncclAllGather(seams)");
-  if (st) return st;
-  return seam_resolve(c->d_gather, c->world, c->seam_cap, d_out, n, s);
+// size the communicator's seam buffers for `cap` pairs per list (outside the hot path)
+static int comm_reserve(ftk_comm* c, long long cap) {
+  const size_t gather = (size_t)seam_stride(cap) * c->world;
+  const size_t scratch = seam_scratch_bytes(c->world, cap);
+  cudaFree(c->d_gather);
+  cudaFree(c->d_scratch);
+  c->d_gather = nullptr;
+  c->d_scratch = nullptr;
+  c->seam_cap = 0;
+  FTK_CUDA_TRY(cudaMalloc(&c->d_gather, gather * sizeof(long long)));
+  FTK_CUDA_TRY(cudaMalloc(&c->d_scratch, scratch));
+  c->scratch_bytes = scratch;
+  c->seam_cap = cap;
+  return FTK_OK;
 }
 
-// exchange this slab's A and B lists with every slab (two allgathers over NVLink), resolve, relabel
-static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity,
-                       cudaStream_t s) {
-  if (c->seam_cap > 0 && !getenv("FTK_STITCH_HOST")) {
-    const int st = stitch_device(c, d_out, n, d_ws, capacity, s);
-    if (st != FTK_ERR_CAPACITY) return st;  // else: a list outgrew the blocks; host path, resized
+// status code a failed slab publishes in its block header (as -code): every other error outranks a
+// capacity shortfall, so all ranks agree on one status and either all retry or all give up
+static long long fail_code(int st) { return st == FTK_ERR_CAPACITY ? st : st + 16; }
+static int code_status(unsigned long long code) { return code >= 16 ? (int)code - 16 : (int)code; }
+
+// Device path: pack this slab's lists (or, if its track failed, the failure code) into its block of
+// the pre-sized gather buffer, one in-place NCCL allgather of the fixed-size blocks, resolve and
+// relabel on the device -- no allocation and no host round trip except the final flag read.
+// Returns the agreed status; *overflow when some slab's list outgrew the blocks.
+static int stitch_device(ftk_comm* c, int local_st, ftk_cp* d_out, i64 n, void* d_ws, int64_t capacity,
+                         cudaStream_t s, bool* overflow) {
+  *overflow = false;
+  const long long stride = seam_stride(c->seam_cap);
+  long long* mine = c->d_gather + (size_t)c->rank * stride;
+  int st;
+  if (local_st) {
+    const long long hdr[2] = {-fail_code(local_st), 0};
+    FTK_CUDA_TRY(cudaMemcpyAsync(mine, hdr, sizeof hdr, cudaMemcpyHostToDevice, s));
+  } else {
+    st = seam_pack(d_ws, capacity, mine, c->seam_cap, s);
+    if (st) return st;
+  }
+  st = nccl_check(g_nccl.allGather(mine, c->d_gather, (size_t)stride, ncclInt64, c->comm, s), "ncclAllGather(seams)");
+  if (st) return st;
+  SeamScratch S;
+  seam_scratch_carve(c->d_scratch, c->world, c->seam_cap, S);
+  unsigned long long fl[3];
+  st = seam_resolve_flags(c->d_gather, c->world, c->seam_cap, S, d_out, local_st ? 0 : n, s, fl);
+  if (st) return st;
+  if (fl[2]) {
+    if (local_st) return local_st;
+    g_last_error = "the track of another time slab failed";
+    return code_status(fl[2]);
+  }
+  if (fl[0]) {
+    *overflow = true;
+    return FTK_OK;
+  }
+  if (fl[1]) {
+    g_last_error = "seam faces without a partner slab: " + std::to_string(fl[1]);
+    return FTK_ERR_INVARIANT;
+  }
+  return FTK_OK;
+}
+
+// Exchange this slab's A and B lists with every slab over NVLink, resolve, relabel.  Every rank
+// calls this after its local track, failed or not (local_st), so the collectives always match: the
+// device path carries the failure codes and all ranks return the same status.  Only when some list
+// outgrew the pre-sized blocks (every rank sees it) do all ranks take the host path, which also
+// re-sizes the blocks for the next calls.
+static int stitch_nccl(ftk_comm* c, int local_st, const ftk_desc* desc, ftk_cp* d_out, i64 n, void* d_ws,
+                       int64_t capacity, cudaStream_t s) {
+  // testing (FTK_DEBUG_STITCH_HOST): the device exchange only agrees on the status, then the host path
+  const bool force_host = (g_debug & FTK_DEBUG_STITCH_HOST) != 0;
+  bool overflow = false;
+  {
+    const int st = stitch_device(c, local_st, d_out, force_host ? 0 : n, d_ws, capacity, s, &overflow);
+    if (st || (!overflow && !force_host)) return st;
   }
   std::vector<long long> A, B;
   int st = read_exports(desc, d_ws, capacity, A, B, s);
@@ -579,7 +649,11 @@ static int stitch_nccl(ftk_comm* c, const ftk_desc* desc, ftk_cp* d_out, i64 n, 
     maxB = std::max(maxB, counts[2 * r + 1]);
   }
   // every rank sees the same counts: size the device path's blocks for the next calls
-  c->seam_cap = ((std::max(maxA, maxB) * 3 / 2 + 1024) + 4095) / 4096 * 4096;
+  const long long want = ((std::max(maxA, maxB) * 3 / 2 + 1024) + 4095) / 4096 * 4096;
+  if (want > c->seam_cap) {
+    st = comm_reserve(c, want);
+    if (st) return st;
+  }
   const size_t per = (size_t)(maxA + maxB);  // pairs per rank, padded
   if (per > c->cap_pairs) {
     cudaFree(c->d_send);
@@ -675,7 +749,6 @@ static int tracker_window(ftk_tracker* tr, bool last) {
   k_window_reset<<<1, 32, 0, tr->stream>>>(counters);
   FTK_CUDA_TRY(cudaGetLastError());
   ExtractParams EP = extract_params(&c, tr->buf, tr->out, tr->capacity, tr->ws, tr->L, counters, true);
-  EP.table = nullptr;
   int st = is_vector(&c) ? (c.ndim == 2 ? launch_extract_vec2d(EP, tr->stream) : launch_extract_vec3d(EP, tr->stream))
                          : (c.ndim == 2 ? launch_extract2d(EP, tr->stream) : launch_extract3d(EP, tr->stream));
   if (st) return st;
@@ -741,33 +814,59 @@ int ftk_workspace_size(const ftk_desc* d, int64_t capacity, size_t* bytes) {
   return FTK_OK;
 }
 
+// FTK_SORTED: records in face-id order (sort.cu), scratch from the workspace regions that are dead
+// once the labels are final (stitch lists, relabel map, survivor lists and windows)
+static int sort_output(const ftk_desc* desc, ftk_cp* d_out, int64_t n, void* d_ws, size_t ws_bytes, int64_t capacity,
+                       cudaStream_t s) {
+  if (!(desc->flags & FTK_SORTED) || n <= 1) return FTK_OK;
+  const Layout L = layout(capacity, esz_of(desc));
+  char* ws = static_cast<char*>(d_ws);
+  if (L.cross + sort_scratch_bytes(n) > ws_bytes) return FTK_ERR_INVALID_ARG;  // cannot happen: n <= capacity
+  const int T = desc->ndim == 2 ? 12 : 60;
+  const unsigned long long maxfid = (unsigned long long)T * desc->n[0] * desc->n[1] * desc->n[2] * desc->nt_global - 1;
+  const int bits = 64 - __builtin_clzll(maxfid | 1ull);
+  const SortScratch S = sort_scratch(ws + L.cross, n);
+  int st = launch_sort_records(d_out, reinterpret_cast<const long long*>(ws + L.fid), n, bits, S, s);
+  if (st) return st;
+  FTK_CUDA_TRY(cudaStreamSynchronize(s));
+  return FTK_OK;
+}
+
 int ftk_cp_extract(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
                    void* d_ws, size_t ws_bytes, ftk_stream stream) {
-  return run(desc, d_field, d_out, capacity, n_out, d_ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), false);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int st = run(desc, d_field, d_out, capacity, n_out, d_ws, ws_bytes, s, false);
+  if (st) return st;
+  return sort_output(desc, d_out, *n_out, d_ws, ws_bytes, capacity, s);
 }
 
 int ftk_cp_track(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
                  void* d_ws, size_t ws_bytes, ftk_stream stream, ftk_comm* comm) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int st = run(desc, d_field, d_out, capacity, n_out, d_ws, ws_bytes, s, true);
-  if (st || !comm || comm->world <= 1) return st;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (g_profiling) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, s);
+  if (comm && comm->world > 1) {
+    // every rank enters the exchange, so a failure on one slab cannot leave its peers waiting in
+    // NCCL: the failure codes travel in the seam blocks and all ranks return the agreed status
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_profiling) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+    const int local = st;
+    st = stitch_nccl(comm, local, desc, d_out, local ? 0 : *n_out, d_ws, capacity, s);
+    if (g_profiling) {
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&g_ms[2], e0, e1);
+      g_ms[3] += g_ms[2];
+      g_kms[3] = g_ms[2];
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
   }
-  st = stitch_nccl(comm, desc, d_out, *n_out, d_ws, capacity, s);
-  if (g_profiling) {
-    cudaEventRecord(e1, s);
-    cudaEventSynchronize(e1);
-    cudaEventElapsedTime(&g_ms[2], e0, e1);
-    g_ms[3] += g_ms[2];
-    g_kms[3] = g_ms[2];
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-  }
-  return st;
+  if (st) return st;
+  return sort_output(desc, d_out, *n_out, d_ws, ws_bytes, capacity, s);
 }
 
 int ftk_stitch_export(const ftk_desc* desc, void* d_ws, size_t ws_bytes, int64_t capacity, int64_t* h_A,
@@ -893,7 +992,7 @@ int ftk_tracker_finish(ftk_tracker* tr, int64_t* n_out) {
   f.nt_global = tr->pushed;
   f.flags = tr->desc.flags & FTK_VECTOR_FIELD;
   auto* counters = reinterpret_cast<unsigned long long*>(tr->ws + tr->L.counters);
-  TrackParams TP = track_params(&f, tr->out, tr->capacity, tr->ws, tr->L, counters, false);
+  TrackParams TP = track_params(&f, tr->out, tr->capacity, tr->ws, tr->L, counters);
   const i64 ext[4] = {f.n[0], f.n[1], f.n[2], f.nt_global};
   st = launch_track(TP, f.ndim, ext, tr->stream);
   if (st) return st;
@@ -931,7 +1030,7 @@ int ftk_post_adjacency(const ftk_desc* desc, const ftk_cp* d_rec, int64_t n, int
   char* ws = static_cast<char*>(d_ws);
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  TrackParams TP = track_params(desc, const_cast<ftk_cp*>(d_rec), n, ws, L, counters, false);
+  TrackParams TP = track_params(desc, const_cast<ftk_cp*>(d_rec), n, ws, L, counters);
   FTK_CUDA_TRY(cudaMemsetAsync(counters + CNT_INVARIANT, 0, sizeof(u64), s));
   const i64 ext[4] = {desc->n[0], desc->n[1], desc->n[2], desc->nt_global};
   st = launch_post_adjacency(TP, desc->ndim, ext, n, reinterpret_cast<long long*>(d_nbr), s);
@@ -957,7 +1056,7 @@ static int post_op(int op, const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d
   char* ws = static_cast<char*>(d_ws);
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  TrackParams TP = track_params(desc, d_rec, n, ws, L, counters, false);
+  TrackParams TP = track_params(desc, d_rec, n, ws, L, counters);
   PostCall c;
   c.rec = d_rec;
   c.rec_mut = d_rec;
@@ -1028,7 +1127,7 @@ int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ft
   ExtractParams EP = extract_params(desc, d_field, d_out, capacity, ws, L, counters, false);
   st = launch_iso(EP, (long long)cqd, desc->ndim, stream);
   if (st) return st;
-  TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters, false);
+  TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters);
   TP.T = desc->ndim == 2 ? 7 : 15;           // edge types per cube
   TP.lookup_types = (1ull << TP.T) - 1ull;   // links may name any edge
   TP.prelinked = false;
@@ -1107,13 +1206,24 @@ int ftk_comm_init(ftk_comm** comm, int rank, int world, const uint8_t id[128]) {
   ftk_comm* c = new ftk_comm();
   c->rank = rank;
   c->world = world;
-  const int st = nccl_check(g_nccl.commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+  int st = FTK_OK;
+  const cudaError_t de = cudaGetDevice(&c->device);
+  if (de != cudaSuccess) st = set_cuda_error(de, "cudaGetDevice");
+  if (!st) st = nccl_check(g_nccl.commInitRank(&c->comm, world, u, rank), "ncclCommInitRank");
+  // the seam blocks and resolve tables are allocated here, not in ftk_cp_track
+  if (!st && world > 1) st = comm_reserve(c, kDefaultSeamPairs);
   if (st) {
-    delete c;
+    ftk_comm_destroy(c);
     return st;
   }
   *comm = c;
   return FTK_OK;
+}
+
+int ftk_comm_reserve(ftk_comm* comm, int64_t seam_pairs) {
+  if (!comm || seam_pairs < 1) return FTK_ERR_INVALID_ARG;
+  if (comm->world <= 1 || seam_pairs <= comm->seam_cap) return FTK_OK;
+  return comm_reserve(comm, seam_pairs);
 }
 
 int ftk_comm_destroy(ftk_comm* comm) {
@@ -1122,7 +1232,15 @@ int ftk_comm_destroy(ftk_comm* comm) {
   cudaFree(comm->d_send);
   cudaFree(comm->d_recv);
   cudaFree(comm->d_gather);
+  cudaFree(comm->d_scratch);
   delete comm;
+  return FTK_OK;
+}
+
+int ftk_set_debug(uint32_t flags) {
+  if (flags & ~(uint32_t)(FTK_DEBUG_FORCE_GENERIC | FTK_DEBUG_VERIFY_LINK | FTK_DEBUG_STITCH_HOST))
+    return FTK_ERR_INVALID_ARG;
+  g_debug = flags;
   return FTK_OK;
 }
 

@@ -46,7 +46,7 @@ __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   return n < P.capacity ? n : P.capacity;
 }
 
-// the slot mask chosen by whoever cleared the table (k_clear here, or K1's table preparation)
+// the slot mask chosen by k_clear for this call
 __device__ __forceinline__ u64 table_mask(const TrackParams& P) { return P.counters[CNT_HMASK]; }
 
 __global__ void k_clear(const __grid_constant__ TrackParams P) {
@@ -106,17 +106,6 @@ __device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int
   }
 }
 
-__device__ __forceinline__ int uf_find_count(int* parent, int i, unsigned long long& steps) {
-  while (true) {
-    const int p = parent[i];
-    ++steps;
-    if (p == i) return i;
-    const int gp = parent[p];
-    if (gp != p) parent[i] = gp;
-    i = p;
-  }
-}
-
 __global__ void k_edges(const __grid_constant__ TrackParams P) {
   const i64 nrec = n_records(P);
   const i64 ne0 = (i64)P.counters[CNT_EDGES];
@@ -145,22 +134,6 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
     }
     if (a < 0 || b < 0 || a >= nrec || b >= nrec) {
       atomicAdd(&P.counters[CNT_INVARIANT], 1ull);  // a cell's partner face was never emitted
-      continue;
-    }
-    if (P.diag == 1) continue;  // diagnostics: lookups only
-    if (P.diag == 3) {  // diagnostics: count find steps and CAS retries (counters 30, 31)
-      unsigned long long steps = 0, retries = 0;
-      int ra = (int)a, rb = (int)b;
-      while (true) {
-        ra = uf_find_count(P.parent, ra, steps);
-        rb = uf_find_count(P.parent, rb, steps);
-        if (ra == rb) break;
-        if (P.fid[ra] < P.fid[rb]) { const int t = ra; ra = rb; rb = t; }
-        if (atomicCAS(&P.parent[ra], ra, rb) == ra) break;
-        ++retries;
-      }
-      atomicAdd(&P.counters[30], steps);
-      atomicAdd(&P.counters[31], retries);
       continue;
     }
     uf_unite(P.parent, P.fid, (int)a, (int)b);
@@ -263,7 +236,7 @@ __global__ void k_seam_clear(const __grid_constant__ SeamArgs A) {
     A.S.hl_key[i] = -1;
     A.S.hl_parent[i] = (int)i;
   }
-  if (i0 < 2) A.S.flags[i0] = 0;
+  if (i0 < 3) A.S.flags[i0] = 0;
 }
 
 __device__ __forceinline__ int hl_insert(const SeamScratch& S, long long label) {
@@ -292,6 +265,10 @@ __global__ void k_seam_insert(const __grid_constant__ SeamArgs A) {
   for (int r = 0; r < A.world; ++r) {
     const long long* blk = A.all + r * bs;
     const i64 nA = blk[0], nB = blk[1];
+    if (nA < 0) {  // the slab's track failed: -nA is its status code (see seam_fail)
+      if (i0 == 0) atomicMax(&A.S.flags[2], (unsigned long long)(-nA));
+      continue;
+    }
     if ((nA > A.cap || nB > A.cap) && i0 == 0) A.S.flags[0] = 1;
     const i64 mA = min(nA, (i64)A.cap), mB = min(nB, (i64)A.cap);
     for (i64 i = i0; i < mB; i += stride) {
@@ -359,7 +336,8 @@ __global__ void k_seam_union(const __grid_constant__ SeamArgs A) {
 
 // records whose label is on a seam take the label of its component root
 __global__ void k_seam_relabel(const __grid_constant__ SeamArgs A) {
-  if (A.S.flags[0]) return;  // a list overflowed its block: the caller takes the host path
+  if (A.S.flags[0] || A.S.flags[2]) return;  // a list overflowed its block (the caller takes the host
+                                              // path) or a slab failed (every rank reports it)
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
     const long long l = A.rec[i].label;
     const int node = hl_find(A.S, l);
@@ -729,12 +707,10 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
   using namespace trk;
   const int sms = num_sms();
   const int threads = 256, blocks = sms * 8;
-  if (!P.inserted) {  // 3D: K1 does not fill the table
-    k_clear<<<blocks, threads, 0, stream>>>(P);
-    FTK_CUDA_TRY(cudaGetLastError());
-    k_hash_insert<<<blocks, threads, 0, stream>>>(P);
-    FTK_CUDA_TRY(cudaGetLastError());
-  }
+  k_clear<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
+  k_hash_insert<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
   k_edges<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   for (int j = 0; j < FTK_LABEL_JUMP; ++j) k_jump<<<blocks, threads, 0, stream>>>(P);

@@ -18,12 +18,10 @@ struct TrackParams {
   int* parent;                   // [capacity] union-find parents
   const long long* edges;        // [capacity][2] edges from K1
   bool verify;                   // also re-derive every face's parent cells in closed form
-  bool inserted;                 // K1 already filled the table (experiment, FTK_K1B_INSERT)
   unsigned long long lookup_types;  // face types (bit per type) inserted into the table: the types
                                  // an edge or the verifier can look up
   bool prelinked;                // K1 initialised parent[] with its in-cube unions and emitted only
                                  // the edges to faces of neighbour cubes (2D)
-  int diag;                      // diagnostics (FTK_PASS2_DIAG): 1 = k_edges skips the unions
   // time slabs (multi-GPU stitch)
   int T;                         // face types per cube (12 / 60)
   i64 plane;                     // vertices per timestep (nx * ny * nz)
@@ -63,7 +61,7 @@ int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t st
 namespace ftk {
 
 // Device-side seam resolve for time slabs (no host round trip).  A packed seam block per slab:
-//   [0] nA, [1] nB, [2 .. 2 + 2 cap) A pairs (ghost-plane face id, local label),
+//   [0] nA (or -code when the slab's track failed), [1] nB, [2 .. 2 + 2 cap) A pairs (ghost-plane face id, local label),
 //   [2 + 2 cap .. 2 + 4 cap) B pairs (first-plane ordinal face id, local label);
 // the blocks of all slabs are concatenated (NCCL allgather), every rank resolves all of them the
 // same way and relabels its own records.
@@ -76,7 +74,8 @@ struct SeamScratch {            // library-owned, sized for world * cap pairs pe
   long long* hl_key;            // label -> node table; the node is the slot, parent per slot
   int* hl_parent;
   unsigned long long hl_mask;
-  unsigned long long* flags;    // [0] overflow (a slab's list exceeded cap), [1] unmatched A pairs
+  unsigned long long* flags;    // [0] overflow (a slab's list exceeded cap), [1] unmatched A pairs,
+                                // [2] max status code of the slabs whose track failed (0: none)
 };
 
 // pack this slab's lists (from the workspace after k_export) into its seam block

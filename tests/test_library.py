@@ -121,3 +121,25 @@ def test_capacity_bounds(ftk):
     assert L.ftk_workspace_size(ctypes.byref(desc), ftk.MAX_CAPACITY + 1, ctypes.byref(b)) == ftk.ERR_INVALID_ARG
     assert L.ftk_workspace_size(ctypes.byref(desc), -1, ctypes.byref(b)) == ftk.ERR_INVALID_ARG
     assert ftk.default_capacity(torch.empty(0)) == 1 << 16
+
+
+def test_debug_switches_validated_on_host(ftk):
+    """ftk_set_debug (the testing switches that replaced environment variables) rejects unknown bits"""
+    L = ftk.lib()
+    assert L.ftk_set_debug(ftk.DEBUG_FORCE_GENERIC | ftk.DEBUG_VERIFY_LINK | ftk.DEBUG_STITCH_HOST) == ftk.OK
+    assert L.ftk_set_debug(8) == ftk.ERR_INVALID_ARG
+    assert L.ftk_set_debug(0) == ftk.OK
+
+
+def test_product_reads_no_environment():
+    """the library takes no hidden switches from the environment (behaviour is fixed by
+    the descriptor and the explicit calls)"""
+    csrc = os.path.join(ROOT, "paper_2011_08697_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in src, f
+
+
+def test_comm_reserve_rejects_bad_args(ftk):
+    L = ftk.lib()
+    assert L.ftk_comm_reserve(None, 1024) == ftk.ERR_INVALID_ARG

@@ -104,24 +104,24 @@ def test_generic_loader_matches_tma(ftk, oracle_lib):
     w = fi.Woven(132, 72, 20, sigma=0.02)
     f = w.generate().cuda()
     a = ftk.to_numpy(ftk.track(f, 26))
-    os.environ["FTK_FORCE_GENERIC"] = "1"
+    ftk.set_debug(ftk.DEBUG_FORCE_GENERIC)
     try:
         b = ftk.to_numpy(ftk.track(f, 26))
     finally:
-        del os.environ["FTK_FORCE_GENERIC"]
+        ftk.set_debug(0)
     assert _sorted(a).tobytes() == _sorted(b).tobytes()
 
 
 def test_closed_form_link_verification(ftk, oracle_lib):
-    """K1 pairs faces per cell; the independent closed-form side_of verifier (FTK_VERIFY_LINK)
+    """K1 pairs faces per cell; the independent closed-form side_of verifier (FTK_DEBUG_VERIFY_LINK)
     re-derives every punctured face's parent cells and finds exactly one partner in each."""
-    os.environ["FTK_VERIFY_LINK"] = "1"
+    ftk.set_debug(ftk.DEBUG_VERIFY_LINK)
     try:
         for f in (fi.Woven(150, 140, 40, sigma=0.08).generate(), fi.random_degenerate((6, 37, 150), seed=4)):
             s = 26 if f.abs().max() < 2 and f.dtype == torch.float32 and (f != f.round()).any() else 0
             run_pair(ftk, oracle_lib, f, s)
     finally:
-        del os.environ["FTK_VERIFY_LINK"]
+        ftk.set_debug(0)
 
 
 def test_extract_window_with_ghost(ftk, oracle_lib):
