@@ -10,8 +10,11 @@ synthetic input already resident in HBM.  Metric (BASELINE.json): spacetime face
 measured HBM roofline.
 
 N = 1: workload C2 (2D woven 1024 x 1024 x 256, BASELINE.json configs[1]).
-N > 1: weak scaling -- every rank owns a C2-sized time slab (256 timesteps + one ghost plane) of a
-global woven field with 256*N timesteps; trajectories are stitched across slabs (NCCL).
+N > 1 (default --scaling weak): every rank owns a C2-sized time slab (256 timesteps + one ghost plane)
+of a global woven field with 256*N timesteps; trajectories are stitched across slabs (NCCL).
+--scaling strong: the configuration's whole time axis (e.g. --config C4, 4096^2 x 512, the north_star
+strong-scaling target) split into N contiguous slabs of nt/N timesteps + one ghost plane; N = 1 tracks
+the whole field on one GPU.  The driver computes the scaling efficiency from the per-N values.
 
 --impl reference: the CPU oracle (oracle/, plain C + OpenMP, never tuned) on this box's host cores,
 same metric and config, each step a bounded sample of the workload.
@@ -209,7 +212,11 @@ def run_ours(args):
     spatial, nt = cfg.shape[:-1], cfg.shape[-1]
     vec = cfg.kind in ("gyre2d", "abc3d")  # vector fields (FTK_VECTOR_FIELD), SURVEY.md 8(f) NEXT row 2
     w = cfg.make()
-    if world > 1:
+    if args.scaling == "strong":  # the config's time axis split into world slabs (+ one ghost plane)
+        b = ftk.slab_bounds(nt, world)
+        nt_global, t0, ghost = nt, b[rank], rank < world - 1
+        nbuf = b[rank + 1] - b[rank] + (1 if ghost else 0)
+    elif world > 1:  # weak: a slab of the config's size per rank
         nt_global = nt * world
         w.nt = nt_global
         t0 = rank * nt
@@ -307,6 +314,33 @@ def run_ours(args):
 
     # end to end through the C-ABI from pinned host memory (H2D + D2H inside the timed region)
     e2e = None
+    if world > 1 and not args.no_e2e:
+        # every rank: its slab from pinned host memory, track with the stitch, records back to the host;
+        # CUDA events on the launch stream, max over ranks
+        host = field.cpu().pin_memory()
+        stage = torch.empty_like(field)
+        times, nrec = [], 0
+        for i in range(max(3, min(args.steps, 20)) + 1):
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            stage.copy_(host, non_blocking=True)
+            rec_e = ftk.track(stage, cfg.scale_log2, t0=t0, nt_global=nt_global, ghost=ghost, buffers=buf, comm=cptr,
+                              vector=vec)
+            out = rec_e.cpu()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            nrec = out.shape[0]
+            if i:
+                times.append(e0.elapsed_time(e1))
+        t = torch.tensor([sum(times) / len(times)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": total_faces / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": field.numel() * esz, "d2h_bytes_per_step": nrec * ftk.RECORD_BYTES,
+               "per": "rank (max over ranks); bytes of rank 0"}
+        del host, stage
     if world == 1 and not args.no_e2e:
         host = field.cpu().pin_memory()
         out_host = torch.empty(buf.capacity * ftk.RECORD_BYTES, dtype=torch.uint8).pin_memory()
@@ -412,9 +446,12 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.desc}" + (f", {world} time slabs of {nt} + ghost" if world > 1 else ""),
+        "config": {"workload": f"{cfg.name}: {cfg.desc}" + (
+                       f", {world} time slabs of {nt} + ghost" if world > 1 and args.scaling == "weak" else
+                       f", strong scaling: {nt} timesteps in {world} slab(s) of ~{nt // world} + ghost"
+                       if args.scaling == "strong" else ""),
                    "grid": [*spatial, nt_global], "faces_per_step": int(total_faces),
                    "punctured_per_step": int(n_punct), "input": f"{field.dtype}".replace("torch.", ""),
                    "arith": "exact int64/int128 predicates, fixed-order f64 location/type, f32 prefilter",
@@ -465,6 +502,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = a config-sized slab per rank; strong = the config's time axis split")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
