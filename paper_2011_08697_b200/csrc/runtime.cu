@@ -236,6 +236,15 @@ static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t cap
   TP.parent = reinterpret_cast<int*>(ws + L.parent);
   TP.T = desc->ndim == 2 ? 12 : 60;
   TP.plane = desc->n[0] * desc->n[1] * desc->n[2];
+  TP.ndim = desc->ndim;
+  TP.ext[0] = desc->n[0];
+  TP.ext[1] = desc->n[1];
+  TP.ext[2] = desc->n[2];
+  TP.ext[3] = desc->nt_global;
+  TP.inv[0] = 1.0 / TP.T;
+  TP.inv[1] = 1.0 / (double)desc->n[0];
+  TP.inv[2] = 1.0 / (double)desc->n[1];
+  TP.inv[3] = 1.0 / (double)desc->n[2];
   TP.ghost_t = (desc->flags & FTK_GHOST_PLANE) ? desc->t0 + desc->nt - 1 : -1;
   TP.first_t = desc->t0 > 0 ? desc->t0 : -1;
   TP.cross = reinterpret_cast<long long*>(ws + L.cross);
@@ -1129,6 +1138,7 @@ int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ft
   if (st) return st;
   TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters);
   TP.T = desc->ndim == 2 ? 7 : 15;           // edge types per cube
+  TP.inv[0] = 1.0 / TP.T;
   TP.lookup_types = (1ull << TP.T) - 1ull;   // links may name any edge
   TP.prelinked = false;
   TP.verify = false;

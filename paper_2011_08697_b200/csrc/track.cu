@@ -41,6 +41,46 @@ __constant__ KuhnTables<4> cK4 = kKuhn4;
 
 __device__ __forceinline__ u64 mix(u64 k) { return hash_mix(k); }
 
+// exact n / d for 0 <= n < 2^52 from a floating-point first guess (off by at most one)
+__device__ __forceinline__ i64 divq(i64 n, i64 d, double inv) {
+  i64 q = (i64)((double)n * inv);
+  if (q * d > n) --q;
+  else if ((q + 1) * d <= n) ++q;
+  return q;
+}
+
+// Slot of a face id in the pass-2 table: spatially blocked open addressing.  The table is cut into
+// blocks of HBLK slots; a face's block is picked by a hash of its coarse position -- the 128-column x
+// tile, 64 rows (3D: 8 rows x 8 slices) and 32 (3D: 16) timesteps, the grain of K1a's work items, whose
+// records are emitted together -- and the slot inside it by a hash of the face id.  The inserts and
+// lookups of one work item's records and edges (processed in emission order) thus stay within a few
+// blocks that are resident in L2, instead of touching the whole table.  Linear probing continues into
+// the next block on a full block (rare: the table holds 1.5 slots per record).
+constexpr int HBLK_LOG2 = 12;
+__device__ __forceinline__ u64 slot_of(const TrackParams& P, u64 hm, long long key) {
+  const u64 h = mix((u64)key);
+  if (hm < (1ull << HBLK_LOG2)) return h & hm;
+  const i64 I = divq(key, P.T, P.inv[0]);
+  const i64 r1 = divq(I, P.ext[0], P.inv[1]);
+  const i64 x = I - r1 * P.ext[0];
+  const i64 r2 = divq(r1, P.ext[1], P.inv[2]);
+  const i64 y = r1 - r2 * P.ext[1];
+  u64 coarse;
+  if (P.ndim == 2) {  // r2 = t
+    coarse = ((u64)(r2 >> 5) * (u64)((P.ext[1] + 63) >> 6) + (u64)(y >> 6)) * (u64)((P.ext[0] + 127) >> 7) + (u64)(x >> 7);
+  } else {
+    const i64 t = divq(r2, P.ext[2], P.inv[3]);
+    const i64 z = r2 - t * P.ext[2];
+    coarse = (((u64)(t >> 4) * (u64)((P.ext[2] + 7) >> 3) + (u64)(z >> 3)) * (u64)((P.ext[1] + 7) >> 3) + (u64)(y >> 3)) *
+                 (u64)((P.ext[0] + 127) >> 7) + (u64)(x >> 7);
+  }
+  // consecutive coarse cells take consecutive blocks (modulo the block count): no two cells share a
+  // block while there are at least as many blocks as cells, and then each block holds ~one cell's faces
+  // at the table's load factor; a hashed block choice would collide cells and grow long probe chains
+  const u64 blk = coarse & (hm >> HBLK_LOG2);
+  return (blk << HBLK_LOG2) | (h & ((1ull << HBLK_LOG2) - 1));
+}
+
 __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   const i64 n = (i64)P.counters[CNT_NOUT];
   return n < P.capacity ? n : P.capacity;
@@ -64,14 +104,14 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
     if (!P.prelinked) P.parent[i] = (int)i;
     // only faces that some cell of a neighbour cube looks up (the "upper" types) need a slot
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
-    u64 h = mix((u64)key) & hm;
+    u64 h = slot_of(P, hm, key);
     // face ids are unique among the records: claim the first empty slot of the probe sequence
     while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) h = (h + 1) & hm;
   }
 }
 
 __device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long long key) {
-  u64 h = mix((u64)key) & hm;
+  u64 h = slot_of(P, hm, key);
   while (true) {
     const int r = P.table[h];
     if (r == EMPTY) return -1;

@@ -22,8 +22,12 @@ struct TrackParams {
                                  // an edge or the verifier can look up
   bool prelinked;                // K1 initialised parent[] with its in-cube unions and emitted only
                                  // the edges to faces of neighbour cubes (2D)
+  // geometry of the face ids (the spatially blocked hash decodes them)
+  int ndim;
+  i64 ext[4];                    // nx, ny, nz, nt (global)
+  double inv[4];                 // 1 / T, 1 / nx, 1 / ny, 1 / nz (first guess of the id divisions)
   // time slabs (multi-GPU stitch)
-  int T;                         // face types per cube (12 / 60)
+  int T;                         // face types per cube (12 / 60; isovolumes: edge types 7 / 15)
   i64 plane;                     // vertices per timestep (nx * ny * nz)
   i64 ghost_t;                   // global t of the ghost plane, -1 without one
   i64 first_t;                   // global t of the first owned plane if t0 > 0, else -1
