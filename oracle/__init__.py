@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
                                    ctypes.c_int64, P, P]
         L.ftko_track.argtypes = [ctypes.POINTER(_Desc), P, P, ctypes.c_int64, P, P, P]
         L.ftko_iso_track.argtypes = [ctypes.POINTER(_Desc), P, ctypes.c_double, P, ctypes.c_int64, P, P, P]
+        L.ftko_iso_mesh.argtypes = [ctypes.POINTER(_Desc), P, ctypes.c_double, P, ctypes.c_int64, P]
     return _lib
 
 
@@ -217,3 +218,21 @@ def iso_track(field: np.ndarray, scale_log2: int, isovalue: float, nthreads: int
         raise OracleError(st, "iso_track")
     info = dict(cells=int(stats[0]), bad_cells=int(stats[1]), components=int(stats[2]), status=st)
     return out[: n_out.value], n_edges.value, info
+
+
+def iso_mesh(field: np.ndarray, scale_log2: int, isovalue: float, nthreads: int = 0) -> np.ndarray:
+    """The isovolume's simplices: int64 [n_elems, n + 1] edge ids (triangles in
+    2D+t, tetrahedra in 3D+t), one per staircase path of every cell the level set crosses."""
+    d, field = _desc(field, scale_log2, 0, None, nthreads)
+    dim = d.ndim + 1
+    n_out = ctypes.c_int64(0)
+    st = lib().ftko_iso_mesh(ctypes.byref(d), field.ctypes.data, ctypes.c_double(isovalue), None, 0,
+                             ctypes.byref(n_out))
+    if st not in (OK, CAPACITY):
+        raise OracleError(st, "iso_mesh")
+    out = np.zeros((max(n_out.value, 1), dim), np.int64)
+    st = lib().ftko_iso_mesh(ctypes.byref(d), field.ctypes.data, ctypes.c_double(isovalue), out.ctypes.data,
+                             n_out.value, ctypes.byref(n_out))
+    if st != OK:
+        raise OracleError(st, "iso_mesh")
+    return out[: n_out.value]
