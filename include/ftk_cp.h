@@ -276,6 +276,19 @@ FTK_API int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int
  * records AND the cell links (several per crossed edge). */
 FTK_API int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
                           int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream);
+/* As ftk_iso_track, plus the isovolume itself as a simplicial mesh ("the output isovolumes
+ * ... can be represented as a tetrahedral grid"): for every cell the level set crosses, with P / M its
+ * positive / negative vertices in chain order (|P| + |M| = n + 2), the staircase triangulation of the
+ * product simplex(P) x simplex(M) -- one simplex per monotone lattice path from (P_0, M_0) to
+ * (P_last, M_last), its n + 1 vertices the crossed edges (P_i, M_j) along the path, given by their edge
+ * ids (= the records' face_id; the intersection points are the records' locations).  That is 1 simplex
+ * in case I and C(|P| + |M| - 2, |P| - 1) in case II: 3 tetrahedra for ++--- in 3D+t, 2
+ * triangles for ++-- in 2D+t.  d_elems: device int64 [elem_cap][n + 1] (n = desc->ndim), order
+ * unspecified across cells; *n_elems = the simplex count, FTK_ERR_CAPACITY when it exceeds elem_cap
+ * (retry with *n_elems).  FTK_ERR_INVALID_ARG for a null n_elems or elem_cap > 0 with a null d_elems. */
+FTK_API int ftk_iso_track_mesh(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out,
+                               int64_t capacity, int64_t* n_out, int64_t* d_elems, int64_t elem_cap, int64_t* n_elems,
+                               void* d_ws, size_t ws_bytes, ftk_stream stream);
 
 /* Multi-GPU communicator over NCCL (one process per GPU).  Rank 0 creates the unique id, the
  * caller broadcasts the 128 bytes (e.g. with torch.distributed), every rank calls init. */

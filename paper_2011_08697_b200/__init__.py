@@ -44,6 +44,7 @@ EXPORTS = [
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
     "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
     "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types", "ftk_iso_track",
+    "ftk_iso_track_mesh",
 ]
 
 
@@ -109,6 +110,7 @@ def lib() -> ctypes.CDLL:
         L.ftk_post_filter.argtypes = [PD, P, P, I64, ctypes.c_double, ctypes.c_int32, P, I64, P, P, SZ, I64, P]
         L.ftk_post_smooth_types.argtypes = [PD, P, P, I64, ctypes.c_int32, P, SZ, I64, P]
         L.ftk_iso_track.argtypes = [PD, ctypes.c_double, P, P, I64, P, P, SZ, P]
+        L.ftk_iso_track_mesh.argtypes = [PD, ctypes.c_double, P, P, I64, P, P, I64, P, P, SZ, P]
         _lib = L
     return _lib
 
@@ -221,30 +223,47 @@ def _run(fn_name: str, field: torch.Tensor, scale_log2: int, t0: int, nt_global,
 
 
 def iso_track(field: torch.Tensor, scale_log2: int, isovalue: float, capacity: int | None = None,
-              buffers: Buffers | None = None, return_buffers: bool = False):
+              buffers: Buffers | None = None, return_buffers: bool = False, mesh: bool = False):
     """Isovolume tracking: the crossed spacetime edges of f = isovalue as 56-byte
     records (face_id = edge id, Eq. 2 location, type 1 = upward crossing, label = min edge id of the
-    connected isovolume piece).  field: [t][y][x] or [t][z][y][x] on the device, the whole domain."""
+    connected isovolume piece).  field: [t][y][x] or [t][z][y][x] on the device, the whole domain.
+    mesh=True also returns the isovolume's simplices (ftk_iso_track_mesh: triangles in 2D+t, tetrahedra in
+    3D+t) as an int64 [n, ndim + 1] device tensor of edge ids: (rec, elems[, buffers])."""
     if not field.is_cuda:
         raise FtkError(ERR_INVALID_ARG, "iso_track: field must be a CUDA tensor (no CPU fallback)")
     field = field.contiguous()
     desc = make_desc(tuple(field.shape), field.dtype, scale_log2)
     cap = capacity if capacity is not None else (buffers.capacity if buffers else default_capacity(field))
+    ecap = 4 * cap
+    elems = None
     while True:
         if buffers is None or buffers.capacity < cap:
             buffers = Buffers.allocate(desc, cap, field.device)
         n_out = ctypes.c_int64(0)
-        st = lib().ftk_iso_track(ctypes.byref(desc), ctypes.c_double(isovalue), ctypes.c_void_p(field.data_ptr()),
-                                 ctypes.c_void_p(buffers.records.data_ptr()), buffers.capacity, ctypes.byref(n_out),
-                                 ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
-                                 ctypes.c_void_p(_stream_ptr(field.device)))
+        n_el = ctypes.c_int64(0)
+        common = (ctypes.byref(desc), ctypes.c_double(isovalue), ctypes.c_void_p(field.data_ptr()),
+                  ctypes.c_void_p(buffers.records.data_ptr()), buffers.capacity, ctypes.byref(n_out))
+        tail = (ctypes.c_void_p(buffers.workspace.data_ptr()), buffers.workspace.numel(),
+                ctypes.c_void_p(_stream_ptr(field.device)))
+        if mesh:
+            if elems is None or elems.shape[0] < ecap:
+                elems = torch.empty((max(ecap, 1), desc.ndim + 1), dtype=torch.int64, device=field.device)
+            st = lib().ftk_iso_track_mesh(*common, ctypes.c_void_p(elems.data_ptr()), elems.shape[0],
+                                          ctypes.byref(n_el), *tail)
+        else:
+            st = lib().ftk_iso_track(*common, *tail)
         if st == ERR_CAPACITY and cap < MAX_CAPACITY:
-            cap = min(MAX_CAPACITY, int(n_out.value * 1.25) + 1024)
-            buffers = None
+            if n_out.value > buffers.capacity:
+                cap = min(MAX_CAPACITY, int(n_out.value * 1.25) + 1024)
+                buffers = None
+            if mesh and n_el.value > elems.shape[0]:
+                ecap = n_el.value
             continue
         _check(st, "ftk_iso_track")
         rec = buffers.records[: n_out.value * RECORD_BYTES].view(torch.int64).view(-1, 7)
-        return (rec, buffers) if return_buffers else rec
+        out = (rec, elems[: n_el.value]) if mesh else (rec,)
+        out = out + (buffers,) if return_buffers else out
+        return out if len(out) > 1 else out[0]
 
 
 def extract(field: torch.Tensor, scale_log2: int, t0: int = 0, nt_global: int | None = None,

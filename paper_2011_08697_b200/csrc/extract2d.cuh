@@ -31,6 +31,9 @@ struct ExtractParams {
   int* wz;
   int *cx, *cy, *ct;
   i64 wcap;
+  bool mesh;           // isovolume mesh requested: count the simplices, write up to elem_cap of them
+  long long* elems;    // [elem_cap][ndim + 1] crossed-edge ids per simplex
+  i64 elem_cap;
   bool force_generic;  // testing: disable TMA
   void* ev_mid;        // profiling: cudaEvent_t recorded between K1a and K1b (2D), or null
 };

@@ -13,7 +13,9 @@
 //     (0, D or 2 (D - 1) of them -- cases I and II, else FTK_ERR_INVARIANT) are united in a
 //     cube-local union-find over the cube's comparable corner pairs, and every local component is
 //     emitted as trajectory-graph links (representative, member) -- an end is a record index when the
-//     edge is anchored at v, else -1 - edge id (resolved by pass 2 through the hash).
+//     edge is anchored at v, else -1 - edge id (resolved by pass 2 through the hash);
+//   * mesh (optional): the cells' isovolume simplices (staircase triangulation) as tuples of
+//     crossed-edge ids.
 // Pass 2 (track.cu: hash of every record, links, lock-free union-find, min-id labels) is shared.
 #include <cstdio>
 
@@ -233,6 +235,60 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
           }
         }
       if (cnt != 0 && cnt != D && cnt != 2 * (D - 1)) atomicAdd(&P.counters[CNT_INVARIANT], 1ull);
+    }
+    // isovolume mesh: per crossed cell, the staircase triangulation of simplex(P) x
+    // simplex(M) -- P / M the cell's positive / negative chain vertices -- one D-vertex simplex per
+    // monotone lattice path, its vertices the crossed edges along the path (edge ids); C(|P| + |M| - 2,
+    // |P| - 1) of them: 1 in case I, 3 tetrahedra for ++--- (3D+t), 2 triangles for ++-- (2D+t)
+    if (P.mesh) {
+      constexpr int NB[5][5] = {{0, 0, 0, 0, 0}, {0, 1, 1, 1, 1}, {0, 1, 2, 3, 4}, {0, 1, 3, 6, 10}, {0, 1, 4, 10, 20}};
+      int nel = 0;
+      for (int pi = 0; cells && pi < PM.n; ++pi) {
+        int np = 0, c = 0;
+#pragma unroll
+        for (int k = 0; k <= D; ++k) {
+          if (k) c |= 1 << PM.p[pi][k - 1];
+          np += (pos >> c) & 1u;
+        }
+        if (np > 0 && np <= D) nel += NB[np][D + 1 - np];  // C(np - 1 + nm - 1, np - 1), nm = D + 1 - np
+      }
+      unsigned long long el = warp_reserve(nel, CNT_ELEMS);
+      for (int pi = 0; cells && pi < PM.n; ++pi) {
+        int chain[D + 1], Pv[D + 1], Mv[D + 1], np = 0, nm = 0;
+        chain[0] = 0;
+#pragma unroll
+        for (int k = 1; k <= D; ++k) chain[k] = chain[k - 1] | (1 << PM.p[pi][k - 1]);
+#pragma unroll
+        for (int k = 0; k <= D; ++k) {
+          if ((pos >> chain[k]) & 1u) Pv[np++] = k;
+          else Mv[nm++] = k;
+        }
+        if (np == 0 || nm == 0) continue;
+        const int steps = np + nm - 2;
+        for (int code = 0; code < (1 << steps); ++code) {
+          if (__popc(code) != np - 1) continue;
+          if (el < (unsigned long long)P.elem_cap) {
+            long long* out = P.elems + el * D;
+            int ip = 0, im = 0;
+            for (int st = -1; st < steps; ++st) {
+              if (st >= 0) {
+                if ((code >> (steps - 1 - st)) & 1) ++ip;
+                else ++im;
+              }
+              const int a = min(Pv[ip], Mv[im]), b = max(Pv[ip], Mv[im]);
+              const int ca = chain[a], cb = chain[b];
+              i64 id = 0, stride = 1;
+#pragma unroll
+              for (int x = 0; x < D; ++x) {
+                id += (v[x] + ((ca >> x) & 1)) * stride;
+                stride *= ext[x];
+              }
+              out[st + 1] = id * E + ((cb ^ ca) - 1);
+            }
+          }
+          ++el;
+        }
+      }
     }
     // links: every crossed slot of a local component to the component's root slot
     auto end_of = [&](int sl) -> long long {

@@ -1116,8 +1116,9 @@ int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_
 }
 
 // ------------------------------------------------------------------------------ isovolume tracking
-int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
-                  int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream_) {
+static int iso_run(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                   int64_t* n_out, bool mesh, int64_t* d_elems, int64_t elem_cap, int64_t* n_elems, void* d_ws,
+                   size_t ws_bytes, ftk_stream stream_) {
   int st = validate(desc);
   if (st) return st;
   if (is_vector(desc) || (desc->flags & FTK_GHOST_PLANE) || desc->t0 != 0 || desc->nt != desc->nt_global || desc->nt < 2)
@@ -1134,6 +1135,9 @@ int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ft
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
   FTK_CUDA_TRY(cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), stream));
   ExtractParams EP = extract_params(desc, d_field, d_out, capacity, ws, L, counters, false);
+  EP.mesh = mesh;
+  EP.elems = reinterpret_cast<long long*>(d_elems);
+  EP.elem_cap = elem_cap;
   st = launch_iso(EP, (long long)cqd, desc->ndim, stream);
   if (st) return st;
   TrackParams TP = track_params(desc, d_out, capacity, ws, L, counters);
@@ -1151,17 +1155,32 @@ int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ft
   FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = (int64_t)host_cnt[CNT_NOUT];
+  if (n_elems) *n_elems = (int64_t)host_cnt[CNT_ELEMS];
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
   if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity) {
     *n_out = std::max<int64_t>((int64_t)host_cnt[CNT_NOUT], (int64_t)host_cnt[CNT_EDGES]);
     return FTK_ERR_CAPACITY;
   }
+  if (mesh && (int64_t)host_cnt[CNT_ELEMS] > elem_cap) return FTK_ERR_CAPACITY;  // *n_elems = the need
   if (host_cnt[CNT_INVARIANT]) {
     g_last_error = "isovolume cells with a crossed-edge count not in {0, d, 2(d-1)}: " + std::to_string(host_cnt[CNT_INVARIANT]);
     return FTK_ERR_INVARIANT;
   }
   return FTK_OK;
+}
+
+int ftk_iso_track(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                  int64_t* n_out, void* d_ws, size_t ws_bytes, ftk_stream stream) {
+  return iso_run(desc, isovalue, d_field, d_out, capacity, n_out, false, nullptr, 0, nullptr, d_ws, ws_bytes, stream);
+}
+
+int ftk_iso_track_mesh(const ftk_desc* desc, double isovalue, const void* d_field, ftk_cp* d_out, int64_t capacity,
+                       int64_t* n_out, int64_t* d_elems, int64_t elem_cap, int64_t* n_elems, void* d_ws,
+                       size_t ws_bytes, ftk_stream stream) {
+  if (!n_elems || elem_cap < 0 || (elem_cap > 0 && !d_elems)) return FTK_ERR_INVALID_ARG;
+  return iso_run(desc, isovalue, d_field, d_out, capacity, n_out, true, d_elems, elem_cap, n_elems, d_ws, ws_bytes,
+                 stream);
 }
 
 int ftk_set_profiling(int enable) {

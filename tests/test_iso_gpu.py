@@ -74,3 +74,58 @@ def test_degenerate(ftk, oracle_lib, shape, seed):
 def test_fp64(ftk, oracle_lib):
     f = fi.Woven(50, 40, 5, L=15.0).generate(dtype=torch.float64)
     run_pair(ftk, oracle_lib, f, 26, 0.1)
+
+
+# ----------------------------------------------------------------------- isovolume mesh
+def mesh_pair(ftk, oracle_lib, f: torch.Tensor, s: int, c: float):
+    """the GPU's simplices (ftk_iso_track_mesh) against the oracle's iso_mesh: the same set of simplices,
+    each with the same edge ids in the same (staircase path) order"""
+    rec, el = ftk.iso_track(f.cuda(), s, c, mesh=True)
+    g = el.cpu().numpy()
+    r = oracle_lib.iso_mesh(f.numpy(), s, c)
+    assert g.shape == r.shape, (g.shape, r.shape)
+    gs = set(map(tuple, g.tolist()))
+    assert len(gs) == len(g)
+    assert gs == set(map(tuple, r.tolist()))
+    # every simplex vertex is one of the call's crossed-edge records
+    assert set(np.unique(g).tolist()) <= set(ftk.to_numpy(rec)["face_id"].tolist())
+    return len(g)
+
+
+def test_mesh_paper_plane(ftk, oracle_lib):
+    assert mesh_pair(ftk, oracle_lib, plane(0.9, (12, 21, 21, 21)), 20, 0.0) > 1000
+    assert mesh_pair(ftk, oracle_lib, plane(0.875, (9, 13, 140)), 20, 0.0) > 100
+
+
+@pytest.mark.parametrize("shape,c", [((6, 40, 150), 0.3), ((4, 12, 11, 140), 0.25), ((3, 9, 10, 11), 0.0)])
+def test_mesh_woven(ftk, oracle_lib, shape, c):
+    if len(shape) == 3:
+        nt, ny, nx = shape
+        f = fi.Woven(nx, ny, nt, L=15.0, sigma=0.02).generate()
+    else:
+        nt, nz, ny, nx = shape
+        f = fi.Woven(nx, ny, nt, L=15.0, sigma=0.02, nz=nz).generate()
+    assert mesh_pair(ftk, oracle_lib, f, 26, c) > 0
+
+
+@pytest.mark.parametrize("shape,seed", [((4, 5, 6, 7), 0), ((5, 9, 131), 1)])
+def test_mesh_degenerate(ftk, oracle_lib, shape, seed):
+    gen = torch.Generator().manual_seed(seed)
+    v = torch.tensor([-1.0, 0.0, 1.0])[torch.randint(0, 3, shape, generator=gen)].to(torch.float32)
+    mesh_pair(ftk, oracle_lib, v, 0, 0.0)
+
+
+def test_mesh_capacity_retry(ftk, oracle_lib):
+    """a too-small element buffer reports FTK_ERR_CAPACITY with the count; the binding retries"""
+    import ctypes
+    f = fi.Woven(40, 30, 5, L=15.0).generate().cuda()
+    rec, el = ftk.iso_track(f, 26, 0.2, mesh=True, capacity=1 << 16)
+    desc = ftk.make_desc(tuple(f.shape), f.dtype, 26)
+    buf = ftk.Buffers.allocate(desc, 1 << 16, f.device)
+    small = torch.empty((4, 3), dtype=torch.int64, device="cuda")
+    n_out, n_el = ctypes.c_int64(0), ctypes.c_int64(0)
+    st = ftk.lib().ftk_iso_track_mesh(ctypes.byref(desc), ctypes.c_double(0.2), ctypes.c_void_p(f.data_ptr()),
+                                      ctypes.c_void_p(buf.records.data_ptr()), buf.capacity, ctypes.byref(n_out),
+                                      ctypes.c_void_p(small.data_ptr()), 4, ctypes.byref(n_el),
+                                      ctypes.c_void_p(buf.workspace.data_ptr()), buf.workspace.numel(), None)
+    assert st == ftk.ERR_CAPACITY and n_el.value == el.shape[0] > 4
