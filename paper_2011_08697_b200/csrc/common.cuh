@@ -8,6 +8,28 @@
 
 #include "../../include/ftk_cp.h"
 
+// Debug builds (-DFTK_CHECKS=1, paper_2011_08697_b200/build.py variant "checks"): device-side bounds
+// and protocol assertions -- the stand-in for compute-sanitizer, which this pool does not run.  A failed
+// check prints its location and traps (the call returns FTK_ERR_CUDA).  Compiled out otherwise.
+#ifndef FTK_CHECKS
+#define FTK_CHECKS 0
+#endif
+#if FTK_CHECKS
+#include <cstdio>
+#define FTK_ASSERT(cond)                                                                              \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("FTK_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, blockIdx.x, \
+             threadIdx.x);                                                                            \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define FTK_ASSERT(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace ftk {
 
 using i64 = long long;

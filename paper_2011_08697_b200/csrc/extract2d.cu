@@ -638,6 +638,7 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
   bb.lp[lane] = lp;
   bb.pm[lane] = pmask;
   bb.rs[lane] = rstart;
+  FTK_ASSERT(total <= MAXITEMS && rstart + cnt <= total);
   {
     int pos = rstart;
     for (uint32_t pm = pmask; pm; pm &= pm - 1) bb.items[pos++] = (uint16_t)(lane | ((__ffs(pm) - 1) << 5));
@@ -665,6 +666,7 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
   for (int i = lane; i < total; i += 32) {
     const int it = bb.items[i];
     const int le = it & 31, ty = it >> 5;
+    FTK_ASSERT(ty < 12 && ((bb.pm[le] >> ty) & 1u) && bb.qt[le] != -1);
     const int lqt = bb.qt[le];
     const Win<T> w2{bb.ring + le * ws_words<T>(), ((lqt >> 30) & 1) != 0, G.scale_f, G.scale};
     const unsigned long long slot = obase + i;
@@ -774,6 +776,7 @@ __device__ __forceinline__ void scan_plane_f32(const float* S, const ScanCtx& c,
   const int hcol = lane0 ? XOFF - 1 : XOFF + LX;
   auto load = [&](int i, float4& v, float& l, float& r) {
     const int row = c.srow0 - 1 + i;
+    FTK_ASSERT(row >= 0 && row < ROWS);
     v = *reinterpret_cast<const float4*>(S + row * PITCH + XOFF + 4 * c.lane);
     const float h = S[row * PITCH + hcol];  // tile halo (used by lanes 0 and 31)
     const float up = __shfl_up_sync(0xffffffffu, v.w, 1);
@@ -1068,6 +1071,7 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
     int gk = 0;
     int x0 = -1, y0 = -1;
     int mode = 0;
+    int chk_k = -1, chk_p = -1;  // FTK_CHECKS: the previous plane of the item
     ScanCtx sc;
     sc.srow0 = srow0;
     sc.lane = lane;
@@ -1086,6 +1090,11 @@ __global__ void __launch_bounds__(NTHREADS, FTK_K1_MINB)
       pf.lap(PF_WFULL);
       const StageMeta m = sm.meta[s];
       if (m.done) break;
+      // protocol: within a work item the planes arrive in order (a stage refilled too early shows here)
+      FTK_ASSERT(m.k == 0 || (m.k == chk_k + 1 && m.p == chk_p + 1));
+      FTK_ASSERT(m.k < m.nplanes && m.x0 >= 0 && m.y0 >= 0);
+      chk_k = m.k;
+      chk_p = m.p;
       if (m.k == 0) {
         x0 = m.x0;
         y0 = m.y0;

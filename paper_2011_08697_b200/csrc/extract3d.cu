@@ -36,43 +36,17 @@ constexpr int CHUNK3 = 32;                      // survivor-list entries a warp 
 __constant__ KuhnTables<4> cK4 = kKuhn4;
 
 // ------------------------------------------------------------------------------ SoS, 3x3
-// Partial permutations of a 3x3 matrix: the epsilon-monomials prod_{r in R} eps_{r, sigma(r)} of
-// det(M + E), eps_{r,j} = eps^(2^(3r + j)); sorted by exponent = decreasing magnitude.  The empty
-// sigma (the determinant itself) comes first; a full permutation has coefficient +-1.
+// The epsilon-monomials of det(M + E), eps_{r,j} = eps^(2^(3r + j)) (R4), in decreasing
+// magnitude (increasing exponent): per term, for each row r the perturbed column or -1.  A literal
+// table, derived by tools/derive_sos3.py from the Leibniz expansion of det(M + E) (every permutation x
+// every choice of perturbed rows, monomials collected by exponent); tests/test_sos3_table.py checks it
+// against that derivation and the oracle's own order.  Term 0 is the determinant itself; a term's
+// coefficient is the signed complementary minor.
 struct PP3 {
   int n;
   int8_t col[34][3];
 };
-constexpr PP3 make_pp3() {
-  PP3 t{};
-  int keys[34] = {};
-  int n = 0;
-  for (int code = 0; code < 64; ++code) {
-    int c[3] = {code % 4 - 1, (code / 4) % 4 - 1, (code / 16) % 4 - 1};
-    bool ok = true;
-    int key = 0;
-    for (int r = 0; r < 3 && ok; ++r)
-      if (c[r] >= 0) {
-        for (int q = 0; q < r; ++q)
-          if (c[q] == c[r]) ok = false;
-        key |= 1 << (3 * r + c[r]);
-      }
-    if (!ok) continue;
-    int pos = n;  // insertion sort by key
-    while (pos > 0 && keys[pos - 1] > key) {
-      keys[pos] = keys[pos - 1];
-      for (int r = 0; r < 3; ++r) t.col[pos][r] = t.col[pos - 1][r];
-      --pos;
-    }
-    keys[pos] = key;
-    for (int r = 0; r < 3; ++r) t.col[pos][r] = (int8_t)c[r];
-    ++n;
-  }
-  t.n = n;
-  return t;
-}
-__constant__ PP3 cPP3 = make_pp3();
-static_assert(make_pp3().n == 34, "34 monomials for 3x3");
+__constant__ PP3 cPP3 = {34, {{-1, -1, -1}, {0, -1, -1}, {1, -1, -1}, {2, -1, -1}, {-1, 0, -1}, {1, 0, -1}, {2, 0, -1}, {-1, 1, -1}, {0, 1, -1}, {2, 1, -1}, {-1, 2, -1}, {0, 2, -1}, {1, 2, -1}, {-1, -1, 0}, {1, -1, 0}, {2, -1, 0}, {-1, 1, 0}, {2, 1, 0}, {-1, 2, 0}, {1, 2, 0}, {-1, -1, 1}, {0, -1, 1}, {2, -1, 1}, {-1, 0, 1}, {2, 0, 1}, {-1, 2, 1}, {0, 2, 1}, {-1, -1, 2}, {0, -1, 2}, {1, -1, 2}, {-1, 0, 2}, {1, 0, 2}, {-1, 1, 2}, {0, 1, 2}}};
 
 // the same determinant when every entry is below 2^31 in magnitude: the 2x2 minors are exact in int64
 // (|.| < 2^63) and only the three outer products need 64 x 64 -> 128-bit multiplies
@@ -793,6 +767,7 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
     c.nz = nz;
     int gk = 0, x0 = 0, y0 = 0, z0 = 0;
     int mode = 0;
+    int chk_k = -1, chk_p = -1;  // FTK_CHECKS: the previous plane of the item
     c.xe_out = false;
     c.xe_last = false;
     while (true) {
@@ -800,6 +775,10 @@ __global__ void __launch_bounds__(nthreads<T>(), 1)
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
       const Meta m = sm.meta[s];
       if (m.done) break;
+      // protocol: within a work item the planes arrive in order (a stage refilled too early shows here)
+      FTK_ASSERT(m.k == 0 || (m.k == chk_k + 1 && m.p == chk_p + 1));
+      chk_k = m.k;
+      chk_p = m.p;
       if (m.k == 0) {
         x0 = m.x0;
         y0 = m.y0;

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(THREADS) k_rs_scatter(const unsigned long long
     __syncthreads();
     if (ok) {
       const unsigned int pos = wcnt[w][d] + before_in_warp;
+      FTK_ASSERT(pos < (unsigned long long)n);
       kout[pos] = k;
       vout[pos] = v;
     }

@@ -106,13 +106,24 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
     u64 h = slot_of(P, hm, key);
     // face ids are unique among the records: claim the first empty slot of the probe sequence
-    while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) h = (h + 1) & hm;
+    u64 probes = 0;
+    while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) {
+      h = (h + 1) & hm;
+      FTK_ASSERT(++probes <= hm);  // the table always has an empty slot (1.5 slots per record)
+    }
+    (void)probes;
   }
 }
 
 __device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long long key) {
   u64 h = slot_of(P, hm, key);
+#if FTK_CHECKS
+  u64 probes = 0;
+#endif
   while (true) {
+#if FTK_CHECKS
+    FTK_ASSERT(++probes <= hm + 1);
+#endif
     const int r = P.table[h];
     if (r == EMPTY) return -1;
     if (P.fid[r] == key) return r;
@@ -121,8 +132,14 @@ __device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long l
 }
 
 __device__ __forceinline__ int uf_find(int* parent, int i) {
+#if FTK_CHECKS
+  long long steps = 0;
+#endif
   while (true) {
     const int p = parent[i];
+#if FTK_CHECKS
+    FTK_ASSERT(p >= 0 && ++steps < (1ll << 31));  // a parent cycle would never reach a root
+#endif
     if (p == i) return i;
     const int gp = parent[p];
     if (gp != p) parent[i] = gp;  // path halving; benign race (pointers only move to smaller keys)

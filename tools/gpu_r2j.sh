@@ -1,0 +1,11 @@
+#!/bin/bash
+# round 2, call j: full GPU suite (default build), then the suite on the FTK_CHECKS build (device bounds
+# and protocol assertions; compute-sanitizer is not available on this pool)
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_r2j.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_r2j.log; tail -2 gpurun_out/pytest_r2j.log
+FTK_LIB=$PWD/paper_2011_08697_b200/libftk_cp_checks.so timeout 1500 python -m pytest tests -m gpu -q -p no:randomly > gpurun_out/pytest_checks_r2j.log 2>&1
+echo "checks pytest rc=$?" >> gpurun_out/pytest_checks_r2j.log; tail -2 gpurun_out/pytest_checks_r2j.log
+FTK_LIB=$PWD/paper_2011_08697_b200/libftk_cp_checks.so timeout 600 python tools/sanitize.py > gpurun_out/checks_cases_r2j.log 2>&1
+echo "cases rc=$?" >> gpurun_out/checks_cases_r2j.log; tail -3 gpurun_out/checks_cases_r2j.log
