@@ -315,14 +315,27 @@ __constant__ Cells4 cCells4 = make_cells4();
 // the t-pair with the previous plane's cube codes in registers; a
 // zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte repeat bit 2, so no byte is 1..3).
 namespace s3 {
-constexpr int LX = 128, TX = LX, RW = 8, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
+// r2: 4 anchor rows per tile and a 2-stage ring (41.9 KB stages) fit two CTAs of 10 warps per SM at 96
+// registers; the extra halo rows (7 loaded / 5 coded per 4 anchor rows) are paid for by the doubled
+// occupancy: C5 K1a 1.738 -> 1.730 ms, C3 0.139 -> 0.130 ms (issue-active 52% -> 67%, ALU pipe 65%:
+// the scan is now bound by the ALU pipe's rate, not by latency).  RW = 8 / 3 stages / 1 CTA before.
+#ifndef FTK_S3_RW
+#define FTK_S3_RW 4
+#endif
+#ifndef FTK_S3_NSTAGE
+#define FTK_S3_NSTAGE 2
+#endif
+#ifndef FTK_S3_MINB
+#define FTK_S3_MINB 2
+#endif
+constexpr int LX = 128, TX = LX, RW = FTK_S3_RW, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
 constexpr int ROWS = RW + 3;  // y0-1 .. y0+RW+1
 template <typename T>
 constexpr int nzw() { return sizeof(T) == 4 ? 8 : 4; }  // z-slice warps (owned slices per tile)
 template <typename T>
 constexpr int slices() { return nzw<T>() + 3; }         // z0-1 .. z0+NZW+1
 template <typename T>
-constexpr int nstage() { return sizeof(T) == 4 ? 3 : 2; }
+constexpr int nstage() { return sizeof(T) == 4 ? FTK_S3_NSTAGE : 2; }
 #ifndef FTK_S3_PAIRSYNC
 #define FTK_S3_PAIRSYNC 1  // neighbour-pair mbarriers instead of one named barrier per plane
 #endif
@@ -601,7 +614,7 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
 }
 
 template <typename T, bool TMA>
-__global__ void __launch_bounds__(nthreads<T>(), 1)
+__global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
     k_scan3d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
   constexpr int NZW = nzw<T>(), SL = slices<T>(), NSTAGE = nstage<T>();
   constexpr int PRODUCER = (NZW + 1) * SPLIT;
@@ -1225,12 +1238,11 @@ __global__ void __launch_bounds__(XW3 * 32, FTK_X3_MINB) k_exact3d(const __grid_
             if (k < 2) ends[k] = (long long)(rbase + __popcll(pmask & ((1ull << cd.own[q]) - 1ull)));
             ++k;
           }
-        // upper face (w1, w2, w3, 15): vertices are hypercube corners
-        const i64 gu[4][3] = {{g[cd.w[1]][0], g[cd.w[1]][1], g[cd.w[1]][2]},
-                              {g[cd.w[2]][0], g[cd.w[2]][1], g[cd.w[2]][2]},
-                              {g[cd.w[3]][0], g[cd.w[3]][1], g[cd.w[3]][2]},
-                              {g[15][0], g[15][1], g[15][2]}};
-        if (punctured4(gu, small, mid)) {
+        // upper face (w1, w2, w3, 15), owned by the neighbour hypercube: a cell holds 0 or 2 punctured
+        // faces (SoS), so with k own faces punctured the upper one is punctured iff
+        // k == 1 -- no test needed.  (Were the invariant ever broken, the edge would name a face no
+        // record has and pass 2 reports FTK_ERR_INVARIANT; k > 2 is caught right here.)
+        if (k == 1) {
           if (k < 2) {
             const int a1 = cd.w[1];
             const i64 fx = x + (a1 & 1), fy = y + ((a1 >> 1) & 1), fz = z + ((a1 >> 2) & 1), ft = t + ((a1 >> 3) & 1);
