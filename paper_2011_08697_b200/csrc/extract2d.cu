@@ -116,7 +116,7 @@ constexpr int ws_words() { return sizeof(T) == 4 ? 49 : 66; }  // odd stride for
 constexpr int MAXITEMS = 32 * 12;   // punctured faces per batch (upper bound)
 constexpr int EXW = 8;              // warps per K1b block
 #ifndef FTK_X_MINB
-#define FTK_X_MINB 3
+#define FTK_X_MINB 2                // 128 registers: the prefetched window stays in registers
 #endif
 
 struct BatchBuf {                   // one warp's batch in shared memory
@@ -1238,6 +1238,19 @@ __global__ void __launch_bounds__(256) k_expand2d(const __grid_constant__ Extrac
 // K1b: the exact kernel -- one warp per batch of 32 window-buffer entries (grid-stride, the entry
 // count is read from the device counter K1a left behind)
 // ---------------------------------------------------------------------------------------------
+// window of a cube on the spatial boundary (zero outside the grid), raw values; out of line -- rare,
+// and it keeps the guarded loads out of the kernel's hot code
+template <typename T>
+__device__ __noinline__ void load_window_edge(T* dst, const T* field, i64 t0, const Geo& G, int x, int y, int et) {
+  const T* pa = field + ((i64)(et & 0x3fffffff) - t0) * G.nx * G.ny;
+  const T* pb = et < 0 ? pa + G.nx * G.ny : pa;
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const i64 xx = x - 1 + (k & 3), yy = y - 1 + ((k >> 2) & 3);
+    dst[k] = (xx >= 0 && xx < G.nx && yy >= 0 && yy < G.ny) ? __ldg((k < 16 ? pa : pb) + yy * G.nx + xx) : (T)0;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_constant__ ExtractParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1260,63 +1273,75 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
 #pragma unroll
   for (int i = 0; i < PF_N; ++i) pf.acc[i] = 0;
   pf.start();
-  for (long long b = (long long)blockIdx.x * EXW + w; b < nbat; b += (long long)gridDim.x * EXW) {
+  // Each lane's cube of the batch in flight: its list entry and (interior cubes) its raw 4x4x2 window.
+  // The next batch's loads are issued before this batch's exact stage (fp32), so the window fetch
+  // overlaps the face tests and records instead of stalling the warp.
+  constexpr bool PREFETCH = sizeof(T) == 4;
+  int et = -1, cxv = 0, cyv = 0;
+  bool inner = false;
+  T v[32];
+  auto fetch = [&](long long b) {
     const long long e = b * 32 + lane;
-    const int et = e < nwin ? P.ct[e] : -1;
+    et = e < nwin ? P.ct[e] : -1;
+    inner = false;
+    if (et != -1) {
+      cxv = P.cx[e];
+      cyv = P.cy[e];
+      inner = cxv >= 1 && cxv + 2 < G.nx && cyv >= 1 && cyv + 2 < G.ny;
+      if (inner) {
+        // the cube's 4x4x2 window (planes t and t+1; t again when t+1 is not in the domain)
+        const T* pa = field + ((i64)(et & 0x3fffffff) - P.t0) * G.nx * G.ny + (i64)(cyv - 1) * G.nx + (cxv - 1);
+        const T* pb = et < 0 ? pa + G.nx * G.ny : pa;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = __ldg((k < 16 ? pa : pb) + ((k >> 2) & 3) * G.nx + (k & 3));
+      }
+    }
+  };
+  const long long stride = (long long)gridDim.x * EXW;
+  long long b = (long long)blockIdx.x * EXW + w;
+  if (b < nbat) fetch(b);
+  for (; b < nbat; b += stride) {
     uint32_t* ent = bb.ring + lane * ws_words<T>();
     bool fast = false;
     if (et != -1) {
-      const int x = P.cx[e], y = P.cy[e];
       const bool hasB = et < 0;
-      // the cube's 4x4x2 window (planes t and t+1; t again when t+1 is not in the domain), zero
-      // outside the grid
-      const T* pa = field + ((i64)(et & 0x3fffffff) - P.t0) * G.nx * G.ny;
-      const T* pb = hasB ? pa + G.nx * G.ny : pa;
-      const bool inner = x >= 1 && x + 2 < G.nx && y >= 1 && y + 2 < G.ny;
-      T v[32];
       if (inner) {
-        const T* a0 = pa + (i64)(y - 1) * G.nx + (x - 1);
-        const T* b0 = pb + (i64)(y - 1) * G.nx + (x - 1);
+        if constexpr (sizeof(T) == 4) {
+          float mx = 0.f;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = __ldg((k < 16 ? a0 : b0) + ((k >> 2) & 3) * G.nx + (k & 3));
-      } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const i64 xx = x - 1 + (k & 3), yy = y - 1 + ((k >> 2) & 3);
-          v[k] = (xx >= 0 && xx < G.nx && yy >= 0 && yy < G.ny) ? __ldg((k < 16 ? pa : pb) + yy * G.nx + xx) : (T)0;
+          for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
+          fast = hasB && mx < qmaxf;
         }
-      }
-      if constexpr (sizeof(T) == 4) {
-        float mx = 0.f;
+        if (fast) {
+          int qv[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
-        fast = hasB && inner && mx < qmaxf;
-      }
-      if (fast) {
-        int qv[32];
+          for (int k = 0; k < 32; ++k) {
+            qv[k] = __float2int_rn(__fmul_rn((float)v[k], G.scale_f));  // |v 2^s| < 2^29: exact
+            ent[k] = (uint32_t)qv[k];
+          }
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          qv[k] = __float2int_rn(__fmul_rn((float)v[k], G.scale_f));  // |v 2^s| < 2^29: exact
-          ent[k] = (uint32_t)qv[k];
-        }
+          for (int c = 0; c < 8; ++c) {  // central differences at corner c: window (cx+1, cy+1)
+            const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
+            ent[32 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 1) * 4 + cx + 2] - qv[pl * 16 + (cy + 1) * 4 + cx]);
+            ent[33 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 2) * 4 + cx + 1] - qv[pl * 16 + cy * 4 + cx + 1]);
+          }
+        } else {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // central differences at corner c: window (cx+1, cy+1)
-          const int cx = c & 1, cy = (c >> 1) & 1, pl = c >> 2;
-          ent[32 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 1) * 4 + cx + 2] - qv[pl * 16 + (cy + 1) * 4 + cx]);
-          ent[33 + 2 * c] = (uint32_t)(qv[pl * 16 + (cy + 2) * 4 + cx + 1] - qv[pl * 16 + cy * 4 + cx + 1]);
+          for (int k = 0; k < 32; ++k) reinterpret_cast<T*>(ent)[k] = v[k];
         }
       } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) reinterpret_cast<T*>(ent)[k] = v[k];
+        load_window_edge<T>(reinterpret_cast<T*>(ent), field, P.t0, G, cxv, cyv, et);
       }
-      bb.qx[lane] = x;
-      bb.qy[lane] = y;
+      bb.qx[lane] = cxv;
+      bb.qy[lane] = cyv;
     }
     bb.qt[lane] = et == -1 ? -1 : (et | (fast ? 0x40000000 : 0));
     __syncwarp();
+    if (PREFETCH && b + stride < nbat) fetch(b + stride);
     pf.lap(PF_EXLOAD);
     process_batch<T>(bb, G, P, pf);
     __syncwarp();
+    if (!PREFETCH && b + stride < nbat) fetch(b + stride);
     pf.lap(PF_EXREC);
   }
   if (FTK_K1_PROF && lane == 0) {

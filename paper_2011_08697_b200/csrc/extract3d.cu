@@ -304,49 +304,65 @@ constexpr Cells4 make_cells4() {
 __constant__ Cells4 cCells4 = make_cells4();
 
 // ------------------------------------------------------------------------------ K1a (3D): the scan
-// Persistent, one CTA per SM.  A work item is a 124 x 8 x 8 tile of anchors (x, y, z) times a chunk
-// of TCH anchor timesteps.  Per timestep the producer warp stages the 136 x 11 x 11 halo box
-// (x0-4.., y0-1.., z0-1..) with one 4D TMA load into an NSTAGE3-deep ring.  Scan warp w < 8 owns
-// z-slice z0 + w (8 rows, rolled through a 3-row register window as in 2D, plus the slices z +- 1 of
-// the centre row for dz); warp 8 computes the squares of slice z0 + 8 only.  Per vertex a 6-bit
-// "strict sign holds" code (dx > thr, dx < -thr, dy.., dz..) in the top of a byte; ANDed over the
-// y-pair and x-pair in registers, over the z-pair through a double-buffered shared exchange (per
-// neighbour pair: slice w's warp waits only for slice w + 1's squares, xfull / xempty mbarriers), over
-// the t-pair with the previous plane's cube codes in registers; a
-// zero byte is a survivor (the exact zero-byte test holds: the two low bits of every byte repeat bit 2, so no byte is 1..3).
+// Persistent, two CTAs per SM.  A work item is a 128 x RW x 8 tile of anchors (x, y, z) times a chunk
+// of TCH anchor timesteps.  Per timestep the producer warp stages the 136 x (RW + 3) x 11 halo box
+// (x0-4.., y0-1.., z0-1..) with one 4D TMA load into an NSTAGE-deep ring.  Scan warp w owns the
+// hypercubes anchored at slice z0 + w (RW rows x 128 columns; lane = 4 consecutive x).
+//
+// Region test first (r2): a hypercube can hold a punctured face only if no gradient component keeps
+// one strict sign on its 16 corners; so if dz > thr (or dz < -thr) on EVERY vertex of the warp's
+// region -- slices z and z + 1, rows y0 .. y0 + RW, columns x0 .. x0 + 128 -- on both planes of a
+// plane pair, every hypercube of the warp is rejected for that pair.  The test is a min / max of dz
+// over the region (FMNMX3), per plane; the per-vertex codes below are computed only for the pairs it
+// does not reject (smooth fields: most of them are).  It rejects nothing the per-vertex codes would
+// keep and keeps nothing they would reject (the same fp32 dz and the same strict comparison), so the
+// survivor set is unchanged.  A plane's stage is held until the next plane of the item has been
+// tested, so its codes can still be computed when the following pair needs them.
+//
+// Per-vertex codes (the pairs the region test keeps): per vertex a 6-bit "strict sign holds" code
+// (dx > thr, dx < -thr, dy.., dz..) in the top of a byte, ANDed over the y-pair and x-pair in
+// registers (slice_squares), over the z-pair by computing slice z + 1's squares in the same warp, over
+// the t-pair with the previous plane's cube codes; a zero byte is a survivor (the exact zero-byte test
+// holds: the two low bits of every byte repeat bit 2, so no byte is 1..3).
 namespace s3 {
-// r2: 4 anchor rows per tile and a 2-stage ring (41.9 KB stages) fit two CTAs of 10 warps per SM at 96
-// registers; the extra halo rows (7 loaded / 5 coded per 4 anchor rows) are paid for by the doubled
-// occupancy: C5 K1a 1.738 -> 1.730 ms, C3 0.139 -> 0.130 ms (issue-active 52% -> 67%, ALU pipe 65%:
-// the scan is now bound by the ALU pipe's rate, not by latency).  RW = 8 / 3 stages / 1 CTA before.
 #ifndef FTK_S3_RW
-#define FTK_S3_RW 4
+#define FTK_S3_RW 8
 #endif
 #ifndef FTK_S3_NSTAGE
-#define FTK_S3_NSTAGE 2
+#define FTK_S3_NSTAGE 3
 #endif
 #ifndef FTK_S3_MINB
-#define FTK_S3_MINB 2
+#define FTK_S3_MINB 1
+#endif
+#ifndef FTK_S3_COUNT
+#define FTK_S3_COUNT 0   // experiment builds: region-test statistics in counters[CNT_PROF..]
+#endif
+#ifndef FTK_S3_NOCODES
+#define FTK_S3_NOCODES 0  // experiment builds: skip the per-vertex codes (timing floor; results invalid)
+#endif
+#ifndef FTK_S3_REGION
+#define FTK_S3_REGION 1  // region-first dz test (0: per-vertex codes for every plane pair)
+#endif
+#ifndef FTK_S3_SPLIT
+#define FTK_S3_SPLIT 1   // scan warps per z-slice (each owns RW / SPLIT anchor rows); 2 measured slower
+#endif
+#ifndef FTK_S3_TP
+#define FTK_S3_TP 2      // squares tasks per slice (each RW / TP code rows): finer load balance
 #endif
 constexpr int LX = 128, TX = LX, RW = FTK_S3_RW, XOFF = 4, PITCH = LX + 8;  // tiles own all 128 columns
 constexpr int ROWS = RW + 3;  // y0-1 .. y0+RW+1
+constexpr int SPLIT = FTK_S3_SPLIT, NR = RW / SPLIT;  // NR: anchor rows of one scan warp
+constexpr int TP = FTK_S3_TP, NRT = RW / TP;           // NRT: code rows of one squares task
+static_assert(RW % SPLIT == 0 && RW % TP == 0 && NR % NRT == 0, "SPLIT, TP divide RW; tasks within a warp's rows");
+static_assert(TP * 9 <= 64, "task masks are 64-bit");
 template <typename T>
 constexpr int nzw() { return sizeof(T) == 4 ? 8 : 4; }  // z-slice warps (owned slices per tile)
 template <typename T>
 constexpr int slices() { return nzw<T>() + 3; }         // z0-1 .. z0+NZW+1
 template <typename T>
 constexpr int nstage() { return sizeof(T) == 4 ? FTK_S3_NSTAGE : 2; }
-#ifndef FTK_S3_PAIRSYNC
-#define FTK_S3_PAIRSYNC 1  // neighbour-pair mbarriers instead of one named barrier per plane
-#endif
-#ifndef FTK_S3_SPLIT
-#define FTK_S3_SPLIT 1  // 2 (16 + 2 scan warps of 4 code rows) on C5: K1a 1.885 -> 1.872 ms with the named barrier, 1.737 -> 1.759 ms with pair sync; kept at 1
-#endif
-constexpr int SPLIT = FTK_S3_SPLIT;  // warps per z-slice (each owns RW / SPLIT code-row pairs)
-constexpr int RWW = RW / SPLIT;
-static_assert(RW % SPLIT == 0, "SPLIT divides RW");
 template <typename T>
-constexpr int nthreads() { return ((nzw<T>() + 1) * SPLIT + 1) * 32; }  // NZW + 1 slices x SPLIT warps + producer
+constexpr int nthreads() { return (nzw<T>() * SPLIT + 1) * 32; }  // NZW x SPLIT scan warps + producer
 template <typename T>
 constexpr int stage_elems() { return (PITCH * ROWS * slices<T>() * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T); }
 constexpr uint32_t NEUTRAL = 0xFCFCFCFCu;
@@ -360,9 +376,10 @@ template <typename T>
 struct alignas(128) Smem {
   static constexpr int NSTAGE = nstage<T>(), NZW = nzw<T>();
   T plane[NSTAGE][stage_elems<T>()];
-  uint32_t xch[2][NZW + 1][RW][32];  // per plane parity: squares of every slice
-  uint64_t xfull[2][NZW + 1];         // FTK_S3_PAIRSYNC: slice w's squares of this parity are written
-  uint64_t xempty[2][NZW + 1];        // ... and were read by the warp of slice w - 1
+  uint32_t sq[2][NZW + 1][RW][32];  // per plane parity: the squares of every slice computed this plane
+  unsigned long long need[3][2];     // per plane (gk mod 3): squares tasks of this plane / the previous
+                                     // plane that are needed (bit TP j + h: slice z0 + j, rows of part h)
+  unsigned long long have[2];        // per plane parity: squares tasks whose results are in sq
   Meta meta[NSTAGE];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
@@ -613,11 +630,82 @@ __device__ __forceinline__ void slice_squares(const T* S, int zstride, const Ctx
   }
 }
 
+// Warp-region dz test of one plane (fp32; MODE 0 / 1: y and z interior, so every dz of the region is
+// the central difference): returns bit 1 when dz > thr on every vertex of the warp's region -- slices
+// z and z + 1, code rows 0 .. RW, columns x0 .. x0 + 128, out-of-grid columns excluded -- and bit 0 when
+// dz < -thr on every one (the same fp32 dz and strict comparisons as the per-vertex codes).  Also tracks
+// max |f| over the warp's owned vertices.  S: slice z - 1, row y0 of the stage.
+template <int MODE>
+__device__ __forceinline__ uint32_t region_dz(const float* S, const Ctx& c, float thr, f2 nan01, f2 nan23,
+                                              uint32_t& maxb) {
+  constexpr int ZS = PITCH * ROWS;
+  float mn = __int_as_float(0x7f800000), mx = __int_as_float(0xff800000);  // +inf, -inf
+#pragma unroll
+  for (int k = 0; k <= NR; ++k) {
+    const float* p = S + k * PITCH + XOFF + 4 * c.lane;
+    const float4 a0 = *reinterpret_cast<const float4*>(p);
+    const float4 a1 = *reinterpret_cast<const float4*>(p + ZS);
+    const float4 a2 = *reinterpret_cast<const float4*>(p + 2 * ZS);
+    const float4 a3 = *reinterpret_cast<const float4*>(p + 3 * ZS);
+    if (k < NR) maxb = max_abs_bits(maxb, a1.x, a1.y, a1.z, a1.w);
+    f2 d0 = sub2(pack2(a2.x, a2.y), pack2(a0.x, a0.y));  // dz at slice z, positions 0, 1
+    f2 d1 = sub2(pack2(a2.z, a2.w), pack2(a0.z, a0.w));  //                 positions 2, 3
+    f2 e0 = sub2(pack2(a3.x, a3.y), pack2(a1.x, a1.y));  // dz at slice z + 1
+    f2 e1 = sub2(pack2(a3.z, a3.w), pack2(a1.z, a1.w));
+    if (MODE == 1) {  // out-of-grid positions become NaN: neutral for fminf / fmaxf
+      d0 = add2(d0, nan01);
+      d1 = add2(d1, nan23);
+      e0 = add2(e0, nan01);
+      e1 = add2(e1, nan23);
+    }
+    mn = fminf(fminf(mn, __uint_as_float(lo32(d0))), __uint_as_float(hi32(d0)));
+    mx = fmaxf(fmaxf(mx, __uint_as_float(lo32(d0))), __uint_as_float(hi32(d0)));
+    mn = fminf(fminf(mn, __uint_as_float(lo32(d1))), __uint_as_float(hi32(d1)));
+    mx = fmaxf(fmaxf(mx, __uint_as_float(lo32(d1))), __uint_as_float(hi32(d1)));
+    mn = fminf(fminf(mn, __uint_as_float(lo32(e0))), __uint_as_float(hi32(e0)));
+    mx = fmaxf(fmaxf(mx, __uint_as_float(lo32(e0))), __uint_as_float(hi32(e0)));
+    mn = fminf(fminf(mn, __uint_as_float(lo32(e1))), __uint_as_float(hi32(e1)));
+    mx = fmaxf(fmaxf(mx, __uint_as_float(lo32(e1))), __uint_as_float(hi32(e1)));
+  }
+  // column x0 + 128 (the next tile's first column: the x + 1 corners of lane 31's hypercubes), rows
+  // 0 .. RW of slices z - 1 .. z + 2: lane 4 k + j holds row k of slice z - 1 + j, dz from lane + 2
+  {
+    const int k = c.lane >> 2, j = c.lane & 3;
+    const float v = c.lane < 4 * (NR + 1) ? S[j * ZS + k * PITCH + XOFF + LX] : 0.f;
+    const float w = __shfl_down_sync(0xffffffffu, v, 2);
+    const bool ok = c.lane < 4 * (NR + 1) && j < 2 && !c.xe_out;
+    const float d = ok ? __fsub_rn(w, v) : __int_as_float(0x7fc00000);
+    mn = fminf(mn, d);
+    mx = fmaxf(mx, d);
+  }
+  return (__all_sync(0xffffffffu, mn > thr) ? 2u : 0u) | (__all_sync(0xffffffffu, mx < -thr) ? 1u : 0u);
+}
+
+// max |f| over the warp's owned vertices of a plane (slice z, rows y0 .. y0 + RW - 1; positions outside
+// the grid are zero-filled by the loaders); S: slice z, row y0 of the stage
+template <typename T>
+__device__ __forceinline__ void owned_max(const T* S, int lane, uint32_t& maxb, double& maxd) {
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const T* p = S + k * PITCH + XOFF + 4 * lane;
+    if constexpr (sizeof(T) == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p);
+      maxb = max_abs_bits(maxb, v.x, v.y, v.z, v.w);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double a = fabs(p[q]);
+        maxd = (a != a || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, a);
+      }
+    }
+  }
+}
+
 template <typename T, bool TMA>
 __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
     k_scan3d(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ExtractParams P) {
   constexpr int NZW = nzw<T>(), SL = slices<T>(), NSTAGE = nstage<T>();
-  constexpr int PRODUCER = (NZW + 1) * SPLIT;
+  constexpr int PRODUCER = NZW * SPLIT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const uint32_t mis = smem_u32(smem_raw) & 127u;
   Smem<T>& sm = *reinterpret_cast<Smem<T>*>(smem_raw + (mis ? 128 - mis : 0));
@@ -625,19 +713,18 @@ __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
   const i64 nx = P.nx, ny = P.ny, nz = P.nz;
   constexpr uint32_t STAGE_BYTES = PITCH * ROWS * SL * sizeof(T);
   const int ntx = (int)((nx + TX - 1) / TX), nty = (int)((ny + RW - 1) / RW), ntz = (int)((nz + NZW - 1) / NZW);
-  const int ntc = (int)((P.tb - P.ta + TCH - 1) / TCH);
+  const int tch = (int)P.tchunk;  // anchor timesteps per work item (set by the launcher)
+  const int ntc = (int)((P.tb - P.ta + tch - 1) / tch);
   const long long nitems = (long long)ntx * nty * ntz * ntc;
   if (tid == 0) {
     sm.surv = 0;
     sm.maxbits32 = 0;
     sm.maxbits64 = 0;
+    for (int i = 0; i < 3; ++i) sm.need[i][0] = sm.need[i][1] = 0ull;
+    sm.have[0] = sm.have[1] = 0ull;
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], (NZW + 1) * SPLIT);
-    }
-    for (int i = 0; i < 2 * (NZW + 1); ++i) {
-      mbar_init(&sm.xfull[0][0] + i, SPLIT * 32);  // every lane arrives (release of its own accesses)
-      mbar_init(&sm.xempty[0][0] + i, SPLIT * 32);
+      mbar_init(&sm.empty[s], NZW * SPLIT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -656,8 +743,8 @@ __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
       const int ty_ = (int)(r % nty); r /= nty;
       const int tz = (int)(r % ntz); r /= ntz;
       const i64 x0 = (i64)tx * TX, y0 = (i64)ty_ * RW, z0 = (i64)tz * NZW;
-      const i64 ta = P.ta + r * TCH;
-      const i64 tb = min(ta + TCH, P.tb);
+      const i64 ta = P.ta + r * tch;
+      const i64 tb = min(ta + tch, P.tb);
       const i64 plast = min(tb, P.nt_global - 1);
       const int np = (int)(plast - ta + 1);
       for (int k = 0; k < np; ++k, ++gk) {
@@ -698,18 +785,16 @@ __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
       mbar_arrive(&sm.full[s]);
     }
   } else {
-    // scan warps: warp w owns slice z0 + w / SPLIT, code-row pairs r0 .. r0 + RWW - 1 (r0 = (w % SPLIT) *
-    // RWW); slice NZW is the top slice (squares only)
-    const int slice = warp / SPLIT, r0 = (warp % SPLIT) * RWW;
+    // scan warps: warp w owns the hypercubes anchored at slice z0 + w / SPLIT, rows y0 + r0 .. y0 + r0 +
+    // NR - 1 (r0 = NR (w % SPLIT))
+    const int slice = warp / SPLIT, part = warp % SPLIT, r0 = part * NR;
     const T thr = (T)P.thr;
     const f2 thr2 = pack2((float)P.thr, (float)P.thr);
     const f2 nthr2 = pack2(-(float)P.thr, -(float)P.thr);
     uint32_t maxb32 = 0;
     double maxd = 0.0;
     unsigned long long mysurv = 0;
-    uint32_t prevK[RWW];
     long long cur = 0, end = 0;
-    const bool top = slice == NZW;
     const uint32_t lt_mask = (1u << lane) - 1u;
     auto enqueue = [&](uint32_t mask, int tflag, int x0, int y0, int z) {
       const uint32_t bal = __ballot_sync(0xffffffffu, mask != 0);
@@ -774,15 +859,40 @@ __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
         mysurv += n;
       }
     };
-    Ctx c;
+    Ctx c;  // slice z0 + slice (the warp's own; region test and enqueue)
     c.lane = lane;
     c.ny = ny;
     c.nz = nz;
     int gk = 0, x0 = 0, y0 = 0, z0 = 0;
     int mode = 0;
+    bool xedge = false, yedge = false;
     int chk_k = -1, chk_p = -1;  // FTK_CHECKS: the previous plane of the item
     c.xe_out = false;
     c.xe_last = false;
+    f2 nan01 = pack2(0.f, 0.f), nan23 = nan01;  // NaN on the lane's out-of-grid positions (region test)
+    int prev_s = -1;     // stage of the previous plane of the item (held until this plane is done)
+    uint32_t prevR = 0;  // region code of the previous plane
+    auto survivors_of = [&](const uint32_t* Q) {
+      uint32_t mask = 0;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
+      return mask;
+    };
+    // squares of task part h (rows NRT h ..) of slice z0 + j of the plane in stage st into sq[par][j]
+    auto squares_task = [&](int st, int j, int h, int par) {
+      Ctx cj = c;
+      cj.gz = z0 + j;
+      cj.gy0 = y0 + h * NRT;
+      const bool zedge = cj.gz < 1 || cj.gz + 1 >= nz;
+      const int md = (yedge || zedge) ? 2 : (xedge ? 1 : 0);
+      const T* S = sm.plane[st] + (j + 1) * (PITCH * ROWS) + h * NRT * PITCH;  // slice z0 + j, row y0 + NRT h - 1
+      uint32_t Sq[NRT];
+      if (md == 2) slice_squares<T, 2, NRT>(S, PITCH * ROWS, cj, thr2, nthr2, thr, Sq, maxb32, maxd, false);
+      else if (md == 1) slice_squares<T, 1, NRT>(S, PITCH * ROWS, cj, thr2, nthr2, thr, Sq, maxb32, maxd, false);
+      else slice_squares<T, 0, NRT>(S, PITCH * ROWS, cj, thr2, nthr2, thr, Sq, maxb32, maxd, false);
+#pragma unroll
+      for (int r = 0; r < NRT; ++r) sm.sq[par][j][h * NRT + r][lane] = Sq[r];
+    };
     while (true) {
       const int s = gk % NSTAGE;
       mbar_wait(&sm.full[s], (uint32_t)((gk / NSTAGE) & 1), 3, gk, FTK_K1_MBSLEEP);
@@ -802,58 +912,94 @@ __global__ void __launch_bounds__(nthreads<T>(), FTK_S3_MINB)
         c.lpat = gx == 0;
         c.rpos = (nx - 1 >= gx && nx - 1 <= gx + 3) ? (int)(nx - 1 - gx) : -1;
         c.oob = 0;
+        float nanv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (gx + i >= nx) c.oob |= 0xFCu << (8 * i);
-        const bool xedge = x0 < 1 || x0 + LX + 2 > nx;
-        const bool yzedge = y0 < 1 || y0 + RW + 2 > ny || c.gz < 1 || c.gz + 1 >= nz;
-        mode = yzedge ? 2 : (xedge ? 1 : 0);
+        for (int i = 0; i < 4; ++i) {
+          const bool out = gx + i >= nx;
+          if (out) c.oob |= 0xFCu << (8 * i);
+          nanv[i] = out ? __int_as_float(0x7fc00000) : 0.f;
+        }
+        nan01 = pack2(nanv[0], nanv[1]);
+        nan23 = pack2(nanv[2], nanv[3]);
+        xedge = x0 < 1 || x0 + LX + 2 > nx;
+        yedge = y0 < 1 || y0 + RW + 2 > ny;
+        // region test: both slices of the warp's hypercubes (z, z + 1) z-interior (central dz)
+        const bool zedge = c.gz < 1 || c.gz + 2 >= nz;
+        mode = (yedge || zedge) ? 2 : (xedge ? 1 : 0);
         c.xe_out = x0 + LX >= nx;
         c.xe_last = x0 + LX == nx - 1;
+        prevR = 0;
       }
-      const T* S = sm.plane[s] + (slice + 1) * (PITCH * ROWS) + r0 * PITCH;  // slice z0 + slice, row y0 + r0 - 1
-      uint32_t Sq[RWW];
-      if (mode == 2) slice_squares<T, 2, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      else if (mode == 1) slice_squares<T, 1, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      else slice_squares<T, 0, RWW>(S, PITCH * ROWS, c, thr2, nthr2, thr, Sq, maxb32, maxd, !top);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s]);  // the plane is no longer needed by this warp
       const int par = gk & 1;
-      if (FTK_S3_PAIRSYNC && slice > 0 && gk >= 2)  // slice - 1's warp has read this buffer (plane gk - 2)
-        mbar_wait_sleep(&sm.xempty[par][slice], (uint32_t)(((gk >> 1) - 1) & 1), 5, gk);
-#pragma unroll
-      for (int r = 0; r < RWW; ++r) sm.xch[par][slice][r0 + r][lane] = Sq[r];
-      if (FTK_S3_PAIRSYNC) {
-        mbar_arrive(&sm.xfull[par][slice]);
+      // 1. region test (and the range statistics of the owned vertices)
+      uint32_t R = 0;
+      if (sizeof(T) == 4 && FTK_S3_REGION && mode <= 1) {
+        const float* S = reinterpret_cast<const float*>(sm.plane[s]) + slice * (PITCH * ROWS) + (r0 + 1) * PITCH;  // slice z - 1, row y0 + r0
+        R = mode == 1 ? region_dz<1>(S, c, (float)P.thr, nan01, nan23, maxb32)
+                      : region_dz<0>(S, c, (float)P.thr, nan01, nan23, maxb32);
       } else {
-        asm volatile("bar.sync 1, %0;" ::"r"((NZW + 1) * SPLIT * 32) : "memory");
+        owned_max<T>(sm.plane[s] + (slice + 1) * (PITCH * ROWS) + (r0 + 1) * PITCH, lane, maxb32, maxd);
       }
-      if (!top) {
-        if (FTK_S3_PAIRSYNC) mbar_wait_sleep(&sm.xfull[par][slice + 1], (uint32_t)((gk >> 1) & 1), 6, gk);
-        uint32_t K[RWW];
-#pragma unroll
-        for (int r = 0; r < RWW; ++r) K[r] = Sq[r] & sm.xch[par][slice + 1][r0 + r][lane];  // z-pair
-        if (FTK_S3_PAIRSYNC) mbar_arrive(&sm.xempty[par][slice + 1]);
-        auto survivors_of = [&](const uint32_t* Q) {
-          uint32_t mask = 0;
-#pragma unroll
-          for (int r = 0; r < RWW; ++r) mask |= (((Q[r] - 0x01010101u) & ~Q[r] & 0x80808080u) >> (7 - r));
-          return mask;
-        };
-        const bool inz = z0 + slice < nz;
-        const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
-        if (inz) {
-          if (m.k > 0) {
-            uint32_t Q[RWW];
-#pragma unroll
-            for (int r = 0; r < RWW; ++r) Q[r] = prevK[r] & K[r];
-            enqueue(survivors_of(Q), (int)((uint32_t)(m.p - 1) | 0x80000000u), x0, y0 + r0, z0 + slice);
-          }
-          if (lastg) enqueue(survivors_of(K), m.p, x0, y0 + r0, z0 + slice);
+      const bool inz = z0 + slice < nz;
+      const bool lastg = m.p == P.nt_global - 1 && m.p < m.tb;
+      const bool pair = inz && m.k > 0 && (prevR & R) == 0 && !FTK_S3_NOCODES;  // anchors at p - 1
+      const bool single = inz && lastg && R == 0 && !FTK_S3_NOCODES;           // anchors at p (no t + 1)
+      if (FTK_S3_COUNT && lane == 0 && inz && m.k > 0) {
+        atomicAdd(&P.counters[CNT_PROF + 0], 1ull);                    // plane pairs
+        if (prevR & R) atomicAdd(&P.counters[CNT_PROF + 1], 1ull);    // rejected by the region test
+        if (mode == 2) atomicAdd(&P.counters[CNT_PROF + 3], 1ull);
+      }
+      // 2. the CTA's squares tasks for this plane: slices z, z + 1 of every warp with a pair or single
+      //    (this plane), and of every pair (the previous plane, unless computed there)
+      const int slot = gk % 3;
+      // the task parts covering the warp's rows, of slices z and z + 1
+      const unsigned long long parts = ((1ull << (NR / NRT)) - 1ull) << (r0 / NRT);
+      const unsigned long long mybits = (parts << (TP * slice)) | (parts << (TP * (slice + 1)));
+      if (lane == 0 && (pair || single)) {
+        atomicOr(&sm.need[slot][0], mybits);
+        if (pair) atomicOr(&sm.need[slot][1], mybits);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NZW * SPLIT * 32) : "memory");
+      const unsigned long long needc = sm.need[slot][0];
+      const unsigned long long needp = m.k > 0 ? sm.need[slot][1] & ~sm.have[par ^ 1] : 0ull;
+      // the slot of plane gk + 2 was last read at plane gk - 1, which every warp has left
+      if (warp == 0 && lane == 0) sm.need[(gk + 2) % 3][0] = sm.need[(gk + 2) % 3][1] = 0ull;
+      const int nc = __popcll(needc), ntask = nc + __popcll(needp);
+      if (ntask) {
+        for (int i = warp; i < ntask; i += NZW * SPLIT) {
+          const bool cur_plane = i < nc;
+          unsigned long long mm = cur_plane ? needc : needp;
+          for (int r = cur_plane ? i : i - nc; r > 0; --r) mm &= mm - 1;
+          const int b = __ffsll((long long)mm) - 1;
+          squares_task(cur_plane ? s : prev_s, b / TP, b % TP, cur_plane ? par : par ^ 1);
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(NZW * SPLIT * 32) : "memory");
+        // 3. the owner ANDs the z-pair (and the t-pair) and hands the survivors on
+        if (pair) {
+          uint32_t Q[NR];
 #pragma unroll
-        for (int r = 0; r < RWW; ++r) prevK[r] = K[r];
+          for (int r = 0; r < NR; ++r)
+            Q[r] = sm.sq[par ^ 1][slice][r0 + r][lane] & sm.sq[par ^ 1][slice + 1][r0 + r][lane] &
+                   sm.sq[par][slice][r0 + r][lane] & sm.sq[par][slice + 1][r0 + r][lane];
+          enqueue(survivors_of(Q), (int)((uint32_t)(m.p - 1) | 0x80000000u), x0, y0 + r0, z0 + slice);
+        }
+        if (single) {
+          uint32_t Q[NR];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) Q[r] = sm.sq[par][slice][r0 + r][lane] & sm.sq[par][slice + 1][r0 + r][lane];
+          enqueue(survivors_of(Q), m.p, x0, y0 + r0, z0 + slice);
+        }
+        // (sq[par ^ 1] is rewritten only after the next plane's first barrier, when every warp is
+        // past these reads)
       }
+      if (warp == 0 && lane == 0) sm.have[par] = needc;  // squares of this plane, for the next plane's pairs
+      __syncwarp();
+      if (lane == 0) {
+        if (m.k > 0) mbar_arrive(&sm.empty[prev_s]);         // the previous plane is done with
+        if (m.k == m.nplanes - 1) mbar_arrive(&sm.empty[s]);  // the item's last plane: nothing follows
+      }
+      prev_s = s;
+      prevR = R;
       ++gk;
     }
     for (long long e = cur + lane; e < end; e += 32)
@@ -1364,11 +1510,15 @@ static int launch3_t(const ExtractParams& P, cudaStream_t stream) {
   const sm100::LaunchGeom lg = sm100::launch_geom(kern, nthreads<T>(), smem);
   if (lg.err != cudaSuccess) return set_cuda_error(lg.err, "k_scan3d launch geometry");
   const int sms = lg.sms, per_sm = lg.per_sm;
-  const long long items = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>()) *
-                          ((P.tb - P.ta + TCH - 1) / TCH);
+  const long long tiles = ((P.nx + TX - 1) / TX) * ((P.ny + RW - 1) / RW) * ((P.nz + nzw<T>() - 1) / nzw<T>());
+  const long long slots = (long long)sms * std::max(per_sm, 1);
+  ExtractParams Q = P;
+  Q.tchunk = TCH;  // halved (down to 4) while there would be fewer than 8 work items per CTA: tail balance
+  while (Q.tchunk > 4 && tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk) < 8 * slots) Q.tchunk /= 2;
+  const long long items = tiles * ((P.tb - P.ta + Q.tchunk - 1) / Q.tchunk);
   if (items <= 0) return FTK_OK;
-  const long long grid = std::min<long long>(items, (long long)sms * std::max(per_sm, 1));
-  kern<<<(unsigned)grid, nthreads<T>(), smem, stream>>>(map, P);
+  const long long grid = std::min<long long>(items, slots);
+  kern<<<(unsigned)grid, nthreads<T>(), smem, stream>>>(map, Q);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.ev_mid) FTK_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(P.ev_mid), stream));
   const sm100::LaunchGeom xg = sm100::launch_geom(k_exact3d<T>, XW3 * 32, 0);

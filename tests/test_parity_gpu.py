@@ -277,3 +277,34 @@ def test_x_tile_boundaries_2d(ftk, oracle_lib, nx):
 def test_x_tile_boundaries_3d(ftk, oracle_lib, nx):
     w = fi.Woven(nx, 9, 3, L=15.0, sigma=0.02, nz=10)
     run_pair(ftk, oracle_lib, w.generate(), 26)
+
+
+@pytest.mark.parametrize("shape,sigma", [
+    ((5, 19, 14, 300), 0.0),    # x tile 128..255 is interior (MODE 0): the dz region test rejects most
+    ((4, 19, 14, 300), 0.02),   # warps; the slice through z = 0 (dz = 0 exactly) is never rejected
+    ((4, 21, 13, 261), 0.05),   # x-boundary tiles (MODE 1) with out-of-grid positions and column x0 + 128
+])
+def test_woven3d_region_test_parity(ftk, oracle_lib, shape, sigma):
+    """k_scan3d rejects whole warp regions when dz keeps one strict sign on both planes of a pair; the
+    survivor set must stay that of the per-vertex codes (checked through the oracle's result)."""
+    nt, nz, ny, nx = shape
+    w = fi.Woven(nx, ny, nt, sigma=sigma, nz=nz)
+    _, n = run_pair(ftk, oracle_lib, w.generate(), 26)
+    assert n > 0
+
+
+def test_moving_extremum_3d_region_test(ftk, oracle_lib):
+    """a paraboloid: dz changes sign only near the centre's slice, dx / dy keep one sign far from it"""
+    me = fi.MovingExtremum((300, 12, 20), 5, c0=(200.0, 6.0, 10.0), v=(0.5, 0.25, 0.75))
+    d, n = run_pair(ftk, oracle_lib, me.generate(), me.scale_log2)
+    assert n >= 4
+
+
+@pytest.mark.parametrize("where", [(0, 9, 5, 200), (1, 10, 7, 299), (2, 0, 0, 150), (1, 18, 13, 128), (0, 4, 6, 255)])
+def test_range_error_region_path_3d(ftk, where):
+    """the range statistics of the region-test path (interior tiles) cover every vertex"""
+    f = fi.Woven(300, 14, 3, sigma=0.0, nz=19).generate()
+    f[where] = float("inf") if where[0] == 2 else float("nan")
+    with pytest.raises(ftk.FtkError) as e:
+        ftk.track(f.cuda(), 26)
+    assert e.value.status == ftk.ERR_RANGE

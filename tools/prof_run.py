@@ -17,3 +17,6 @@ for i in range(reps):
     km = ftk.last_kernel_timings()
     print(f'{name} rep {i}: k1 {ms[0]:.3f} ms (k1a {km[0]:.3f} k1b {km[1]:.3f}) pass2 {ms[1]:.3f} ms call {ms[3]:.3f} ms faces {st[0]} survivors {st[1]} punctured {st[2]}')
 torch.cuda.synchronize()
+if '--counters' in sys.argv:
+    c = buf.workspace[:256].view(torch.int64).cpu().tolist()
+    print('counters[16..30]:', c[16:30])

@@ -25,6 +25,24 @@ VARIANTS = {
     "vminb8": ["FTK_V_MINB=8"],
     "jump2": ["FTK_LABEL_JUMP=2"],
     "jump4": ["FTK_LABEL_JUMP=4"],
+    "xcount": ["FTK_X_COUNT=1"],
+    "xru2": ["FTK_X_RUNROLL=2"],
+    "s3r0": ["FTK_S3_REGION=0"],
+    "s3cnt": ["FTK_S3_COUNT=1"],
+    "s3sp1": ["FTK_S3_SPLIT=1"],
+    "s3tp1": ["FTK_S3_TP=1"],
+    "s3tp4": ["FTK_S3_TP=4"],
+    "s3sp2": ["FTK_S3_SPLIT=2"],
+    "s3noc": ["FTK_S3_NOCODES=1"],
+    "s3noc8": ["FTK_S3_NOCODES=1", "FTK_S3_RW=8", "FTK_S3_MINB=1", "FTK_S3_NSTAGE=3"],
+    "s3rw8": ["FTK_S3_RW=8", "FTK_S3_MINB=1", "FTK_S3_NSTAGE=3"],
+    "s3st3": ["FTK_S3_NSTAGE=3", "FTK_S3_MINB=1"],
+    "fprof": ["FTK_K1_PROF=1"],
+    "fprof1": ["FTK_K1_PROF=1", "FTK_F_NXW=1"],
+    "nxw1": ["FTK_F_NXW=1"],
+    "nxw3": ["FTK_F_NXW=3"],
+    "nxw4": ["FTK_F_NXW=4"],
+    "xnopf": ["FTK_X_PREFETCH=0"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
