@@ -53,6 +53,7 @@ enum Counter : int {
   CNT_CUBES = 11,     // 2D: surviving cubes expanded from K1a's group entries (may exceed wcap)
   CNT_WIN_MAX = 12,   // streaming: max of CNT_WIN / CNT_CUBES over the chunks already processed
   CNT_POST = 13,      // post-processing: output records (slice / filter)
+  CNT_HGROUP = 14,    // pass 2: log2 of the hash-table blocks per coarse cell (set with CNT_HMASK)
   CNT_ELEMS = 15,     // isovolume mesh: simplices emitted (may exceed the element capacity)
   CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
   CNT_N = 32

@@ -50,13 +50,26 @@ __device__ __forceinline__ i64 divq(i64 n, i64 d, double inv) {
 }
 
 // Slot of a face id in the pass-2 table: spatially blocked open addressing.  The table is cut into
-// blocks of HBLK slots; a face's block is picked by a hash of its coarse position -- the 128-column x
-// tile, 64 rows (3D: 8 rows x 8 slices) and 32 (3D: 16) timesteps, the grain of K1a's work items, whose
-// records are emitted together -- and the slot inside it by a hash of the face id.  The inserts and
-// lookups of one work item's records and edges (processed in emission order) thus stay within a few
-// blocks that are resident in L2, instead of touching the whole table.  Linear probing continues into
-// the next block on a full block (rare: the table holds 1.5 slots per record).
+// blocks of HBLK slots; a face's block is picked by its coarse position -- the 128-column x tile, 64
+// rows (3D: 8 rows x 8 slices) and 32 (3D: 16) timesteps, the grain of K1a's work items, whose records
+// are emitted together -- and the slot inside it by a hash of the face id.  The inserts and lookups of
+// one work item's records and edges (processed in emission order) thus stay within a few blocks that
+// are resident in L2, instead of touching the whole table.  When the table has more blocks than there
+// are coarse cells (dense records: noisy fields, isovolumes), every coarse cell owns a group of 2^gs
+// consecutive blocks and the face-id hash picks the block within it, so a cell's records spread over
+// as many slots as the table has per cell (gs = 0: one block per cell).  Probing (TProbe) is linear
+// within a block for at most HRUN slots, then jumps to another block of the table, chosen by the key
+// (home + j s, s odd: every block in turn), so a cell with more records than its blocks hold -- records
+// concentrated in a few cells, or the spatially clustered first records of a call whose capacity is
+// too small -- spills into the whole table at its load factor instead of growing one linear cluster.
 constexpr int HBLK_LOG2 = 12;
+constexpr int HRUN = 32;
+__device__ __forceinline__ u64 coarse_cells(const TrackParams& P) {
+  if (P.ndim == 2)
+    return (u64)((P.ext[0] + 127) >> 7) * (u64)((P.ext[1] + 63) >> 6) * (u64)((P.ext[3] + 31) >> 5);
+  return (u64)((P.ext[0] + 127) >> 7) * (u64)((P.ext[1] + 7) >> 3) * (u64)((P.ext[2] + 7) >> 3) *
+         (u64)((P.ext[3] + 15) >> 4);
+}
 __device__ __forceinline__ u64 slot_of(const TrackParams& P, u64 hm, long long key) {
   const u64 h = mix((u64)key);
   if (hm < (1ull << HBLK_LOG2)) return h & hm;
@@ -74,12 +87,46 @@ __device__ __forceinline__ u64 slot_of(const TrackParams& P, u64 hm, long long k
     coarse = (((u64)(t >> 4) * (u64)((P.ext[2] + 7) >> 3) + (u64)(z >> 3)) * (u64)((P.ext[1] + 7) >> 3) + (u64)(y >> 3)) *
                  (u64)((P.ext[0] + 127) >> 7) + (u64)(x >> 7);
   }
-  // consecutive coarse cells take consecutive blocks (modulo the block count): no two cells share a
-  // block while there are at least as many blocks as cells, and then each block holds ~one cell's faces
-  // at the table's load factor; a hashed block choice would collide cells and grow long probe chains
-  const u64 blk = coarse & (hm >> HBLK_LOG2);
+  // consecutive coarse cells take consecutive block groups (modulo the block count): no two cells share
+  // a block while there are at least as many blocks as cells; a hashed group choice would collide cells
+  // and grow long probe chains
+  const int gs = (int)P.counters[CNT_HGROUP];
+  const u64 blk = ((coarse << gs) | ((h >> HBLK_LOG2) & ((1ull << gs) - 1))) & (hm >> HBLK_LOG2);
   return (blk << HBLK_LOG2) | (h & ((1ull << HBLK_LOG2) - 1));
 }
+
+// the probe sequence of a key: slot_of, then HRUN-slot runs in the blocks home + j s
+struct TProbe {
+  u64 hm, h, blk0, stride;
+  int run;
+  long long j;
+  __device__ TProbe(const TrackParams& P, u64 hm_, long long key) : hm(hm_), run(0), j(0) {
+    h = slot_of(P, hm, key);
+    blk0 = h >> HBLK_LOG2;
+    stride = (mix((u64)key ^ 0x5bd1e995ull) >> 20) | 1ull;
+  }
+  __device__ __forceinline__ u64 slot() const { return h; }
+  __device__ __forceinline__ void next() {
+    if (hm < (1ull << HBLK_LOG2) || run < 0) {  // small table (or every block visited): linear probing
+      h = (h + 1) & hm;
+      return;
+    }
+    if (++run < HRUN) {
+      h = (h & ~((1ull << HBLK_LOG2) - 1)) | ((h + 1) & ((1ull << HBLK_LOG2) - 1));
+      return;
+    }
+    run = 0;
+    ++j;
+    const u64 nblk = (hm >> HBLK_LOG2) + 1;
+    if ((u64)j >= nblk) {  // every block visited (cannot happen below full load): linear over the table
+      h = (h + 1) & hm;
+      run = -1;
+      return;
+    }
+    const u64 blk = (blk0 + (u64)j * stride) & (nblk - 1);
+    h = (blk << HBLK_LOG2) | (h & ((1ull << HBLK_LOG2) - 1));
+  }
+};
 
 __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   const i64 n = (i64)P.counters[CNT_NOUT];
@@ -91,7 +138,15 @@ __device__ __forceinline__ u64 table_mask(const TrackParams& P) { return P.count
 
 __global__ void k_clear(const __grid_constant__ TrackParams P) {
   const u64 hm = hash_slots(n_records(P), P.table_cap) - 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[CNT_HMASK] = hm;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.counters[CNT_HMASK] = hm;
+    // blocks per coarse cell: 2^gs, the largest power of two with 2^gs x (cells rounded up to a power of
+    // two) <= blocks
+    const u64 nblk = (hm + 1) >> HBLK_LOG2, nc = coarse_cells(P);
+    int gs = 0;
+    while ((1ull << (gs + 1)) * nc <= nblk) ++gs;
+    P.counters[CNT_HGROUP] = (unsigned long long)gs;
+  }
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= hm; i += (u64)gridDim.x * blockDim.x)
     P.table[i] = EMPTY;
 }
@@ -104,30 +159,30 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
     if (!P.prelinked) P.parent[i] = (int)i;
     // only faces that some cell of a neighbour cube looks up (the "upper" types) need a slot
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
-    u64 h = slot_of(P, hm, key);
+    TProbe pr(P, hm, key);
     // face ids are unique among the records: claim the first empty slot of the probe sequence
     u64 probes = 0;
-    while (atomicCAS(&P.table[h], EMPTY, (int)i) != EMPTY) {
-      h = (h + 1) & hm;
-      FTK_ASSERT(++probes <= hm);  // the table always has an empty slot (1.5 slots per record)
+    while (atomicCAS(&P.table[pr.slot()], EMPTY, (int)i) != EMPTY) {
+      pr.next();
+      FTK_ASSERT(++probes <= 2 * hm + 2);  // the table always has an empty slot (1.5 slots per record)
     }
     (void)probes;
   }
 }
 
 __device__ __forceinline__ long long lookup(const TrackParams& P, u64 hm, long long key) {
-  u64 h = slot_of(P, hm, key);
+  TProbe pr(P, hm, key);
 #if FTK_CHECKS
   u64 probes = 0;
 #endif
   while (true) {
 #if FTK_CHECKS
-    FTK_ASSERT(++probes <= hm + 1);
+    FTK_ASSERT(++probes <= 2 * hm + 2);
 #endif
-    const int r = P.table[h];
+    const int r = P.table[pr.slot()];
     if (r == EMPTY) return -1;
     if (P.fid[r] == key) return r;
-    h = (h + 1) & hm;
+    pr.next();
   }
 }
 

@@ -129,3 +129,12 @@ def test_mesh_capacity_retry(ftk, oracle_lib):
                                       ctypes.c_void_p(small.data_ptr()), 4, ctypes.byref(n_el),
                                       ctypes.c_void_p(buf.workspace.data_ptr()), buf.workspace.numel(), None)
     assert st == ftk.ERR_CAPACITY and n_el.value == el.shape[0] > 4
+
+
+def test_iso_dense_blocked_hash(ftk, oracle_lib):
+    """an isovolume far denser than the critical points the pass-2 table blocks were sized for: every
+    coarse cell must spread over a group of blocks (a single 4096-slot block per cell made the probe
+    chains quadratic -- the C2 isovolume never finished)"""
+    f = fi.Woven(512, 384, 20, sigma=0.0).generate()
+    g, info = run_pair(ftk, oracle_lib, f, 26, 0.5)
+    assert len(g) > 500_000
