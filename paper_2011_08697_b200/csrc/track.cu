@@ -63,7 +63,10 @@ __device__ __forceinline__ i64 divq(i64 n, i64 d, double inv) {
 // concentrated in a few cells, or the spatially clustered first records of a call whose capacity is
 // too small -- spills into the whole table at its load factor instead of growing one linear cluster.
 constexpr int HBLK_LOG2 = 12;
-constexpr int HRUN = 32;
+#ifndef FTK_HRUN
+#define FTK_HRUN 32
+#endif
+constexpr int HRUN = FTK_HRUN;  // slots probed per block before the jump
 __device__ __forceinline__ u64 coarse_cells(const TrackParams& P) {
   if (P.ndim == 2)
     return (u64)((P.ext[0] + 127) >> 7) * (u64)((P.ext[1] + 63) >> 6) * (u64)((P.ext[3] + 31) >> 5);
@@ -98,12 +101,13 @@ __device__ __forceinline__ u64 slot_of(const TrackParams& P, u64 hm, long long k
 // the probe sequence of a key: slot_of, then HRUN-slot runs in the blocks home + j s
 struct TProbe {
   u64 hm, h, blk0, stride;
+  long long key;
   int run;
   long long j;
-  __device__ TProbe(const TrackParams& P, u64 hm_, long long key) : hm(hm_), run(0), j(0) {
+  __device__ TProbe(const TrackParams& P, u64 hm_, long long key_) : hm(hm_), key(key_), run(0), j(0) {
     h = slot_of(P, hm, key);
     blk0 = h >> HBLK_LOG2;
-    stride = (mix((u64)key ^ 0x5bd1e995ull) >> 20) | 1ull;
+    stride = 0;  // computed at the first jump
   }
   __device__ __forceinline__ u64 slot() const { return h; }
   __device__ __forceinline__ void next() {
@@ -123,6 +127,7 @@ struct TProbe {
       run = -1;
       return;
     }
+    if (j == 1) stride = (mix((u64)key ^ 0x5bd1e995ull) >> 20) | 1ull;
     const u64 blk = (blk0 + (u64)j * stride) & (nblk - 1);
     h = (blk << HBLK_LOG2) | (h & ((1ull << HBLK_LOG2) - 1));
   }

@@ -1,18 +1,25 @@
 #!/bin/bash
-# usage: tools/round_final.sh TAG -- GPU box: for C2, C5, V2, V5 a bench line, the launch list of the
-# same bench command and one ncu --set full capture of the scan + exact kernels (each after its plain
-# command exited 0); bench lines for C3, C4
-tag=$1
+# usage: tools/round_final.sh TAG [CONFIG...] -- GPU box: for each of C2, C5, V2, V5 (or the configs
+# given) a bench line, the launch list of the same bench command and one ncu --set full capture of the
+# scan + exact kernels (each after its plain command exited 0); C3 / C4 / ref: bench lines only
+tag=$1; shift
+cfgs=${@:-C2 C5 V2 V5 C3 C4 ref}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv > gpurun_out/box_$tag.txt 2>&1
-for cfg in C2 C5 V2 V5; do
+for cfg in $cfgs; do
   t=${tag}_$(echo $cfg | tr C c | tr V v)
   case $cfg in
+    ref)
+      timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
+      echo "reference rc=$?"; continue;;
+    C3|C4)
+      timeout 1200 python bench.py --config $cfg --steps 20 --warmup 3 > gpurun_out/bench_$t.json 2> gpurun_out/bench_$t.err
+      echo "bench $cfg rc=$?"; continue;;
     C2) re="k_scan2d|k_exact2d";; C5) re="k_scan3d|k_exact3d";;
     V2) re="k_scanvec2d|k_exactvec2d";; V5) re="k_scanvec3d|k_exact3d";;
   esac
   steps=100; [ $cfg = C2 ] || steps=30
-  python bench.py --config $cfg --steps $steps --warmup 5 > gpurun_out/bench_$t.json 2> gpurun_out/bench_$t.err
+  timeout 1200 python bench.py --config $cfg --steps $steps --warmup 5 > gpurun_out/bench_$t.json 2> gpurun_out/bench_$t.err
   rc=$?; echo "bench $cfg rc=$rc"
   if [ $rc -eq 0 ]; then
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv \
@@ -23,10 +30,3 @@ for cfg in C2 C5 V2 V5; do
     echo "ncu full $cfg rc=$?"
   fi
 done
-for cfg in C3 C4; do
-  t=${tag}_$(echo $cfg | tr C c)
-  python bench.py --config $cfg --steps 20 --warmup 3 > gpurun_out/bench_$t.json 2> gpurun_out/bench_$t.err
-  echo "bench $cfg rc=$?"
-done
-python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
-echo "reference rc=$?"

@@ -18,6 +18,8 @@ VARIANTS = {
     "s3tp4": ["FTK_S3_TP=4"],
     "x3m4": ["FTK_X3_MINB=4"],              # k_exact3d occupancy
     "jump2": ["FTK_LABEL_JUMP=2"],          # pointer jumping before k_label
+    "hrun128": ["FTK_HRUN=128"],            # pass-2 hash: slots probed per block before a jump
+    "hrun512": ["FTK_HRUN=512"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
