@@ -1,10 +1,14 @@
 // iso.cu -- isovolume tracking (Alg. 1 right) on the
 // Kuhn spacetime mesh of a 2D+t / 3D+t scalar field.
 //
-// k_iso<D> -- one thread per grid vertex v (D = 3: 2D+t, D = 4: 3D+t), x fastest across the threads:
-//   * the 2^D corners of the cube anchored at v, quantized (q = rint(f 2^s)) minus the quantized
-//     isovalue: g = q - rint(c 2^s);  a cube whose corners all share one SoS sign (g >= 0 counts as
-//     positive, the +eps of the 1D SoS test) holds no crossed edge and no isovolume piece;
+// k_iso_scan<D> -- the sign scan: warp tasks of 32 columns x 8 rows [x one z-slice] x 32 timesteps;
+//   each vertex row is loaded once per task (coalesced) and its signs g >= 0 (g = q - rint(c 2^s), q =
+//   rint(f 2^s); 0 counts as positive, the +eps of the 1D SoS test) are balloted into 32-bit
+//   words; a cube whose 2^D corners share one sign holds no crossed edge, cell crossing, simplex or
+//   link, and is dropped with a few bitwise operations per 32 cubes; the rest (and the cubes on the
+//   grid's last column / row / slice / timestep) go to a candidate list.
+// k_iso_cube<D> -- one thread per candidate cube (warp-uniform loop):
+//   * the 2^D corners, quantized;
 //   * edge pass: the 2^D - 1 edges anchored at v (v -> v + m) whose two signs differ are crossed: one
 //     record each, located by Eq. 2 with n = 1 (mu_a = -g_b / (g_a - g_b), mu_b = g_a / (g_a - g_b),
 //     FP64 without FMA), id = I(v) (2^D - 1) + m - 1, type 1 if g increases along the edge, flags
@@ -94,25 +98,17 @@ __device__ __forceinline__ const Perms<D>& perms() {
   else return cPm4;
 }
 
+// The cube anchored at vertex i (one per lane, `active` lanes only; warp-uniform: the record, link and
+// simplex slots are reserved with one atomic per warp): crossed edges, cells, mesh, links.
 template <typename T, int D>
-__global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractParams P, long long cq) {
+__device__ __forceinline__ void iso_cube(const ExtractParams& P, long long cq, const i64 (&ext)[4], int4 vc, bool active,
+                                      uint32_t& maxb, double& maxd) {
   constexpr int NC = 1 << D, E = NC - 1, NP = D == 3 ? 19 : 65;
-  const i64 ext[4] = {P.nx, P.ny, D == 4 ? P.nz : P.nt_global, P.nt_global};
-  const i64 nv = P.nx * P.ny * P.nz * P.nt_global;
   const T* F = reinterpret_cast<const T*>(P.field);
-  uint32_t maxb = 0;
-  double maxd = 0.0;
   const int lane = threadIdx.x & 31;
-  // warp-uniform loop (the record and link slots are reserved with one atomic per warp)
-  for (i64 base = (i64)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nv; base += (i64)gridDim.x * blockDim.x) {
-    const i64 i = base + lane;
-    const bool active = i < nv;
-    i64 v[4], rem = active ? i : 0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      v[a] = a < D - 1 ? rem % ext[a] : rem;
-      rem = a < D - 1 ? rem / ext[a] : 0;
-    }
+  {
+    // the anchor's coordinates (x, y, [z,] t)
+    const i64 v[4] = {active ? vc.x : 0, active ? vc.y : 0, active ? vc.z : 0, active ? vc.w : 0};
     // corner values
     i64 g[NC];
     uint32_t exist = 0, pos = 0;
@@ -315,15 +311,159 @@ __global__ void __launch_bounds__(256) k_iso(const __grid_constant__ ExtractPara
       ++es;
     }
   }
+}
+
+// sign of g = rint(f 2^s) - rint(c 2^s) >= 0 (the SoS sign of the 1D test), as iso_cube
+// computes it
+template <typename T>
+__device__ __forceinline__ bool iso_pos(T f, double scale, float scale_f, long long cq) {
+  // fp32: f 2^s is exact in fp32 as in FP64, so rint of either is the same integer
+  if constexpr (sizeof(T) == 4) return __float2ll_rn(__fmul_rn(f, scale_f)) >= cq;
+  else return __double2ll_rn(__dmul_rn(f, scale)) >= cq;
+}
+
+// k_iso_scan<D>: warp tasks = 32 columns x RB anchor rows [x one z-slice] x a chunk of TCI timesteps.
+// Per timestep the warp loads the task's vertex rows (coalesced) and ballots their signs into one
+// 32-bit word per row (plus the sign of column x0 + 32); a cube whose corners (x, x + 1 within the
+// words, the row pairs, [the slice pair,] the plane pair) all share one sign holds no crossed edge, no
+// cell crossing, no simplex and no link, and is skipped; the others (and every cube on the grid's last
+// column, row, slice or timestep, whose corners are partly outside) are appended to the candidate list
+// (the survivor-list region: anchors in wx, wy, wz, wt; one atomic per warp and 32-entry chunk) for
+// k_iso_cube.  Every vertex of the grid is loaded here (range statistics).
+constexpr int RB = 8, TCI = 32;
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) k_iso_scan(const __grid_constant__ ExtractParams P, long long cq) {
+  constexpr int NS = D == 4 ? 2 : 1;  // slices per task (z0, z0 + 1)
+  const i64 nx = P.nx, ny = P.ny, nz = D == 4 ? P.nz : 1, nt = P.nt_global;
+  const T* F = reinterpret_cast<const T*>(P.field);
+  const float scale_f = (float)P.scale;
+  uint32_t maxb = 0;
+  double maxd = 0.0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const i64 ntx = (nx + 31) / 32, nty = (ny + RB - 1) / RB, ntc = (nt + TCI - 1) / TCI, ntasks = ntx * nty * nz * ntc;
+  long long cur = 0, end = 0;  // the warp's current chunk of the candidate list
+  for (i64 task = (i64)blockIdx.x * 8 + wid; task < ntasks; task += (i64)gridDim.x * 8) {
+    const i64 tx = task % ntx, ty = (task / ntx) % nty, tz = (task / (ntx * nty)) % nz, tc = task / (ntx * nty * nz);
+    const i64 x0 = tx * 32, y0 = ty * RB, z0 = tz;
+    const i64 x = x0 + lane;
+    // anchor timesteps [tc TCI, min(tc TCI + TCI, nt)): planes up to the chunk end, inclusive
+    const i64 tlo = tc * TCI, thi = min(tlo + TCI, nt - 1);
+    uint32_t Wp[NS][RB + 1], Ep[NS];  // previous plane's row sign words; Ep / Ex: bit r = column x0 + 32
+    for (i64 t = tlo; t <= thi; ++t) {
+      uint32_t W[NS][RB + 1], Ex[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        uint32_t eb = 0;
+#pragma unroll
+        for (int r = 0; r <= RB; ++r) {
+          const i64 y = y0 + r, z = z0 + s;
+          const bool rowin = y < ny && z < nz;
+          const T* row = F + ((t * nz + z) * ny + y) * nx;
+          bool p = false, pe = false;
+          if (rowin && x < nx) {
+            const T f = __ldg(row + x);
+            if constexpr (sizeof(T) == 4) maxb = max(maxb, __float_as_uint(f) & 0x7fffffffu);
+            else {
+              const double a = fabs((double)f);
+              maxd = (a != a || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, a);
+            }
+            p = iso_pos<T>(f, P.scale, scale_f, cq);
+          }
+          if (lane == 0 && rowin && x0 + 32 < nx) pe = iso_pos<T>(__ldg(row + x0 + 32), P.scale, scale_f, cq);
+          W[s][r] = __ballot_sync(0xffffffffu, p);
+          eb |= (pe ? 1u : 0u) << r;
+        }
+        Ex[s] = __shfl_sync(0xffffffffu, eb, 0);
+      }
+      // the cubes anchored at plane t - 1 (both planes), and at t itself when it is the last
+      for (int pass = t > tlo ? 0 : 1; pass < (t == nt - 1 ? 2 : 1); ++pass) {
+        const i64 ta = pass == 0 ? t - 1 : t;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const i64 y = y0 + r;
+          uint32_t band = 0xffffffffu, bor = 0u;
+          auto take = [&](uint32_t w, uint32_t e) {
+            const uint32_t sh = (w >> 1) | (e << 31);
+            band &= w & sh;
+            bor |= w | sh;
+          };
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            take(W[s][r], (Ex[s] >> r) & 1u);
+            take(W[s][r + 1], (Ex[s] >> (r + 1)) & 1u);
+            if (pass == 0) {
+              take(Wp[s][r], (Ep[s] >> r) & 1u);
+              take(Wp[s][r + 1], (Ep[s] >> (r + 1)) & 1u);
+            }
+          }
+          // anchors in the grid; cubes with corners outside it are always candidates
+          const bool anchor = x < nx && y < ny && z0 < nz;
+          const bool edge = x == nx - 1 || y == ny - 1 || (D == 4 && z0 == nz - 1) || ta == nt - 1;
+          const bool cand = anchor && (edge || ((bor & ~band) >> lane & 1u));
+          const uint32_t m = __ballot_sync(0xffffffffu, cand);
+          if (m) {
+            const int n = __popc(m), rank = __popc(m & lt);
+            const int avail = (int)(end - cur);
+            long long e = cur + rank;
+            if (n > avail) {  // the chunk runs out: the rest goes to a fresh one (n <= 32)
+              long long c = 0;
+              if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_WIN], 32ull);
+              c = __shfl_sync(0xffffffffu, c, 0);
+              if (rank >= avail) e = c + (rank - avail);
+              cur = c + (n - avail);
+              end = c + 32;
+            } else {
+              cur += n;
+            }
+            if (cand && e < P.wcap) {
+              P.wx[e] = (int)x;
+              P.wy[e] = (int)y;
+              P.wz[e] = (int)z0;
+              P.wt[e] = (int)ta;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        Ep[s] = Ex[s];
+#pragma unroll
+        for (int r = 0; r <= RB; ++r) Wp[s][r] = W[s][r];
+      }
+    }
+  }
+  for (long long e = cur + lane; e < end; e += 32)  // the unused rest of the warp's chunk: no cube
+    if (e < P.wcap) P.wt[e] = -1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     maxb = max(maxb, __shfl_xor_sync(0xffffffffu, maxb, o));
     const double od = __shfl_xor_sync(0xffffffffu, maxd, o);
     maxd = (od != od || maxd != maxd) ? __longlong_as_double(0x7ff8000000000000ll) : fmax(maxd, od);
   }
-  if ((threadIdx.x & 31) == 0)
+  if (lane == 0)
     atomicMax(&P.counters[CNT_MAXBITS],
               sizeof(T) == 4 ? (unsigned long long)maxb : (unsigned long long)__double_as_longlong(maxd));
+}
+
+// k_iso_cube<D>: the candidate cubes, one per thread (warp-uniform loop: the record, link and simplex
+// slots are reserved with one atomic per warp)
+template <typename T, int D>
+__global__ void __launch_bounds__(256) k_iso_cube(const __grid_constant__ ExtractParams P, long long cq) {
+  const i64 ext[4] = {P.nx, P.ny, D == 4 ? P.nz : P.nt_global, P.nt_global};
+  const long long n = min((long long)*(volatile unsigned long long*)&P.counters[CNT_WIN], (long long)P.wcap);
+  uint32_t maxb = 0;
+  double maxd = 0.0;
+  const int lane = threadIdx.x & 31;
+  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long e = base + lane;
+    const int t = e < n ? P.wt[e] : -1;
+    const bool active = t >= 0;
+    int4 vc = make_int4(0, 0, 0, 0);
+    if (active) vc = D == 4 ? make_int4(P.wx[e], P.wy[e], P.wz[e], t) : make_int4(P.wx[e], P.wy[e], t, 0);
+    iso_cube<T, D>(P, cq, ext, vc, active, maxb, maxd);
+  }
 }
 
 template <typename T>
@@ -332,8 +472,13 @@ static int launch_t(const ExtractParams& P, long long cq, int ndim, cudaStream_t
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (ndim == 2) k_iso<T, 3><<<sms * 16, 256, 0, stream>>>(P, cq);
-  else k_iso<T, 4><<<sms * 16, 256, 0, stream>>>(P, cq);
+  if (ndim == 2) {
+    k_iso_scan<T, 3><<<sms * 8, 256, 0, stream>>>(P, cq);
+    k_iso_cube<T, 3><<<sms * 8, 256, 0, stream>>>(P, cq);
+  } else {
+    k_iso_scan<T, 4><<<sms * 8, 256, 0, stream>>>(P, cq);
+    k_iso_cube<T, 4><<<sms * 8, 256, 0, stream>>>(P, cq);
+  }
   FTK_CUDA_TRY(cudaGetLastError());
   return FTK_OK;
 }

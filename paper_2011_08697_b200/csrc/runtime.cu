@@ -1123,6 +1123,8 @@ static int iso_run(const ftk_desc* desc, double isovalue, const void* d_field, f
   if (st) return st;
   if (is_vector(desc) || (desc->flags & FTK_GHOST_PLANE) || desc->t0 != 0 || desc->nt != desc->nt_global || desc->nt < 2)
     return FTK_ERR_INVALID_ARG;
+  if (desc->n[0] >= (1ll << 31) || desc->n[1] >= (1ll << 31) || desc->n[2] >= (1ll << 31) || desc->nt >= (1ll << 31))
+    return FTK_ERR_INVALID_ARG;  // k_iso queues anchors as int32 coordinates
   if (!d_field || !n_out || !d_ws || capacity < 0 || capacity > kMaxCapacity || (capacity > 0 && !d_out) ||
       !(isovalue == isovalue))
     return FTK_ERR_INVALID_ARG;
@@ -1158,8 +1160,10 @@ static int iso_run(const ftk_desc* desc, double isovalue, const void* d_field, f
   if (n_elems) *n_elems = (int64_t)host_cnt[CNT_ELEMS];
   st = range_status(desc, host_cnt[CNT_MAXBITS]);
   if (st) return st;
-  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity) {
-    *n_out = std::max<int64_t>((int64_t)host_cnt[CNT_NOUT], (int64_t)host_cnt[CNT_EDGES]);
+  if ((i64)host_cnt[CNT_NOUT] > capacity || (i64)host_cnt[CNT_EDGES] > capacity || (i64)host_cnt[CNT_WIN] > L.wcap) {
+    // records, links, or candidate cubes (k_iso_scan's list, wcap = max(1024, capacity) entries)
+    *n_out = std::max<int64_t>(std::max<int64_t>((int64_t)host_cnt[CNT_NOUT], (int64_t)host_cnt[CNT_EDGES]),
+                               (int64_t)host_cnt[CNT_WIN]);
     return FTK_ERR_CAPACITY;
   }
   if (mesh && (int64_t)host_cnt[CNT_ELEMS] > elem_cap) return FTK_ERR_CAPACITY;  // *n_elems = the need
