@@ -55,7 +55,8 @@ enum Counter : int {
   CNT_POST = 13,      // post-processing: output records (slice / filter)
   CNT_HGROUP = 14,    // pass 2: log2 of the hash-table blocks per coarse cell (set with CNT_HMASK)
   CNT_ELEMS = 15,     // isovolume mesh: simplices emitted (may exceed the element capacity)
-  CNT_PROF = 16,      // 16.. : optional K1 cycle accounting (FTK_K1_PROF builds)
+  CNT_PROF = 16,      // 16..25 : optional K1 cycle accounting (FTK_K1_PROF builds)
+  CNT_XBATCH = 26,    // 2D K1b: next cube batch to claim (dynamic batch assignment)
   CNT_N = 32
 };
 

@@ -719,7 +719,7 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t m) {
 // byte lies in 0x01..0x0F -- the per-byte zero test stays exact)
 __device__ __forceinline__ uint32_t gather_code(const f2 (&c)[8]) {
   // c[2*j] = condition j for positions 0,1; c[2*j+1] = condition j for positions 2,3
-  if (FTK_GATHER_SR) {
+  if constexpr (FTK_GATHER_SR) {
     // per condition: two sign-replicating PRMTs (positions 0, 1 and 2, 3) and two bit-selects
     uint32_t acc = bitsel(prmt_sr(lo32(c[0]), hi32(c[0])), prmt_sr(lo32(c[1]), hi32(c[1])), 0xFFFF0000u);
 #pragma unroll
@@ -729,16 +729,17 @@ __device__ __forceinline__ uint32_t gather_code(const f2 (&c)[8]) {
       acc = bitsel(acc, prmt_sr(lo32(c[2 * j + 1]), hi32(c[2 * j + 1])), m & 0xFFFF0000u);
     }
     return acc;
-  }
-  uint32_t w[4];
+  } else {
+    uint32_t w[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
-    const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
-    w[j] = __byte_perm(p01, p23, 0x5410);
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
+      const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
+      w[j] = __byte_perm(p01, p23, 0x5410);
+    }
+    return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
+           ((w[3] >> 3) & 0x10101010u);
   }
-  return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
-         ((w[3] >> 3) & 0x10101010u);
 }
 
 __device__ __forceinline__ uint32_t code_f32(const float4 u, const float4 v, const float4 d, float l, float r,
@@ -1235,7 +1236,7 @@ __global__ void __launch_bounds__(256) k_expand2d(const __grid_constant__ Extrac
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1b: the exact kernel -- one warp per batch of 32 window-buffer entries (grid-stride, the entry
+// K1b: the exact kernel -- one warp per batch of 32 window-buffer entries (claimed dynamically, the entry
 // count is read from the device counter K1a left behind)
 // ---------------------------------------------------------------------------------------------
 // window of a cube on the spatial boundary (zero outside the grid), raw values; out of line -- rare,
@@ -1253,7 +1254,7 @@ __device__ __noinline__ void load_window_edge(T* dst, const T* field, i64 t0, co
 
 template <typename T>
 __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_constant__ ExtractParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   ExSmem<T>& sm = *reinterpret_cast<ExSmem<T>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Geo G;
@@ -1297,10 +1298,17 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
       }
     }
   };
-  const long long stride = (long long)gridDim.x * EXW;
-  long long b = (long long)blockIdx.x * EXW + w;
+  // batches are claimed dynamically (one atomic per batch and warp): their cost varies with the
+  // punctured faces they hold, and a static stride leaves the slowest warps as a tail
+  auto claim = [&]() -> long long {
+    long long c = 0;
+    if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_XBATCH], 1ull);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  long long b = claim();
   if (b < nbat) fetch(b);
-  for (; b < nbat; b += stride) {
+  while (b < nbat) {
+    const long long bn = claim();
     uint32_t* ent = bb.ring + lane * ws_words<T>();
     bool fast = false;
     if (et != -1) {
@@ -1337,12 +1345,13 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
     }
     bb.qt[lane] = et == -1 ? -1 : (et | (fast ? 0x40000000 : 0));
     __syncwarp();
-    if (PREFETCH && b + stride < nbat) fetch(b + stride);
+    if (PREFETCH && bn < nbat) fetch(bn);
     pf.lap(PF_EXLOAD);
     process_batch<T>(bb, G, P, pf);
     __syncwarp();
-    if (!PREFETCH && b + stride < nbat) fetch(b + stride);
+    if (!PREFETCH && bn < nbat) fetch(bn);
     pf.lap(PF_EXREC);
+    b = bn;
   }
   if (FTK_K1_PROF && lane == 0) {
 #pragma unroll

@@ -31,7 +31,6 @@ namespace k3d {
 using namespace sm100;
 
 constexpr int TCH = 16;                         // anchor timesteps per work item
-constexpr int CHUNK3 = 32;                      // survivor-list entries a warp reserves at a time
 
 __constant__ KuhnTables<4> cK4 = kKuhn4;
 
@@ -404,7 +403,7 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t m) {
 // (FTK_GATHER_SR: bits 1, 0 repeat bit 2, so a byte is zero iff its six condition bits are, and no byte
 // is 0x01 -- the per-byte zero test stays exact)
 __device__ __forceinline__ uint32_t gather6(const f2 (&c)[12]) {
-  if (FTK_GATHER_SR) {
+  if constexpr (FTK_GATHER_SR) {
     // per condition: two sign-replicating PRMTs (positions 0, 1 and 2, 3) and two bit-selects
     uint32_t acc = bitsel(prmt_sr(lo32(c[0]), hi32(c[0])), prmt_sr(lo32(c[1]), hi32(c[1])), 0xFFFF0000u);
 #pragma unroll
@@ -414,16 +413,17 @@ __device__ __forceinline__ uint32_t gather6(const f2 (&c)[12]) {
       acc = bitsel(acc, prmt_sr(lo32(c[2 * j + 1]), hi32(c[2 * j + 1])), m & 0xFFFF0000u);
     }
     return acc;
-  }
-  uint32_t w[6];
+  } else {
+    uint32_t w[6];  // FTK_GATHER_SR = 0: byte picks
 #pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
-    const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
-    w[j] = __byte_perm(p01, p23, 0x5410);
+    for (int j = 0; j < 6; ++j) {
+      const uint32_t p01 = __byte_perm(lo32(c[2 * j]), hi32(c[2 * j]), 0x0073);
+      const uint32_t p23 = __byte_perm(lo32(c[2 * j + 1]), hi32(c[2 * j + 1]), 0x0073);
+      w[j] = __byte_perm(p01, p23, 0x5410);
+    }
+    return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
+           ((w[3] >> 3) & 0x10101010u) | ((w[4] >> 4) & 0x08080808u) | ((w[5] >> 5) & 0x04040404u);
   }
-  return (w[0] & 0x80808080u) | ((w[1] >> 1) & 0x40404040u) | ((w[2] >> 2) & 0x20202020u) |
-         ((w[3] >> 3) & 0x10101010u) | ((w[4] >> 4) & 0x08080808u) | ((w[5] >> 5) & 0x04040404u);
 }
 
 __device__ __forceinline__ uint32_t code6_f32(const float4 u, const float4 v, const float4 d, const float4 zm,
@@ -1261,7 +1261,14 @@ __global__ void __launch_bounds__(XW3 * 32, FTK_X3_MINB) k_exact3d(const __grid_
   const T* field = reinterpret_cast<const T*>(P.field);
   const i64 plane = G.nx * G.ny * G.nz * (VEC ? 3 : 1);
   i64(&g)[16][3] = sg[w];
-  for (long long e = (long long)blockIdx.x * XW3 + w; e < nwin; e += (long long)gridDim.x * XW3) {
+  // hypercubes are claimed dynamically (one atomic per hypercube and warp): their cost varies with the
+  // punctured faces they hold, and a static stride leaves the slowest warps as a tail
+  auto claim = [&]() -> long long {
+    long long c = 0;
+    if (lane == 0) c = (long long)atomicAdd(&P.counters[CNT_XBATCH], 1ull);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  for (long long e = claim(); e < nwin; e = claim()) {
     const int et = P.wt[e];
     if (et == -1) continue;
     const bool hasB = et < 0;

@@ -739,6 +739,7 @@ __global__ void k_window_reset(unsigned long long* c) {
     c[CNT_WORK] = 0;
     c[CNT_WIN] = 0;
     c[CNT_CUBES] = 0;
+    c[CNT_XBATCH] = 0;
   }
 }
 

@@ -166,12 +166,11 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
     TProbe pr(P, hm, key);
     // face ids are unique among the records: claim the first empty slot of the probe sequence
-    u64 probes = 0;
+    [[maybe_unused]] u64 probes = 0;
     while (atomicCAS(&P.table[pr.slot()], EMPTY, (int)i) != EMPTY) {
       pr.next();
       FTK_ASSERT(++probes <= 2 * hm + 2);  // the table always has an empty slot (1.5 slots per record)
     }
-    (void)probes;
   }
 }
 

@@ -9,6 +9,7 @@ VARIANTS = {
     "prof": ["FTK_K1_PROF=1"],              # K1 cycle accounting in counters[CNT_PROF..]
     "xminb3": ["FTK_X_MINB=3"],             # k_exact2d occupancy
     "rw4": ["FTK_K1_RW=4"],                 # k_scan2d rows per warp
+    "tch16": ["FTK_K1_TCHUNK=16"],          # k_scan2d timesteps per work item (halved for small grids)
     "gsr0": ["FTK_GATHER_SR=0"],            # byte-pick gather instead of sign-replicating PRMT
     "s3r0": ["FTK_S3_REGION=0"],            # k_scan3d without the region test
     "s3cnt": ["FTK_S3_COUNT=1"],            # region-test statistics in counters[CNT_PROF..]
