@@ -324,7 +324,8 @@ __device__ __noinline__ uint32_t cube_faces_general(const Win<T>& w, const Geo& 
 }
 
 // int32 fast path: fast entry (interior cube with both planes, |q| < 2^29), gradients precomputed
-// by the scan warp.  Returns false on a zero determinant (the SoS chains are in the general path).
+// when the window was staged.  Returns false on a zero determinant (the SoS chains are in the general
+// path).
 __device__ __forceinline__ bool cube_faces_fast(const uint32_t* E, uint32_t& pmask) {
   int g[8][2];
 #pragma unroll
@@ -365,6 +366,29 @@ __device__ __forceinline__ bool cube_faces_fast(const uint32_t* E, uint32_t& pma
   }
   FTK_UP(0) FTK_UP(1) FTK_UP(2) FTK_UP(3) FTK_UP(4) FTK_UP(5)
 #undef FTK_UP
+  pmask = m;
+  return true;
+}
+
+// int32 fast path for a fast entry on the last timestep (no t + 1 corners, the window's second plane
+// repeats the first): only the in-plane faces -- types 0 = (x, x|y) and 3 = (y, x|y) -- exist, and no
+// cell.  Returns false on a zero determinant (the SoS chains are in the general path).
+__device__ __forceinline__ bool cube_faces_planar(const uint32_t* E, uint32_t& pmask) {
+  int g[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    g[c][0] = (int)E[32 + 2 * c];
+    g[c][1] = (int)E[33 + 2 * c];
+  }
+  auto det = [&](int a, int b) { return (i64)g[a][0] * g[b][1] - (i64)g[a][1] * g[b][0]; };
+  const i64 d01 = det(0, 1), d02 = det(0, 2), d03 = det(0, 3), d13 = det(1, 3), d23 = det(2, 3);
+  if (d01 == 0 || d02 == 0 || d03 == 0 || d13 == 0 || d23 == 0) return false;
+  static_assert(Face3<0>::m1 == 1 && Face3<0>::m2 == 3 && Face3<3>::m1 == 2 && Face3<3>::m2 == 3, "in-plane types");
+  // s0 = sgn D(m1, 3), s1 = -sgn D(0, 3), s2 = sgn D(0, m1): punctured iff all equal (as cube_faces_fast)
+  const bool b = d03 > 0;
+  uint32_t m = 0;
+  m |= (uint32_t)((d13 < 0) == b && b == (d01 < 0)) << 0;
+  m |= (uint32_t)((d23 < 0) == b && b == (d02 < 0)) << 3;
   pmask = m;
   return true;
 }
@@ -582,7 +606,8 @@ __device__ void process_batch(const BatchBuf& bb, const Geo& G, const ExtractPar
   const bool isq = (qtv >> 30) & 1;
   uint32_t m = 0;
   if (valid) {
-    if (!(isq && cube_faces_fast(E, m))) m = cube_faces_general<T>(Win<T>{E, isq, G.scale_f, G.scale}, G, x, y, hasB);
+    const bool done = isq && (hasB ? cube_faces_fast(E, m) : cube_faces_planar(E, m));
+    if (!done) m = cube_faces_general<T>(Win<T>{E, isq, G.scale_f, G.scale}, G, x, y, hasB);
   }
   const uint32_t pmask = m & 0xFFFu, umask = m >> 16;
   pf.lap(PF_EXFACE);
@@ -1318,7 +1343,7 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
           float mx = 0.f;
 #pragma unroll
           for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fabsf(v[k]));
-          fast = hasB && mx < qmaxf;
+          fast = mx < qmaxf;  // last-timestep cubes too (the second plane repeats the first)
         }
         if (fast) {
           int qv[32];
