@@ -105,3 +105,69 @@ def smooth_types(rec, nbr, half_window):
         if seen[0] and seen[1] and len(set(types)) == 1 and types[0] != int(rec[i]["type"]):
             out[i]["type"] = types[0]
     return out
+
+
+def simplify_types(rec, nbr, tau):
+    """Simplification in time (R23): a trajectory is cut at its folds -- records whose
+    two partners both lie strictly later, or both strictly earlier, in t (a pair is born or annihilates
+    there) -- into segments running from one fold to the next (both folds included).  A segment bounded
+    by folds on both ends whose time extent (max t - min t over its records) is below tau, and whose two
+    outer records (the partners of its folds outside it) exist and share one type T, is a short-lived
+    excursion (the saddle of Fig. 9(b)): its records take T.  A fold lies in two segments; it takes T
+    when the qualifying ones agree.  Decided on the unmodified types, then applied."""
+    n = len(rec)
+    t = [float(r["t"]) for r in rec]
+    ty = [int(r["type"]) for r in rec]
+
+    def is_fold(i):
+        if len(nbr[i]) != 2:
+            return False
+        a, b = (t[j] - t[i] for j in nbr[i])
+        return (a > 0 and b > 0) or (a < 0 and b < 0)
+
+    # order every trajectory as a path (from an end) or a loop (from its smallest index)
+    seen = [False] * n
+    paths = []
+    for s in list(range(n)):
+        if seen[s] or len(nbr[s]) == 2:
+            continue
+        paths.append((_walk(nbr, s, seen), False))
+    for s in range(n):
+        if not seen[s]:
+            paths.append((_walk(nbr, s, seen), True))
+    votes = {}  # record -> set of T from the qualifying segments holding it
+    for path, loop in paths:
+        m = len(path)
+        folds = [p for p in range(m) if is_fold(path[p])]
+        if len(folds) < 2:
+            continue
+        pairs = list(zip(folds, folds[1:]))
+        if loop:
+            pairs.append((folds[-1], folds[0] + m))  # the segment through the path's start
+        for fa, fb in pairs:
+            if not loop and (fa == 0 or fb == m - 1):
+                continue  # a fold needs a partner outside the segment (cannot happen: folds are interior)
+            seg = [path[p % m] for p in range(fa, fb + 1)]
+            ts = [t[k] for k in seg]
+            if not (max(ts) - min(ts) < tau):
+                continue
+            oa, ob = path[(fa - 1) % m], path[(fb + 1) % m]
+            if ty[oa] != ty[ob]:
+                continue
+            for k in seg:
+                votes.setdefault(k, set()).add(ty[oa])
+    out = rec.copy()
+    for k, v in votes.items():
+        if len(v) == 1:
+            out[k]["type"] = next(iter(v))
+    return out
+
+
+def _walk(nbr, s, seen):
+    path, prev, cur = [], -1, s
+    while cur >= 0 and not seen[cur]:
+        seen[cur] = True
+        path.append(cur)
+        nxt = [j for j in nbr[cur] if j != prev]
+        prev, cur = cur, (nxt[0] if nxt else -1)
+    return path
