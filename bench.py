@@ -387,7 +387,8 @@ def run_ours(args):
         del ws, host, planes
 
     # trajectory post-processing over this step's records: adjacency, a slice,
-    # a duration filter and type smoothing, each synchronous; wall clock per operation
+    # a duration filter, simplification in time (tau = 2 timesteps) and type smoothing, each synchronous;
+    # wall clock per operation
     post_line = None
     if world == 1 and not args.no_stream and not args.no_e2e and not d3:
         rec_p, buf_p = ftk.track(field, cfg.scale_log2, buffers=buf, vector=vec, return_buffers=True)
@@ -403,6 +404,10 @@ def run_ours(args):
         t = time.perf_counter()
         n_filt = tj.filter(nt_global / 4, drop_loops=True).shape[0]
         tp["filter_ms"] = (time.perf_counter() - t) * 1000.0
+        t = time.perf_counter()
+        tj.simplify_types(2.0)
+        torch.cuda.synchronize(dev)
+        tp["simplify_ms"] = (time.perf_counter() - t) * 1000.0
         t = time.perf_counter()
         tj.smooth_types(2)
         torch.cuda.synchronize(dev)

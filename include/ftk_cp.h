@@ -228,7 +228,7 @@ FTK_API int ftk_tracker_push(ftk_tracker* tracker, const void* plane);
 FTK_API int ftk_tracker_finish(ftk_tracker* tracker, int64_t* n_out);
 FTK_API int ftk_tracker_abort(ftk_tracker* tracker);
 
-/* Trajectory post-processing (P:419 slicing; P:470-479 filtering and type smoothing) over the labelled
+/* Trajectory post-processing (P:419 slicing; P:470-479 filtering, simplification and type smoothing) over the labelled
  * records d_rec[0, n) of ONE ftk_cp_track call on the whole domain described by desc, with the
  * workspace of that call (d_ws, ws_bytes, capacity; n <= capacity; its hash table, face-id and scratch
  * regions are reused, so the workspace must not be in use by another call).  All arrays are device
@@ -248,6 +248,15 @@ FTK_API int ftk_tracker_abort(ftk_tracker* tracker);
  *   smooth_types: for every record, up to half_window records are visited along the trajectory on each
  *     side; if both sides are non-empty and all visited records share one type T different from the
  *     record's own, its type becomes T (decided on the unmodified types, then applied; in place).
+ *   simplify_types (simplification by persistence in time; R23): a FOLD is a record
+ *     with two partners that both lie strictly later, or both strictly earlier, in t (a critical-point
+ *     pair is born or annihilates there).  Folds cut a trajectory into segments running from one fold
+ *     to the next (both included).  A segment with a fold at each end whose time extent (max t - min t
+ *     over its records) is < tau, and whose two outer records (the partners of its end folds outside
+ *     it) share one type T, is a short-lived excursion: its records take type T.  A fold belongs to
+ *     two segments and takes T when the qualifying ones agree.  A loop with fewer than two folds is not
+ *     cut.  Decided on the unmodified types, then applied (in place).  tau must not be NaN
+ *     (FTK_ERR_INVALID_ARG); tau <= 0 changes nothing.
  *   slice / filter write up to cap records to d_out and set *n_out to the full count (FTK_ERR_CAPACITY
  *   when it exceeds cap); the output order is unspecified. */
 FTK_API int ftk_post_adjacency(const ftk_desc* desc, const ftk_cp* d_rec, int64_t n, int64_t* d_nbr, void* d_ws,
@@ -261,6 +270,8 @@ FTK_API int ftk_post_filter(const ftk_desc* desc, const ftk_cp* d_rec, const int
 FTK_API int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n,
                                   int32_t half_window, void* d_ws, size_t ws_bytes, int64_t capacity,
                                   ftk_stream stream);
+FTK_API int ftk_post_simplify_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n,
+                                    double tau, void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream);
 
 /* Isovolume tracking (Alg. 1 right): the level set f = isovalue of a 2D+t / 3D+t SCALAR
  * field (desc as for track, the whole domain: t0 = 0, nt = nt_global >= 2, no ghost plane) on the same

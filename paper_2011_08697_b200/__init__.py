@@ -43,7 +43,7 @@ EXPORTS = [
     "ftk_stitch_resolve", "ftk_set_debug",
     "ftk_relabel", "ftk_seam_pack", "ftk_seam_resolve",
     "ftk_tracker_workspace_size", "ftk_tracker_begin", "ftk_tracker_push", "ftk_tracker_finish", "ftk_tracker_abort",
-    "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types", "ftk_iso_track",
+    "ftk_post_adjacency", "ftk_post_slice", "ftk_post_filter", "ftk_post_smooth_types", "ftk_post_simplify_types", "ftk_iso_track",
     "ftk_iso_track_mesh",
 ]
 
@@ -109,6 +109,7 @@ def lib() -> ctypes.CDLL:
         L.ftk_post_slice.argtypes = [PD, P, P, I64, ctypes.c_double, P, I64, P, P, SZ, I64, P]
         L.ftk_post_filter.argtypes = [PD, P, P, I64, ctypes.c_double, ctypes.c_int32, P, I64, P, P, SZ, I64, P]
         L.ftk_post_smooth_types.argtypes = [PD, P, P, I64, ctypes.c_int32, P, SZ, I64, P]
+        L.ftk_post_simplify_types.argtypes = [PD, P, P, I64, ctypes.c_double, P, SZ, I64, P]
         L.ftk_iso_track.argtypes = [PD, ctypes.c_double, P, P, I64, P, P, SZ, P]
         L.ftk_iso_track_mesh.argtypes = [PD, ctypes.c_double, P, P, I64, P, P, I64, P, P, SZ, P]
         _lib = L
@@ -381,7 +382,7 @@ class Tracker:
 class Trajectories:
     """Post-processing of the labelled records of one track() call (PAPER.md:419, 470-479;
     include/ftk_cp.h ftk_post_*): adjacency along the trajectories, slicing at a time t0, filtering by
-    duration / loops, type smoothing.  `buffers` are the ones the track call used (return_buffers=True);
+    duration / loops, simplification in time, type smoothing.  `buffers` are the ones the track call used (return_buffers=True);
     `shape` is the tracked field's shape."""
 
     def __init__(self, rec: torch.Tensor, buffers: Buffers, shape, dtype, scale_log2: int, vector: bool = False):
@@ -422,6 +423,14 @@ class Trajectories:
         _check(lib().ftk_post_smooth_types(ctypes.byref(self.desc), ctypes.c_void_p(self.rec.data_ptr()),
                                            ctypes.c_void_p(self.nbr.data_ptr()), self.n, half_window, *self._ws()),
                "ftk_post_smooth_types")
+        return self.rec
+
+    def simplify_types(self, tau: float) -> torch.Tensor:
+        """in place on the records: short-lived fold-to-fold segments (time extent < tau) take the type
+        of the trajectory around them (simplification by persistence in time)"""
+        _check(lib().ftk_post_simplify_types(ctypes.byref(self.desc), ctypes.c_void_p(self.rec.data_ptr()),
+                                             ctypes.c_void_p(self.nbr.data_ptr()), self.n, ctypes.c_double(tau),
+                                             *self._ws()), "ftk_post_simplify_types")
         return self.rec
 
 

@@ -1057,12 +1057,13 @@ int ftk_post_adjacency(const ftk_desc* desc, const ftk_cp* d_rec, int64_t n, int
 
 static int post_op(int op, const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double t0,
                    double dmin, int drop_loops, int half_window, ftk_cp* d_out, int64_t cap, int64_t* n_out,
-                   void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+                   void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream, double tau = 0.0) {
   Layout L;
   int st = post_setup(desc, n, d_ws, ws_bytes, capacity, L);
   if (st) return st;
   if (n > 0 && (!d_rec || !d_nbr)) return FTK_ERR_INVALID_ARG;
-  if (op != 2 && (!n_out || cap < 0 || (cap > 0 && !d_out))) return FTK_ERR_INVALID_ARG;
+  const bool in_place = op == 2 || op == 3;
+  if (!in_place && (!n_out || cap < 0 || (cap > 0 && !d_out))) return FTK_ERR_INVALID_ARG;
   char* ws = static_cast<char*>(d_ws);
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1080,6 +1081,7 @@ static int post_op(int op, const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d
   c.dmin = dmin;
   c.drop_loops = drop_loops;
   c.half_window = half_window;
+  c.tau = tau;
   FTK_CUDA_TRY(cudaMemsetAsync(counters + CNT_POST, 0, sizeof(u64), s));
   if (n > 0) {
     st = launch_post(TP, op, c, s);
@@ -1088,7 +1090,7 @@ static int post_op(int op, const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d
   unsigned long long cnt = 0;
   FTK_CUDA_TRY(cudaMemcpyAsync(&cnt, counters + CNT_POST, sizeof cnt, cudaMemcpyDeviceToHost, s));
   FTK_CUDA_TRY(cudaStreamSynchronize(s));
-  if (op == 2) return FTK_OK;
+  if (in_place) return FTK_OK;
   *n_out = (int64_t)cnt;
   return (int64_t)cnt > cap ? FTK_ERR_CAPACITY : FTK_OK;
 }
@@ -1114,6 +1116,13 @@ int ftk_post_smooth_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_
   if (half_window < 1) return FTK_ERR_INVALID_ARG;
   return post_op(2, desc, d_rec, d_nbr, n, 0.0, 0.0, 0, half_window, nullptr, 0, nullptr, d_ws, ws_bytes, capacity,
                  stream);
+}
+
+int ftk_post_simplify_types(const ftk_desc* desc, ftk_cp* d_rec, const int64_t* d_nbr, int64_t n, double tau,
+                            void* d_ws, size_t ws_bytes, int64_t capacity, ftk_stream stream) {
+  if (!(tau == tau)) return FTK_ERR_INVALID_ARG;
+  return post_op(3, desc, d_rec, d_nbr, n, 0.0, 0.0, 0, 0, nullptr, 0, nullptr, d_ws, ws_bytes, capacity, stream,
+                 tau);
 }
 
 // ------------------------------------------------------------------------------ isovolume tracking

@@ -630,6 +630,7 @@ struct PostArgs {
   int* newtype;               // [n]
   double t0, dmin;
   int drop_loops, half_window;
+  double tau;
 };
 
 __device__ __forceinline__ void post_emit(const PostArgs& A, const ftk_cp& r) {
@@ -730,6 +731,72 @@ __global__ void k_post_smooth(const __grid_constant__ PostArgs A) {
   }
 }
 
+// simplification in time (R23).  A fold is a record whose two partners both lie
+// strictly later or both strictly earlier in t (a pair is born or annihilates there); folds cut a
+// trajectory into segments (fold to fold, both included).  A segment with folds on both ends, time
+// extent (max t - min t) below tau and outer records (the partners of its folds outside it) of one
+// type T is a short-lived excursion: its records take T; a fold, in two segments, takes T when the
+// qualifying ones agree.  Each record walks its segment(s) along the trajectory, stopping as soon as the
+// extent reaches tau (the extent only grows), so a walk visits the records within tau of it in time.
+__device__ __forceinline__ bool post_is_fold(const PostArgs& A, long long i) {
+  const long long a = A.nbr[2 * i], b = A.nbr[2 * i + 1];
+  if (a < 0 || b < 0) return false;
+  const double ti = A.rec[i].t, da = A.rec[a].t - ti, db = A.rec[b].t - ti;
+  return (da > 0 && db > 0) || (da < 0 && db < 0);
+}
+// walk from record `from` (already in the segment, extent [lo, hi]) through `cur` to the next fold;
+// returns the fold's outer record (-1: no fold before a trajectory end, back at `start`, or extent >= tau)
+__device__ __forceinline__ long long post_to_fold(const PostArgs& A, long long start, long long from, long long cur,
+                                                  double& lo, double& hi, long long& fold) {
+  long long prev = from;
+  while (true) {
+    if (cur < 0 || cur == start) return -1;
+    const double tc = A.rec[cur].t;
+    lo = fmin(lo, tc);
+    hi = fmax(hi, tc);
+    if (!(hi - lo < A.tau)) return -1;
+    const long long a = A.nbr[2 * cur], b = A.nbr[2 * cur + 1];
+    const long long nx = a == prev ? b : a;
+    if (post_is_fold(A, cur)) {
+      fold = cur;
+      return nx;
+    }
+    prev = cur;
+    cur = nx;
+  }
+}
+__global__ void k_post_simplify(const __grid_constant__ PostArgs A) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x) {
+    const int own = A.rec[i].type;
+    const double ti = A.rec[i].t;
+    const long long n0 = A.nbr[2 * i], n1 = A.nbr[2 * i + 1];
+    int T = -1;
+    bool clash = false;
+    if (post_is_fold(A, i)) {
+      // two segments: one on each side, the other partner of i being the outer record at this end
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        double lo = ti, hi = ti;
+        long long f;
+        const long long o = post_to_fold(A, i, i, side ? n1 : n0, lo, hi, f);
+        if (o < 0) continue;
+        const int ta = A.rec[side ? n0 : n1].type, tb = A.rec[o].type;
+        if (ta != tb) continue;
+        if (T >= 0 && T != ta) clash = true;
+        T = ta;
+      }
+    } else if (n0 >= 0 && n1 >= 0) {
+      double lo = ti, hi = ti;
+      long long f0 = -1, f1 = -1;
+      const long long o0 = post_to_fold(A, i, i, n0, lo, hi, f0);
+      const long long o1 = o0 < 0 ? -1 : post_to_fold(A, i, i, n1, lo, hi, f1);
+      // (f0 == f1: a loop with a single fold, not cut into segments)
+      if (o1 >= 0 && f0 != f1 && A.rec[o0].type == A.rec[o1].type) T = A.rec[o0].type;
+    }
+    A.newtype[i] = (T >= 0 && !clash) ? T : own;
+  }
+}
+
 __global__ void k_post_apply_types(const __grid_constant__ PostArgs A, ftk_cp* rec) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += (i64)gridDim.x * blockDim.x)
     rec[i].type = A.newtype[i];
@@ -784,6 +851,7 @@ int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t st
   A.dmin = c.dmin;
   A.drop_loops = c.drop_loops;
   A.half_window = c.half_window;
+  A.tau = c.tau;
   if (op == 0) {
     k_post_slice<<<blocks, threads, 0, stream>>>(A);
   } else if (op == 1) {
@@ -792,6 +860,10 @@ int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t st
     k_post_stats<<<blocks, threads, 0, stream>>>(P, A);
     FTK_CUDA_TRY(cudaGetLastError());
     k_post_filter<<<blocks, threads, 0, stream>>>(P, A);
+  } else if (op == 3) {
+    k_post_simplify<<<blocks, threads, 0, stream>>>(A);
+    FTK_CUDA_TRY(cudaGetLastError());
+    k_post_apply_types<<<blocks, threads, 0, stream>>>(A, c.rec_mut);
   } else {
     k_post_smooth<<<blocks, threads, 0, stream>>>(A);
     FTK_CUDA_TRY(cudaGetLastError());

@@ -55,10 +55,11 @@ struct PostCall {
   long long* scratch;         // [3 n] int64 + [n] int32
   double t0, dmin;
   int drop_loops, half_window;
+  double tau;                 // simplification: persistence-in-time threshold
 };
 int launch_post_adjacency(const TrackParams& P, int ndim, const i64* ext, long long n, long long* nbr,
                           cudaStream_t stream);
-int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t stream);  // 0 slice, 1 filter, 2 smooth
+int launch_post(const TrackParams& P, int op, const PostCall& c, cudaStream_t stream);  // 0 slice, 1 filter, 2 smooth, 3 simplify
 
 }  // namespace ftk
 

@@ -1,6 +1,7 @@
 """GPU trajectory post-processing (include/ftk_cp.h ftk_post_*) against the
 plain-Python reference oracle/post.py on the oracle's records: adjacency (as a set of linked face-id
-pairs), slices at integer and fractional t0, duration / loop filtering, and type smoothing -- bit-exact
+pairs), slices at integer and fractional t0, duration / loop filtering, simplification in time and type
+smoothing -- bit-exact
 (same records, same fixed-order FP64)."""
 import numpy as np
 import pytest
@@ -75,6 +76,17 @@ def test_smooth(ftk, oracle_lib, w):
     r = _key(post.smooth_types(ref, nbr, w))
     assert np.array_equal(g["type"], r["type"])
     assert (r["type"] != _key(ref)["type"]).any()  # the case exercises the rule
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.0, 3.0])
+def test_simplify(ftk, oracle_lib, tau):
+    field = fi.Woven(48, 40, 12, L=15.0, sigma=0.08).generate()
+    tj, ref, nbr = setup_case(ftk, oracle_lib, field, 26, (48, 40, 12))
+    g = _key(ftk.to_numpy(tj.simplify_types(tau)))
+    r = _key(post.simplify_types(ref, nbr, tau))
+    assert np.array_equal(g["type"], r["type"])
+    if tau == 3.0:
+        assert (r["type"] != _key(ref)["type"]).any()  # the case exercises the rule
 
 
 def test_3d_adjacency_and_slice(ftk, oracle_lib):
