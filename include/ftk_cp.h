@@ -315,10 +315,15 @@ FTK_API int ftk_comm_destroy(ftk_comm* comm);
  * path taken): FTK_DEBUG_FORCE_GENERIC stages the 2D planes with the generic loader instead of TMA,
  * FTK_DEBUG_VERIFY_LINK re-derives every punctured face's parent cells in closed form after pass 2
  * (side_of; a cell without exactly one partner counts as FTK_ERR_INVARIANT), FTK_DEBUG_STITCH_HOST
- * resolves time-slab seams through the host path.  FTK_ERR_INVALID_ARG for unknown bits. */
+ * resolves time-slab seams through the host path, FTK_DEBUG_NO_GRAPH launches every kernel of a track
+ * call directly instead of replaying the call's cached CUDA graph (ftk_cp_track captures the launch
+ * sequence of a call on first use and replays it when the same call -- descriptor, pointers, capacity,
+ * workspace, switches -- repeats on the same host thread and device; a caller capturing its own stream
+ * gets plain launches).  FTK_ERR_INVALID_ARG for unknown bits. */
 #define FTK_DEBUG_FORCE_GENERIC 1u
 #define FTK_DEBUG_VERIFY_LINK 2u
 #define FTK_DEBUG_STITCH_HOST 4u
+#define FTK_DEBUG_NO_GRAPH 8u
 FTK_API int ftk_set_debug(uint32_t flags);
 
 #ifdef __cplusplus

@@ -274,6 +274,83 @@ static int result_status(const ftk_desc* desc, const unsigned long long* host_cn
   return FTK_OK;
 }
 
+// CUDA graphs of the launch sequence of a call (counter reset, extraction kernels, pass 2, export),
+// replayed when the same call repeats -- same descriptor, pointers, capacity, workspace and debug
+// switches (the kernels' parameters, the TMA descriptor and every grid size derive from these alone) --
+// so a step costs one graph launch instead of ~8 kernel launches (fixed per-step
+// overheads).  Not used while profiling events are recorded (they time individual kernels) or under
+// FTK_DEBUG_NO_GRAPH.
+struct GraphKey {
+  ftk_desc desc;
+  const void* field;
+  const void* out;
+  const void* ws;
+  int64_t capacity;
+  uint32_t debug;
+  int32_t track;
+  int32_t dev;
+  int32_t pad;
+};
+struct GraphEnt {
+  GraphKey key;
+  cudaGraphExec_t exec;
+};
+static std::vector<GraphEnt>& graph_cache() {
+  thread_local std::vector<GraphEnt> cache;  // per host thread; the key holds the device
+  return cache;
+}
+
+static int enqueue_call(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, char* ws,
+                        const Layout& L, unsigned long long* counters, cudaStream_t stream, bool track, Events& ev);
+static int finish_call(const ftk_desc* desc, const Layout& L, int64_t capacity, int64_t* n_out,
+                       unsigned long long* counters, cudaStream_t stream, Events& ev);
+
+// the stream graphs are captured on (per host thread and device): capture needs a stream other than the
+// legacy default stream, which callers (torch's default) often pass; the captured work does not run there
+static cudaStream_t capture_stream(int dev) {
+  thread_local std::unordered_map<int, cudaStream_t> streams;
+  cudaStream_t& s = streams[dev];
+  if (!s && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    s = nullptr;
+  }
+  return s;
+}
+
+template <typename F>
+static int launch_graphed(const GraphKey& key, cudaStream_t stream, F&& enqueue) {
+  std::vector<GraphEnt>& cache = graph_cache();
+  for (GraphEnt& g : cache)
+    if (memcmp(&g.key, &key, sizeof key) == 0) {
+      FTK_CUDA_TRY(cudaGraphLaunch(g.exec, stream));
+      return FTK_OK;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FTK_CUDA_TRY(cudaStreamIsCapturing(stream, &cs));
+  const cudaStream_t cap = capture_stream(key.dev);
+  if (cs != cudaStreamCaptureStatusNone || !cap) return enqueue(stream);  // caller capturing: plain launches
+  FTK_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  const int st = enqueue(cap);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = (st == FTK_OK && ce == cudaSuccess) ? cudaGraphInstantiate(&exec, graph, 0) : ce;
+  if (graph) cudaGraphDestroy(graph);
+  if (st == FTK_OK && ie != cudaSuccess) {
+    // the sequence could not be captured or instantiated: run it directly (nothing of it ran yet)
+    cudaGetLastError();
+    return enqueue(stream);
+  }
+  if (st) return st;
+  if (cache.size() >= 8) {  // a few live configurations per thread; the oldest goes
+    cudaGraphExecDestroy(cache.front().exec);
+    cache.erase(cache.begin());
+  }
+  cache.push_back(GraphEnt{key, exec});
+  FTK_CUDA_TRY(cudaGraphLaunch(exec, stream));
+  return FTK_OK;
+}
+
 static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, int64_t* n_out,
                void* d_ws, size_t ws_bytes, cudaStream_t stream, bool track) {
   int st = validate(desc);
@@ -285,6 +362,30 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
   char* ws = static_cast<char*>(d_ws);
   auto* counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
   Events ev;
+  if (!ev.on && !(g_debug & FTK_DEBUG_NO_GRAPH)) {
+    GraphKey key;
+    memset(&key, 0, sizeof key);
+    key.desc = *desc;
+    key.field = d_field;
+    key.out = d_out;
+    key.ws = d_ws;
+    key.capacity = capacity;
+    key.debug = g_debug;
+    key.track = track;
+    FTK_CUDA_TRY(cudaGetDevice(&key.dev));
+    st = launch_graphed(key, stream, [&](cudaStream_t sq) {
+      return enqueue_call(desc, d_field, d_out, capacity, ws, L, counters, sq, track, ev);
+    });
+  } else {
+    st = enqueue_call(desc, d_field, d_out, capacity, ws, L, counters, stream, track, ev);
+  }
+  if (st) return st;
+  return finish_call(desc, L, capacity, n_out, counters, stream, ev);
+}
+
+static int enqueue_call(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t capacity, char* ws,
+                        const Layout& L, unsigned long long* counters, cudaStream_t stream, bool track, Events& ev) {
+  int st;
   ev.rec(0, stream);
   FTK_CUDA_TRY(cudaMemsetAsync(counters, 0, CNT_N * sizeof(u64), stream));
 
@@ -307,6 +408,11 @@ static int run(const ftk_desc* desc, const void* d_field, ftk_cp* d_out, int64_t
     }
   }
   ev.rec(3, stream);
+  return FTK_OK;
+}
+
+static int finish_call(const ftk_desc* desc, const Layout& L, int64_t capacity, int64_t* n_out,
+                       unsigned long long* counters, cudaStream_t stream, Events& ev) {
   unsigned long long* host_cnt = pinned_counters();
   FTK_CUDA_TRY(cudaMemcpyAsync(host_cnt, counters, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
   FTK_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -1281,7 +1387,7 @@ int ftk_comm_destroy(ftk_comm* comm) {
 }
 
 int ftk_set_debug(uint32_t flags) {
-  if (flags & ~(uint32_t)(FTK_DEBUG_FORCE_GENERIC | FTK_DEBUG_VERIFY_LINK | FTK_DEBUG_STITCH_HOST))
+  if (flags & ~(uint32_t)(FTK_DEBUG_FORCE_GENERIC | FTK_DEBUG_VERIFY_LINK | FTK_DEBUG_STITCH_HOST | FTK_DEBUG_NO_GRAPH))
     return FTK_ERR_INVALID_ARG;
   g_debug = flags;
   return FTK_OK;
