@@ -483,9 +483,10 @@ def run_ours(args):
         "stream": stream_line,
         "post": post_line,
         "iso": iso_line,
-        # K1a + K1b (+ k_expand2d on the 2D vector path) + k_clear + k_hash_insert + k_edges + k_label;
-        # time slabs add k_export and the device seam path (k_seam_pack, _clear, _insert, _union, _relabel)
-        "gpu_launches": ((7 if vec and not d3 else 6) + (6 if world > 1 else 0)) * args.steps,
+        # K1a + K1b (+ k_expand2d in 2D) + k_clear + k_hash_insert + k_edges + k_root + k_label (one CUDA
+        # graph per step; the ncu launch list shows them); time slabs add k_export and the device seam
+        # path (k_seam_pack, _clear, _insert, _union, _relabel)
+        "gpu_launches": ((7 if d3 else 8) + (6 if world > 1 else 0)) * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)

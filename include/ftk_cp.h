@@ -319,11 +319,14 @@ FTK_API int ftk_comm_destroy(ftk_comm* comm);
  * call directly instead of replaying the call's cached CUDA graph (ftk_cp_track captures the launch
  * sequence of a call on first use and replays it when the same call -- descriptor, pointers, capacity,
  * workspace, switches -- repeats on the same host thread and device; a caller capturing its own stream
- * gets plain launches).  FTK_ERR_INVALID_ARG for unknown bits. */
+ * gets plain launches), FTK_DEBUG_UF_BY_ID as below.  FTK_ERR_INVALID_ARG for unknown bits. */
 #define FTK_DEBUG_FORCE_GENERIC 1u
 #define FTK_DEBUG_VERIFY_LINK 2u
 #define FTK_DEBUG_STITCH_HOST 4u
 #define FTK_DEBUG_NO_GRAPH 8u
+#define FTK_DEBUG_UF_BY_ID 16u  /* pass 2 links union-find roots by face id at any record count (by default
+                                   by an index priority up to 2^24 records, with the labels gathered at the
+                                   roots: the same labels, other paths) */
 FTK_API int ftk_set_debug(uint32_t flags);
 
 #ifdef __cplusplus

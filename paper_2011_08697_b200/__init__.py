@@ -25,7 +25,7 @@ OK, ERR_INVALID_ARG, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_INVARIANT,
 F32, F64 = 0, 1
 DEGENERATE, MIN, SADDLE, SADDLE1, SADDLE2, MAX, SOURCE, SINK, CENTER = range(9)
 GHOST_PLANE, SORTED, VECTOR_FIELD = 1, 2, 4
-DEBUG_FORCE_GENERIC, DEBUG_VERIFY_LINK, DEBUG_STITCH_HOST, DEBUG_NO_GRAPH = 1, 2, 4, 8
+DEBUG_FORCE_GENERIC, DEBUG_VERIFY_LINK, DEBUG_STITCH_HOST, DEBUG_NO_GRAPH, DEBUG_UF_BY_ID = 1, 2, 4, 8, 16
 CP_ORDINAL, CP_BOUNDARY, CP_DEGENERATE_LOC = 1, 2, 4
 
 RECORD_DTYPE = np.dtype(
@@ -446,7 +446,7 @@ def set_profiling(enable: bool):
 
 def set_debug(flags: int):
     """Testing switches of the calling thread (DEBUG_FORCE_GENERIC | DEBUG_VERIFY_LINK |
-    DEBUG_STITCH_HOST, DEBUG_NO_GRAPH; include/ftk_cp.h ftk_set_debug): they change the path taken, never the
+    DEBUG_STITCH_HOST, DEBUG_NO_GRAPH, DEBUG_UF_BY_ID; include/ftk_cp.h ftk_set_debug): they change the path taken, never the
     result."""
     _check(lib().ftk_set_debug(int(flags)), "ftk_set_debug")
 

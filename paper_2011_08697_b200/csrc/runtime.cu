@@ -234,6 +234,10 @@ static TrackParams track_params(const ftk_desc* desc, ftk_cp* d_out, int64_t cap
   TP.lookup_types = TP.verify ? ~0ull : (desc->ndim == 2 ? upper_types<3>(kKuhn3) : upper_types<4>(kKuhn4));
   TP.fid = reinterpret_cast<i64*>(ws + L.fid);
   TP.parent = reinterpret_cast<int*>(ws + L.parent);
+  // the relabel-map region is dead during pass 2 (the stitch and post-processing use it afterwards)
+  TP.lab = reinterpret_cast<long long*>(ws + L.map);
+  TP.root = reinterpret_cast<int*>(ws + L.map + (size_t)capacity * sizeof(long long));
+  TP.uf_by_id = (g_debug & FTK_DEBUG_UF_BY_ID) != 0;
   TP.T = desc->ndim == 2 ? 12 : 60;
   TP.plane = desc->n[0] * desc->n[1] * desc->n[2];
   TP.ndim = desc->ndim;
@@ -1387,7 +1391,8 @@ int ftk_comm_destroy(ftk_comm* comm) {
 }
 
 int ftk_set_debug(uint32_t flags) {
-  if (flags & ~(uint32_t)(FTK_DEBUG_FORCE_GENERIC | FTK_DEBUG_VERIFY_LINK | FTK_DEBUG_STITCH_HOST | FTK_DEBUG_NO_GRAPH))
+  if (flags & ~(uint32_t)(FTK_DEBUG_FORCE_GENERIC | FTK_DEBUG_VERIFY_LINK | FTK_DEBUG_STITCH_HOST | FTK_DEBUG_NO_GRAPH |
+                          FTK_DEBUG_UF_BY_ID))
     return FTK_ERR_INVALID_ARG;
   g_debug = flags;
   return FTK_OK;

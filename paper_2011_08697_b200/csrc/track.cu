@@ -67,6 +67,9 @@ constexpr int HBLK_LOG2 = 12;
 #define FTK_HRUN 32
 #endif
 constexpr int HRUN = FTK_HRUN;  // slots probed per block before the jump
+#ifndef FTK_UF_PRIO_MAX
+#define FTK_UF_PRIO_MAX (1ll << 24)  // record counts up to which roots are linked by index priority
+#endif
 __device__ __forceinline__ u64 coarse_cells(const TrackParams& P) {
   if (P.ndim == 2)
     return (u64)((P.ext[0] + 127) >> 7) * (u64)((P.ext[1] + 63) >> 6) * (u64)((P.ext[3] + 31) >> 5);
@@ -138,6 +141,15 @@ __device__ __forceinline__ i64 n_records(const TrackParams& P) {
   return n < P.capacity ? n : P.capacity;
 }
 
+// Union-find linking rule of this call (device-side, from the record count): by a pseudo-random
+// priority of the record index, the label then gathered at the roots (k_root), while the records fit
+// the L2-resident regime (C2: k_edges 106 -> 64 us, pass 2 0.211 -> 0.183 ms; C5 0.150 -> 0.096 ms);
+// by face id beyond it, where the gather pass's extra DRAM traffic costs more than the shorter paths
+// save (C4, 87 M records: pass 2 5.10 ms by face id, 5.70 by priority).  Labels are the same either way.
+__device__ __forceinline__ bool uf_by_prio(const TrackParams& P) {
+  return !P.uf_by_id && n_records(P) <= FTK_UF_PRIO_MAX;
+}
+
 // the slot mask chosen by k_clear for this call
 __device__ __forceinline__ u64 table_mask(const TrackParams& P) { return P.counters[CNT_HMASK]; }
 
@@ -158,10 +170,12 @@ __global__ void k_clear(const __grid_constant__ TrackParams P) {
 
 __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
   const i64 n = n_records(P);
+  const bool prio = uf_by_prio(P);
   const u64 hm = table_mask(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const long long key = P.fid[i];
     if (!P.prelinked) P.parent[i] = (int)i;
+    if (prio) P.lab[i] = key;
     // only faces that some cell of a neighbour cube looks up (the "upper" types) need a slot
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
     TProbe pr(P, hm, key);
@@ -206,12 +220,27 @@ __device__ __forceinline__ int uf_find(int* parent, int i) {
   }
 }
 
-__device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int b) {
+// Priority linking (uf_by_prio): roots are linked by a pseudo-random priority of their record index (the lower under
+// the higher; a parent always outranks its child, so a path is an increasing run of hashes: O(log n)
+// expected depth even when the edges of a trajectory are united concurrently) instead of by face id,
+// whose order along a trajectory (time-major) chains its records into one long path when its edges are
+// processed at once; the component minimum face id -- the label -- is then gathered at the roots
+// (k_root) instead of being the root itself
+__device__ __forceinline__ u64 uf_prio(int r) {
+  unsigned x = (unsigned)r * 0x9E3779B1u;
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return ((u64)x << 32) | (unsigned)r;  // ties broken by the index: a strict order
+}
+__device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int b, bool prio) {
   while (true) {
     a = uf_find(parent, a);
     b = uf_find(parent, b);
     if (a == b) return;
-    if (key[a] < key[b]) {
+    if (prio ? uf_prio(a) > uf_prio(b) : key[a] < key[b]) {
       const int t = a;
       a = b;
       b = t;
@@ -227,6 +256,7 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
   const i64 ne0 = (i64)P.counters[CNT_EDGES];
   const i64 ne = ne0 < P.capacity ? ne0 : P.capacity;
   const u64 hm = table_mask(P);
+  const bool prio = uf_by_prio(P);
   // Edges are visited in emission order (K1b batch order follows the scan: time-major runs of one
   // region), coalesced across the threads.  Measured alternatives -- a scattered permutation, or
   // one contiguous run per thread -- are within 15% on C2 but 3x slower on C4, where the union-find
@@ -252,7 +282,7 @@ __global__ void k_edges(const __grid_constant__ TrackParams P) {
       atomicAdd(&P.counters[CNT_INVARIANT], 1ull);  // a cell's partner face was never emitted
       continue;
     }
-    uf_unite(P.parent, P.fid, (int)a, (int)b);
+    uf_unite(P.parent, P.fid, (int)a, (int)b, prio);
   }
 }
 
@@ -272,9 +302,25 @@ __global__ void k_jump(const __grid_constant__ TrackParams P) {
 
 __global__ void k_label(const __grid_constant__ TrackParams P) {
   const i64 n = n_records(P);
+  const bool prio = uf_by_prio(P);
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    if (prio) {
+      P.rec[i].label = P.lab[P.root[i]];
+    } else {
+      const int r = uf_find(P.parent, (int)i);
+      P.rec[i].label = P.fid[r];
+    }
+  }
+}
+
+// priority linking: every record's root, and the minimum face id of each component at its root
+__global__ void k_root(const __grid_constant__ TrackParams P) {
+  if (!uf_by_prio(P)) return;
+  const i64 n = n_records(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const int r = uf_find(P.parent, (int)i);
-    P.rec[i].label = P.fid[r];
+    P.root[i] = r;
+    if (r != (int)i) atomicMin(&P.lab[r], P.fid[i]);
   }
 }
 
@@ -902,6 +948,8 @@ int launch_track(const TrackParams& P, int ndim, const i64* ext, cudaStream_t st
   k_edges<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   for (int j = 0; j < FTK_LABEL_JUMP; ++j) k_jump<<<blocks, threads, 0, stream>>>(P);
+  k_root<<<blocks, threads, 0, stream>>>(P);
+  FTK_CUDA_TRY(cudaGetLastError());
   k_label<<<blocks, threads, 0, stream>>>(P);
   FTK_CUDA_TRY(cudaGetLastError());
   if (P.verify) {

@@ -16,6 +16,9 @@ struct TrackParams {
   i64* fid;                      // [capacity] face ids of the records, written by K1 (hash keys,
                                  // union-find keys, labels)
   int* parent;                   // [capacity] union-find parents
+  long long* lab;                // [capacity] component minimum face id, kept at each root (priority linking)
+  int* root;                     // [capacity] root of each record (priority linking)
+  bool uf_by_id;                 // link by face id whatever the record count (FTK_DEBUG_UF_BY_ID)
   const long long* edges;        // [capacity][2] edges from K1
   bool verify;                   // also re-derive every face's parent cells in closed form
   unsigned long long lookup_types;  // face types (bit per type) inserted into the table: the types

@@ -127,8 +127,8 @@ def test_debug_switches_validated_on_host(ftk):
     """ftk_set_debug (the testing switches that replaced environment variables) rejects unknown bits"""
     L = ftk.lib()
     assert L.ftk_set_debug(ftk.DEBUG_FORCE_GENERIC | ftk.DEBUG_VERIFY_LINK | ftk.DEBUG_STITCH_HOST
-                           | ftk.DEBUG_NO_GRAPH) == ftk.OK
-    assert L.ftk_set_debug(16) == ftk.ERR_INVALID_ARG
+                           | ftk.DEBUG_NO_GRAPH | ftk.DEBUG_UF_BY_ID) == ftk.OK
+    assert L.ftk_set_debug(32) == ftk.ERR_INVALID_ARG
     assert L.ftk_set_debug(0) == ftk.OK
 
 

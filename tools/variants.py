@@ -21,6 +21,7 @@ VARIANTS = {
     "jump2": ["FTK_LABEL_JUMP=2"],          # pointer jumping before k_label
     "hrun128": ["FTK_HRUN=128"],            # pass-2 hash: slots probed per block before a jump
     "hrun512": ["FTK_HRUN=512"],
+    "ufkey": ["FTK_UF_PRIO=0"],              # union-find linked by face id (round-1 design)
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
