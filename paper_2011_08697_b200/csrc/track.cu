@@ -318,9 +318,10 @@ __global__ void k_root(const __grid_constant__ TrackParams P) {
   if (!uf_by_prio(P)) return;
   const i64 n = n_records(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const long long f = P.fid[i];  // loaded before the find: its latency hides behind the parent chain
     const int r = uf_find(P.parent, (int)i);
     P.root[i] = r;
-    if (r != (int)i) atomicMin(&P.lab[r], P.fid[i]);
+    if (r != (int)i) atomicMin(&P.lab[r], f);
   }
 }
 
