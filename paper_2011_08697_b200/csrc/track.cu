@@ -235,10 +235,35 @@ __device__ __forceinline__ u64 uf_prio(int r) {
   x ^= x >> 16;
   return ((u64)x << 32) | (unsigned)r;  // ties broken by the index: a strict order
 }
+// both finds of a union advanced together: the two parent chains' loads overlap instead of running
+// one after the other (the same path splitting as uf_find on each)
+__device__ __forceinline__ void uf_find2(int* parent, int& a, int& b) {
+#if FTK_CHECKS
+  long long steps = 0;
+#endif
+  while (true) {
+    const int pa = parent[a], pb = parent[b];
+    const bool ra = pa == a, rb = pb == b;
+    if (ra && rb) return;
+#if FTK_CHECKS
+    FTK_ASSERT(pa >= 0 && pb >= 0 && ++steps < (1ll << 31));
+#endif
+    const int ga = ra ? pa : parent[pa];
+    const int gb = rb ? pb : parent[pb];
+    if (!ra) {
+      if (ga != pa) parent[a] = ga;
+      a = pa;
+    }
+    if (!rb) {
+      if (gb != pb) parent[b] = gb;
+      b = pb;
+    }
+  }
+}
+
 __device__ __forceinline__ void uf_unite(int* parent, const i64* key, int a, int b, bool prio) {
   while (true) {
-    a = uf_find(parent, a);
-    b = uf_find(parent, b);
+    uf_find2(parent, a, b);
     if (a == b) return;
     if (prio ? uf_prio(a) > uf_prio(b) : key[a] < key[b]) {
       const int t = a;
