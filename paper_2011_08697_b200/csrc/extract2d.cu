@@ -1337,7 +1337,6 @@ __global__ void __launch_bounds__(EXW * 32, FTK_X_MINB) k_exact2d(const __grid_c
     uint32_t* ent = bb.ring + lane * ws_words<T>();
     bool fast = false;
     if (et != -1) {
-      const bool hasB = et < 0;
       if (inner) {
         if constexpr (sizeof(T) == 4) {
           float mx = 0.f;
