@@ -7,7 +7,7 @@ Cases: c1 (2D woven C1 track: TMA scan with its mbarrier ring, exact stage, pass
 woven, generic loader + x/y boundary tiles, heavy-noise survivors), woven3d (ragged 3D woven: the 3D
 scan's TMA ring and per-pair z exchange, k_exact3d), slabs (3 virtual time slabs through the device
 seam path: export, pack, resolve, relabel), stream (push_field_data windows), vector (2D/3D vector
-fields), post (adjacency / slice / filter / smoothing), iso (isovolume edges + cell unions).
+fields), post (adjacency / slice / filter / simplification / smoothing), iso (isovolume edges + cell unions).
 Prints one line per case; no oracle (the parity suite checks results)."""
 import os
 import sys
@@ -76,6 +76,7 @@ def post():
     rec, buf = ftk.track(f, 26, return_buffers=True)
     tj = ftk.Trajectories(rec, buf, f.shape, f.dtype, 26)
     n = len(tj.slice(5.5)) + len(tj.filter(3.0, drop_loops=True))
+    tj.simplify_types(2.0)
     tj.smooth_types(2)
     return n
 
