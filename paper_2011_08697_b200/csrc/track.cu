@@ -175,7 +175,9 @@ __global__ void k_hash_insert(const __grid_constant__ TrackParams P) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const long long key = P.fid[i];
     if (!P.prelinked) P.parent[i] = (int)i;
-    if (prio) P.lab[i] = key;
+    // a record K1 already hooked under its cube's root (a face of the same cube with a smaller face
+    // id, 2D) is never a component minimum and never a root: -1 tells k_root to skip its atomic
+    if (prio) P.lab[i] = (P.prelinked && P.parent[i] != (int)i) ? -1 : key;
     // only faces that some cell of a neighbour cube looks up (the "upper" types) need a slot
     if (!((P.lookup_types >> (int)(key % P.T)) & 1ull)) continue;
     TProbe pr(P, hm, key);
@@ -343,10 +345,10 @@ __global__ void k_root(const __grid_constant__ TrackParams P) {
   if (!uf_by_prio(P)) return;
   const i64 n = n_records(P);
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const long long f = P.fid[i];  // loaded before the find: its latency hides behind the parent chain
+    const long long f = P.lab[i];  // loaded before the find: its latency hides behind the parent chain
     const int r = uf_find(P.parent, (int)i);
     P.root[i] = r;
-    if (r != (int)i) atomicMin(&P.lab[r], f);
+    if (r != (int)i && f >= 0) atomicMin(&P.lab[r], f);
   }
 }
 
